@@ -1,0 +1,97 @@
+"""Seeded synthetic inputs for the MoE layer -- TEST INFRASTRUCTURE ONLY.
+
+Recipe follows SURVEY.md section 8(d) / the reference backbone's init:
+x ~ N(0,1); x_norm = rmsnorm(x)/sqrt(layer+1) (backbone.py:585-586,
+tensor.py:518-531); x_mod = x_norm * (1 + s2) with s2 ~ N(0, 0.1^2) per
+sample (backbone.py:587-589); t_emb ~ N(0,1); W_r ~ trunc_normal(0.006)
+(backbone.py:415); expert / shared weights ~ trunc_normal(0.02)
+(backbone.py:332-339, :394-395, :416-418).
+
+bf16 mode: the activations and expert weights are rounded to
+bf16-representable values (round-to-nearest-even) but stored as fp32 so the
+oracle (which has no bf16, tensor.py:42-47) sees exactly the values the GPU
+sees; W_r and t_emb stay fp32 so routing stays bit-comparable.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import math
+
+import numpy as np
+
+
+def trunc_normal(rng, shape, std=0.02):
+    """backbone.py:332-339 -- N(0, std) resampled until inside +-2 std."""
+    out = rng.standard_normal(shape) * std
+    bad = np.abs(out) > 2.0 * std
+    while np.any(bad):
+        out[bad] = rng.standard_normal(int(bad.sum())) * std
+        bad = np.abs(out) > 2.0 * std
+    return out
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round fp32 values to the nearest bf16 (ties to even); returns fp32."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    u = a.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def make_layer_inputs(seed: int, B: int, S: int, d: int, E: int, h: int,
+                      h_shared: int | None = None, layer: int = 3,
+                      mode: str = "fp32", expert_std: float = 0.02,
+                      router_std: float = 0.006):
+    """Returns a dict of fp32 arrays: x_norm, x_mod (B,S,d), t_emb (B,d),
+    w_r (2d,E), w1, w3 (E,h,d), w2 (E,d,h), sw1, sw3 (hs,d), sw2 (d,hs)."""
+    hs = h if h_shared is None else h_shared
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((B, S, d))
+    ms = (x * x).mean(axis=-1, keepdims=True) + 1e-6
+    x_norm = x / np.sqrt(ms) / math.sqrt(layer + 1)
+    s2 = rng.standard_normal((B, d)) * 0.1
+    x_mod = x_norm * (1.0 + s2[:, None, :])
+    t_emb = rng.standard_normal((B, d))
+    w_r = trunc_normal(rng, (2 * d, E), router_std)
+    w1 = trunc_normal(rng, (E, h, d), expert_std)
+    w3 = trunc_normal(rng, (E, h, d), expert_std)
+    w2 = trunc_normal(rng, (E, d, h), expert_std)
+    sw1 = trunc_normal(rng, (hs, d), expert_std)
+    sw3 = trunc_normal(rng, (hs, d), expert_std)
+    sw2 = trunc_normal(rng, (d, hs), expert_std)
+    out = dict(x_norm=x_norm, x_mod=x_mod, t_emb=t_emb, w_r=w_r, w1=w1, w3=w3,
+               w2=w2, sw1=sw1, sw3=sw3, sw2=sw2)
+    out = {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in out.items()}
+    if mode == "bf16":
+        for k in ("x_norm", "x_mod", "w1", "w3", "w2", "sw1", "sw3", "sw2"):
+            out[k] = bf16_round(out[k])
+    elif mode != "fp32":
+        raise ValueError(mode)
+    return out
+
+
+def make_router_inputs(seed: int, B: int, S: int, d: int, E: int,
+                       layer: int = 3, mode: str = "fp32"):
+    """Router-only inputs (same recipe, no expert weights)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((B, S, d))
+    ms = (x * x).mean(axis=-1, keepdims=True) + 1e-6
+    x_norm = (x / np.sqrt(ms) / math.sqrt(layer + 1)).astype(np.float32)
+    t_emb = rng.standard_normal((B, d)).astype(np.float32)
+    w_r = trunc_normal(rng, (2 * d, E), 0.006).astype(np.float32)
+    if mode == "bf16":
+        x_norm = bf16_round(x_norm)
+    return dict(x_norm=x_norm, t_emb=t_emb, w_r=w_r)
+
+
+def digest(arrays: dict) -> str:
+    """Stable content hash of a dict of arrays (detects generator drift)."""
+    h = hashlib.sha256()
+    for k in sorted(arrays):
+        a = np.ascontiguousarray(arrays[k])
+        h.update(k.encode())
+        h.update(str(a.dtype).encode())
+        h.update(str(a.shape).encode())
+        h.update(a.tobytes())
+    return h.hexdigest()

@@ -1,0 +1,106 @@
+"""Generate golden vectors from the REAL reference (run in the build container).
+
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+
+Imports /root/reference/pkg/src/nimg under the alias ``nimg_ref`` (it cannot
+travel to the GPU box) and runs its own public API -- router.route_full and
+moe.moe_forward (router.py:104-162, moe.py:138-164) -- on the seeded inputs
+of ``oracle.workloads``. Inputs are NOT stored (they are regenerated from the
+seed, and their sha256 is stored to detect drift); outputs are stored as
+compressed .npz fixtures in this directory.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle.workloads import digest, make_layer_inputs, make_router_inputs  # noqa: E402
+from tests.refimport import load_reference  # noqa: E402
+
+# name -> (kind, params). kind "moe" = full layer, "route" = router only.
+CASES = {
+    # d=256, E=8, h=168, C=2, S=256, B=2, fp32.
+    "cfg1_fp32": ("moe", dict(seed=0, B=2, S=256, d=256, E=8, h=168, C=2.0, mode="fp32")),
+    "cfg1_bf16": ("moe", dict(seed=1, B=2, S=256, d=256, E=8, h=168, C=2.0, mode="bf16")),
+    # non-multiple-of-tile shapes and gate_scale != 1
+    "ragged_fp32": ("moe", dict(seed=2, B=3, S=37, d=24, E=5, h=20, C=1.7, mode="fp32",
+                                gate_scale=1.7)),
+    "mid_bf16": ("moe", dict(seed=3, B=2, S=192, d=512, E=16, h=336, C=4.0, mode="bf16",
+                             layer=7)),
+    # full-width router (d=2048, E=64) on a cfg2 sub-batch: the f64-grade
+    # router accumulation is what must reproduce the fp32 logits bit-exactly.
+    "cfg2_route_fp32": ("route", dict(seed=4, B=2, S=1024, d=2048, E=64, C=4.0, mode="fp32",
+                                      layer=17)),
+    "cfg2_route_bf16": ("route", dict(seed=5, B=1, S=1024, d=2048, E=64, C=4.0, mode="bf16",
+                                      layer=17)),
+    # 1024px column length, C=2 (cap 128), one sample
+    "s4096_route_bf16": ("route", dict(seed=6, B=1, S=4096, d=2048, E=64, C=2.0, mode="bf16",
+                                       layer=17)),
+}
+
+
+def inputs_for(kind, p):
+    if kind == "moe":
+        return make_layer_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"],
+                                 layer=p.get("layer", 3), mode=p["mode"])
+    return make_router_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"],
+                              layer=p.get("layer", 3), mode=p["mode"])
+
+
+def run_reference(ref, kind, p, inp):
+    T = ref.tensor.Tensor
+    f32 = np.float32
+    cfg = ref.router.RouterConfig(d_model=p["d"], n_experts=p["E"], capacity_factor=p["C"],
+                                  gate_scale=p.get("gate_scale", 1.0))
+    with ref.tensor.no_grad():
+        if kind == "route":
+            decisions, routing = ref.router.route_full(
+                T(inp["x_norm"], dtype=f32), T(inp["t_emb"], dtype=f32),
+                T(inp["w_r"], dtype=f32), cfg)
+            out = None
+        else:
+            bank = ref.moe.ExpertBank(
+                w1=T(inp["w1"], dtype=f32), w3=T(inp["w3"], dtype=f32), w2=T(inp["w2"], dtype=f32),
+                shared_w1=T(inp["sw1"], dtype=f32), shared_w3=T(inp["sw3"], dtype=f32),
+                shared_w2=T(inp["sw2"], dtype=f32))
+            xm = T(inp["x_mod"], dtype=f32)
+            out, decisions, routing = ref.moe.moe_forward(
+                xm, T(inp["x_norm"], dtype=f32), xm, T(inp["t_emb"], dtype=f32), cfg, bank,
+                T(inp["w_r"], dtype=f32), return_routing=True)
+    res = {
+        "logits": routing["logits"].data,
+        "token_flat": np.asarray(routing["token_flat"], dtype=np.int64),
+        "gates": routing["gates"].data,
+        "top": np.stack([d.top_indices for d in decisions]),
+        "affinity": np.stack([d.affinity for d in decisions]),
+        "capacity": np.int64(routing["capacity"]),
+    }
+    if out is not None:
+        res["out"] = out.data
+    return res
+
+
+def main():
+    ref = load_reference()
+    manifest = {}
+    for name, (kind, p) in CASES.items():
+        inp = inputs_for(kind, p)
+        res = run_reference(ref, kind, p, inp)
+        res["input_digest"] = np.array(digest(inp))
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **res)
+        manifest[name] = {"kind": kind, "params": p, "input_digest": digest(inp)}
+        print(name, {k: getattr(v, "shape", None) for k, v in res.items()})
+    with open(os.path.join(HERE, "manifest.json"), "w") as f:
+        json.dump(manifest, f, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
