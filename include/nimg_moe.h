@@ -1,0 +1,141 @@
+/*
+ * nimg_moe.h -- C ABI of the B200 (sm_100a) expert-choice MoE layer.
+ *
+ * Drop-in boundary for the reference's MoE operator API
+ * (/root/reference/pkg/src/nimg). The reference is pure Python with no FFI;
+ * each entry point below replaces one reference function, cited file:line.
+ * The Python mirror (paper_2604_12163_b200/{router,moe}.py) binds these with
+ * ctypes -- see INTEGRATION.md.
+ *
+ * Conventions
+ *  - Plain C: pointers, sizes, host scalars. No torch / C++ types.
+ *  - All tensor pointers are DEVICE pointers (CUDA global memory), dense and
+ *    row-major, 16-byte aligned. Host arrays are marked "host".
+ *  - `stream` is a cudaStream_t passed as void*. Every call only enqueues work
+ *    on that stream: no allocation, no host synchronisation, capturable in a
+ *    CUDA graph. The caller owns every buffer, including the workspace.
+ *  - Return 0 on success, else an NIMG_ERR_* code; nimg_last_error() returns a
+ *    thread-local message. Codes map to the reference's exceptions:
+ *    NIMG_ERR_SHAPE -> nimg.tensor.ShapeError (tensor.py:19-20),
+ *    NIMG_ERR_CONFIG -> nimg.router.ConfigError (router.py:22-23).
+ *  - dtypes: NIMG_F32 = float32, NIMG_BF16 = bfloat16. The router weight and
+ *    the timestep embedding are always float32 (routing stays bit-exact).
+ */
+#ifndef NIMG_MOE_H_
+#define NIMG_MOE_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NIMG_OK 0
+#define NIMG_ERR_SHAPE 1
+#define NIMG_ERR_CONFIG 2
+#define NIMG_ERR_CUDA 3
+
+#define NIMG_F32 0
+#define NIMG_BF16 1
+
+#define NIMG_PATH_TCGEN05 0 /* bf16 tcgen05/TMEM/TMA grouped GEMM */
+#define NIMG_PATH_SIMT 1    /* fp32-accumulate CUDA-core grouped GEMM */
+
+/* One MoE layer problem. Mirrors RouterConfig (router.py:36-56) + ExpertBank
+ * shapes (moe.py:73-94). cap must equal capacity_for(S, E, C). */
+typedef struct nimg_moe_desc {
+  int64_t B, S, d, E, cap, h, h_shared;
+  float gate_scale; /* RouterConfig.gate_scale (alpha) */
+  float gate_eps;   /* RouterConfig.gate_eps */
+  int32_t act_dtype; /* x_norm, x_mod, expert weights and out */
+  int32_t reserved;
+} nimg_moe_desc;
+
+/* Routing results (router.py:104-162). Expert-major flat order (e, b, slot)
+ * of length E*B*cap, as the reference's routing["token_flat"]. */
+typedef struct nimg_route_out {
+  float* logits;       /* (B,S,E) fp32        routing["logits"]              */
+  float* scores_bes;   /* (B,E,S) fp32        softmax scores, expert-major   */
+  int32_t* token_flat; /* (E*B*cap) int32     routing["token_flat"]          */
+  float* gate_raw;     /* (E*B*cap) fp32      RouterDecision.affinity         */
+  float* gates;        /* (E*B*cap) fp32      routing["gates"]               */
+  int32_t* comb_rows;  /* (E,B*S) int32       per token: routed rows, expert-ascending */
+  int32_t* comb_cnt;   /* (B*S) int32         number of experts that picked the token */
+} nimg_route_out;
+
+typedef struct nimg_moe_ptrs {
+  const void* x_norm; /* (B,S,d) act: router input (unmodulated)  */
+  const void* x_mod;  /* (B,S,d) act: expert input (modulated)     */
+  const float* t_emb; /* (B,d)   fp32                               */
+  const float* w_r;   /* (2d,E)  fp32                               */
+  const void *w1, *w3, *w2;    /* (E,h,d), (E,h,d), (E,d,h) act     */
+  const void *sw1, *sw3, *sw2; /* (hs,d), (hs,d), (d,hs) act        */
+  void* out;          /* (B,S,d) act                                */
+  nimg_route_out route; /* all members required                     */
+} nimg_moe_ptrs;
+
+/* Expert FFN over explicit segments (grouped_forward, moe.py:115-135) plus an
+ * optional shared-expert bank over other rows (moe.py:160). */
+typedef struct nimg_ffn_desc {
+  int64_t n_rows;        /* rows of x_routed / y_routed            */
+  int64_t n_shared_rows; /* rows of x_shared / y_shared, 0 = none  */
+  int64_t d, h, h_shared;
+  int64_t n_experts;     /* experts in the w1/w3/w2 tensors        */
+  int32_t act_dtype;
+  int32_t nseg;          /* routed segments, <= 256                */
+} nimg_ffn_desc;
+
+/* ------------------------------------------------------------------ misc */
+const char* nimg_last_error(void);
+int nimg_abi_version(void);
+/* Number of SMs the persistent kernels size their grid by (device of stream). */
+int nimg_device_sms(int* sms);
+
+/* router.py:70-74  capacity_for(S, E, C) = min(ceil(C*S/E), S) */
+int nimg_capacity_for(int64_t S, int64_t E, double C, int64_t* cap);
+
+/* ------------------------------------------------------------------ layer */
+/* Workspace for nimg_moe_forward (bytes, 256-B aligned regions). */
+int nimg_moe_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
+/* moe.py:138-164  moe_forward: route on x_norm/t_emb, experts on x_mod,
+ * weighted combine + shared expert -> out. */
+int nimg_moe_forward(const nimg_moe_desc* desc, const nimg_moe_ptrs* ptrs, void* ws,
+                     size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ stages */
+int nimg_route_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
+/* router.py:104-162  route_full (logits, softmax, per-(b,e) top-cap,
+ * expert-major token_flat, renormalised gates) + combine tables. */
+int nimg_route(const nimg_moe_desc* desc, const void* x_norm, const float* t_emb,
+               const float* w_r, const nimg_route_out* out, void* ws, size_t ws_bytes,
+               void* stream);
+
+/* tensor.py:348-363  gather_rows: dst[i,:] = src[idx[i],:] (row_bytes each) */
+int nimg_gather_rows(const void* src, int64_t n_src_rows, int64_t row_bytes, const int32_t* idx,
+                     int64_t n_idx, void* dst, void* stream);
+
+/* Which GEMM path and which y dtype nimg_expert_ffn uses for this problem. */
+int nimg_ffn_path(const nimg_ffn_desc* desc, int32_t* path, int32_t* y_dtype);
+int nimg_ffn_workspace_bytes(const nimg_ffn_desc* desc, size_t* bytes);
+/* moe.py:115-135 grouped_forward / moe.py:31-51 swiglu: for each segment i,
+ * rows [seg_offsets[i], seg_offsets[i+1]) of x_routed go through expert
+ * seg_expert[i] (host arrays). If n_shared_rows > 0, x_shared goes through
+ * the shared expert. y dtype: see nimg_ffn_path. */
+int nimg_expert_ffn(const nimg_ffn_desc* desc, const int64_t* seg_offsets,
+                    const int32_t* seg_expert, const void* x_routed, const void* w1,
+                    const void* w3, const void* w2, void* y_routed, const void* x_shared,
+                    const void* sw1, const void* sw3, const void* sw2, void* y_shared, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* moe.py:156-161 + tensor.py:366-378: out[t] = round(f64(fp32(sum_k
+ * fp32(y_routed[rows_k] * gates[rows_k]))) + f64(y_shared[t])), experts in
+ * ascending order (deterministic; same bits for any expert-parallel split). */
+int nimg_combine(int64_t T, int64_t d, int32_t y_dtype, int32_t out_dtype, const void* y_routed,
+                 const void* y_shared, const float* gates, const int32_t* comb_rows,
+                 const int32_t* comb_cnt, void* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NIMG_MOE_H_ */

@@ -1,0 +1,96 @@
+"""ctypes binding of libnimg_moe.so (the C ABI declared in include/nimg_moe.h).
+
+There is no fallback: if the library is missing or cannot be loaded, import
+fails loudly. Build it with ``python -m paper_2604_12163_b200._build``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import ConfigError, ShapeError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnimg_moe.so")
+
+NIMG_OK, NIMG_ERR_SHAPE, NIMG_ERR_CONFIG, NIMG_ERR_CUDA = 0, 1, 2, 3
+NIMG_F32, NIMG_BF16 = 0, 1
+NIMG_PATH_TCGEN05, NIMG_PATH_SIMT = 0, 1
+
+# Every entry point the header declares (checked by tests/test_abi.py).
+EXPORTS = (
+    "nimg_last_error", "nimg_abi_version", "nimg_device_sms", "nimg_capacity_for",
+    "nimg_moe_workspace_bytes", "nimg_moe_forward", "nimg_route_workspace_bytes", "nimg_route",
+    "nimg_gather_rows", "nimg_ffn_path", "nimg_ffn_workspace_bytes", "nimg_expert_ffn",
+    "nimg_combine",
+)
+
+
+class MoeDesc(C.Structure):
+    _fields_ = [("B", C.c_int64), ("S", C.c_int64), ("d", C.c_int64), ("E", C.c_int64),
+                ("cap", C.c_int64), ("h", C.c_int64), ("h_shared", C.c_int64),
+                ("gate_scale", C.c_float), ("gate_eps", C.c_float),
+                ("act_dtype", C.c_int32), ("reserved", C.c_int32)]
+
+
+class RouteOut(C.Structure):
+    _fields_ = [("logits", C.c_void_p), ("scores_bes", C.c_void_p), ("token_flat", C.c_void_p),
+                ("gate_raw", C.c_void_p), ("gates", C.c_void_p), ("comb_rows", C.c_void_p),
+                ("comb_cnt", C.c_void_p)]
+
+
+class MoePtrs(C.Structure):
+    _fields_ = [("x_norm", C.c_void_p), ("x_mod", C.c_void_p), ("t_emb", C.c_void_p),
+                ("w_r", C.c_void_p), ("w1", C.c_void_p), ("w3", C.c_void_p), ("w2", C.c_void_p),
+                ("sw1", C.c_void_p), ("sw3", C.c_void_p), ("sw2", C.c_void_p),
+                ("out", C.c_void_p), ("route", RouteOut)]
+
+
+class FfnDesc(C.Structure):
+    _fields_ = [("n_rows", C.c_int64), ("n_shared_rows", C.c_int64), ("d", C.c_int64),
+                ("h", C.c_int64), ("h_shared", C.c_int64), ("n_experts", C.c_int64),
+                ("act_dtype", C.c_int32), ("nseg", C.c_int32)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: the CUDA extension is required (no CPU fallback). "
+            "Build it with `python -m paper_2604_12163_b200._build`.")
+    lib = C.CDLL(LIB_PATH)
+    P, I64, I32, SZ = C.c_void_p, C.c_int64, C.c_int32, C.c_size_t
+    sig = {
+        "nimg_last_error": ([], C.c_char_p),
+        "nimg_abi_version": ([], C.c_int),
+        "nimg_device_sms": ([C.POINTER(C.c_int)], C.c_int),
+        "nimg_capacity_for": ([I64, I64, C.c_double, C.POINTER(I64)], C.c_int),
+        "nimg_moe_workspace_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
+        "nimg_moe_forward": ([C.POINTER(MoeDesc), C.POINTER(MoePtrs), P, SZ, P], C.c_int),
+        "nimg_route_workspace_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
+        "nimg_route": ([C.POINTER(MoeDesc), P, P, P, C.POINTER(RouteOut), P, SZ, P], C.c_int),
+        "nimg_gather_rows": ([P, I64, I64, P, I64, P, P], C.c_int),
+        "nimg_ffn_path": ([C.POINTER(FfnDesc), C.POINTER(I32), C.POINTER(I32)], C.c_int),
+        "nimg_ffn_workspace_bytes": ([C.POINTER(FfnDesc), C.POINTER(SZ)], C.c_int),
+        "nimg_expert_ffn": ([C.POINTER(FfnDesc), P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
+                            C.c_int),
+        "nimg_combine": ([I64, I64, I32, I32, P, P, P, P, P, P, P], C.c_int),
+    }
+    for name in EXPORTS:
+        fn = getattr(lib, name)
+        fn.argtypes, fn.restype = sig[name]
+    return lib
+
+
+lib = _load()
+
+
+def check(rc: int) -> None:
+    """Raise the reference's exception type for a non-zero return code."""
+    if rc == NIMG_OK:
+        return
+    msg = lib.nimg_last_error().decode(errors="replace")
+    if rc == NIMG_ERR_SHAPE:
+        raise ShapeError(msg)
+    if rc == NIMG_ERR_CONFIG:
+        raise ConfigError(msg)
+    raise RuntimeError(f"nimg CUDA error: {msg}")

@@ -1,0 +1,472 @@
+// C-ABI layer (include/nimg_moe.h): validation, workspace carving, TMA
+// descriptor encoding and stream-ordered launch sequencing. No allocation and
+// no host synchronisation happen here.
+#include <cudaTypedefs.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/nimg_moe.h"
+#include "nimg_internal.h"
+
+using namespace nimg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess)                                                                 \
+      return fail(NIMG_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));         \
+  } while (0)
+
+#define NIMG_TRY(expr)        \
+  do {                        \
+    int _r = (expr);          \
+    if (_r != NIMG_OK) return _r; \
+  } while (0)
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+inline size_t elt(int32_t dt) { return dt == NIMG_BF16 ? 2 : 4; }
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// ------------------------------------------------------------- tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// bf16 [rows, K] row-major, box (64 x box_rows), 128-B swizzle.
+int map_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(NIMG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {K, rows};
+  cuuint64_t strides[1] = {K * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NIMG_ERR_CUDA, "tensor map 2d encode failed (%d)", (int)r);
+  return NIMG_OK;
+}
+// bf16 [E, N, K] row-major, box (64 x box_rows x 1), 128-B swizzle.
+int map_3d(CUtensorMap* m, const void* base, uint64_t E, uint64_t N, uint64_t K,
+           uint32_t box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(NIMG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {K, N, E};
+  cuuint64_t strides[2] = {K * 2, N * K * 2};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NIMG_ERR_CUDA, "tensor map 3d encode failed (%d)", (int)r);
+  return NIMG_OK;
+}
+
+int device_sms(int* out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  static int cache[64] = {0};
+  if (dev < 64 && cache[dev]) { *out = cache[dev]; return NIMG_OK; }
+  int n = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  if (dev < 64) cache[dev] = n;
+  *out = n;
+  return NIMG_OK;
+}
+
+// ------------------------------------------------------------- validation
+int check_moe_desc(const nimg_moe_desc* d) {
+  if (!d) return fail(NIMG_ERR_CONFIG, "null descriptor");
+  if (d->act_dtype != NIMG_F32 && d->act_dtype != NIMG_BF16)
+    return fail(NIMG_ERR_CONFIG, "unsupported act_dtype %d", d->act_dtype);
+  if (d->B < 1 || d->S < 1 || d->d < 1 || d->h < 1 || d->h_shared < 1)
+    return fail(NIMG_ERR_SHAPE, "empty dimension B=%lld S=%lld d=%lld h=%lld hs=%lld",
+                (long long)d->B, (long long)d->S, (long long)d->d, (long long)d->h,
+                (long long)d->h_shared);
+  if (d->E < 1) return fail(NIMG_ERR_CONFIG, "n_experts must be >= 1");     // router.py:45-46
+  if (!(d->gate_eps > 0.f)) return fail(NIMG_ERR_CONFIG, "gate_eps must be > 0");  // router.py:49-50
+  if (d->cap < 1) return fail(NIMG_ERR_CONFIG, "computed capacity is zero");  // router.py:117-118
+  if (d->cap > d->S) return fail(NIMG_ERR_CONFIG, "capacity %lld > S %lld", (long long)d->cap, (long long)d->S);
+  if (d->E > 512) return fail(NIMG_ERR_CONFIG, "n_experts %lld > 512 unsupported", (long long)d->E);
+  if (d->S > 16384) return fail(NIMG_ERR_CONFIG, "S %lld > 16384 unsupported", (long long)d->S);
+  if (d->cap > 4096) return fail(NIMG_ERR_CONFIG, "capacity %lld > 4096 unsupported", (long long)d->cap);
+  const int64_t T = d->B * d->S;
+  if (d->E * d->B * d->cap >= (int64_t)1 << 31 || T * d->E >= (int64_t)1 << 31)
+    return fail(NIMG_ERR_CONFIG, "problem too large for int32 row indices");
+  return NIMG_OK;
+}
+
+struct RouteWs {
+  double* tb;
+  int16_t* slot_of;
+};
+size_t route_ws_bytes(const nimg_moe_desc* d) {
+  return align_up((size_t)d->B * d->E * 8) + align_up((size_t)d->E * d->B * d->S * 2);
+}
+RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
+  uint8_t* p = static_cast<uint8_t*>(ws);
+  RouteWs r;
+  r.tb = reinterpret_cast<double*>(p);
+  p += align_up((size_t)d->B * d->E * 8);
+  r.slot_of = reinterpret_cast<int16_t*>(p);
+  return r;
+}
+
+bool ffn_use_tc(const nimg_ffn_desc* f) {
+  if (f->act_dtype != NIMG_BF16) return false;
+  if (f->d % 16 || f->h % 16) return false;
+  if (f->n_shared_rows > 0 && f->h_shared % 16) return false;
+  return true;
+}
+size_t ffn_ws_bytes(const nimg_ffn_desc* f) {
+  const size_t e = ffn_use_tc(f) ? 2 : 4;
+  return align_up((size_t)f->n_rows * f->h * e) + align_up((size_t)f->n_shared_rows * f->h_shared * e);
+}
+
+template <class P>
+int fill_segments(P& p, const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex, int bm,
+                  int ntn0, int ntn1) {
+  int64_t tiles = 0;
+  int n = 0;
+  for (int i = 0; i < f->nseg; ++i, ++n) {
+    const int64_t rows = off[i + 1] - off[i];
+    p.seg_row0[n] = (int)off[i];
+    p.seg_rows[n] = (int)rows;
+    p.seg_expert[n] = ex ? ex[i] : i;
+    p.seg_tile0[n] = (int)tiles;
+    tiles += (rows + bm - 1) / bm * ntn0;
+  }
+  p.nseg0 = n;
+  if (f->n_shared_rows > 0) {
+    p.seg_row0[n] = 0;
+    p.seg_rows[n] = (int)f->n_shared_rows;
+    p.seg_expert[n] = 0;
+    p.seg_tile0[n] = (int)tiles;
+    tiles += (f->n_shared_rows + bm - 1) / bm * ntn1;
+    ++n;
+  }
+  p.nseg = n;
+  p.seg_tile0[n] = (int)tiles;
+  if (tiles >= ((int64_t)1 << 31)) return fail(NIMG_ERR_CONFIG, "too many tiles");
+  p.total_tiles = (int)tiles;
+  return NIMG_OK;
+}
+
+int check_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex) {
+  if (!f) return fail(NIMG_ERR_CONFIG, "null descriptor");
+  if (f->act_dtype != NIMG_F32 && f->act_dtype != NIMG_BF16)
+    return fail(NIMG_ERR_CONFIG, "unsupported act_dtype %d", f->act_dtype);
+  if (f->nseg < 0 || f->nseg > kMaxSeg - 8)
+    return fail(NIMG_ERR_CONFIG, "nseg %d outside [0, %d]", f->nseg, kMaxSeg - 8);
+  if (f->d < 1 || f->h < 1 || (f->n_shared_rows > 0 && f->h_shared < 1))
+    return fail(NIMG_ERR_SHAPE, "empty feature dimension");
+  if (f->n_rows < 0 || f->n_shared_rows < 0 || f->n_rows >= ((int64_t)1 << 31) ||
+      f->n_shared_rows >= ((int64_t)1 << 31))
+    return fail(NIMG_ERR_SHAPE, "row count out of range");
+  if (f->nseg > 0) {
+    if (!off) return fail(NIMG_ERR_SHAPE, "null offsets");
+    // GroupedBatch validation (moe.py:105-112)
+    if (off[0] != 0) return fail(NIMG_ERR_SHAPE, "invalid offsets: offsets[0] != 0");
+    for (int i = 0; i < f->nseg; ++i)
+      if (off[i + 1] < off[i]) return fail(NIMG_ERR_SHAPE, "invalid offsets: decreasing at %d", i);
+    if (off[f->nseg] != f->n_rows)
+      return fail(NIMG_ERR_SHAPE, "offsets end %lld != token count %lld", (long long)off[f->nseg],
+                  (long long)f->n_rows);
+    for (int i = 0; i < f->nseg; ++i) {
+      const int e = ex ? ex[i] : i;
+      if (e < 0 || e >= f->n_experts) return fail(NIMG_ERR_SHAPE, "segment %d expert %d out of range", i, e);
+    }
+  } else if (f->n_rows != 0) {
+    return fail(NIMG_ERR_SHAPE, "rows without segments");
+  }
+  return NIMG_OK;
+}
+
+int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex,
+                    const void* xr, const void* w1, const void* w3, const void* w2, void* yr,
+                    const void* xs, const void* sw1, const void* sw3, const void* sw2, void* ys,
+                    void* ws, size_t ws_bytes, cudaStream_t st) {
+  NIMG_TRY(check_ffn(f, off, ex));
+  if (ws_bytes < ffn_ws_bytes(f)) return fail(NIMG_ERR_CONFIG, "workspace too small");
+  const bool has_r = f->n_rows > 0, has_s = f->n_shared_rows > 0;
+  if (!has_r && !has_s) return NIMG_OK;
+  if ((has_r && (!xr || !w1 || !w3 || !w2 || !yr)) || (has_s && (!xs || !sw1 || !sw3 || !sw2 || !ys)))
+    return fail(NIMG_ERR_SHAPE, "null tensor pointer");
+  const bool tc = ffn_use_tc(f);
+  const size_t e = tc ? 2 : 4;
+  uint8_t* pre_r = static_cast<uint8_t*>(ws);
+  uint8_t* pre_s = pre_r + align_up((size_t)f->n_rows * f->h * e);
+  const int d = (int)f->d, h = (int)f->h, hs = (int)(has_s ? f->h_shared : f->h);
+
+  if (tc) {
+    const void* ptrs[] = {xr, w1, w3, w2, yr, xs, sw1, sw3, sw2, ys, pre_r, pre_s};
+    for (const void* q : ptrs)
+      if (q && !aligned16(q)) return fail(NIMG_ERR_SHAPE, "tensor not 16-byte aligned");
+    int sms = 0;
+    NIMG_TRY(device_sms(&sms));
+    // GEMM1: pre = SiLU(x W1^T) * (x W3^T)
+    {
+      GroupedParams p;
+      memset(&p, 0, sizeof(p));
+      const int bn = tc_bn_out(0), box = tc_b_box(0);
+      NIMG_TRY(fill_segments(p, f, off, ex, 128, (h + bn - 1) / bn, (hs + bn - 1) / bn));
+      TmapSet tm;
+      memset(&tm, 0, sizeof(tm));
+      const int rb = has_r ? 0 : 1;  // any valid bank to alias an unused one
+      if (has_r) {
+        NIMG_TRY(map_2d(&tm.a[0], xr, f->n_rows, d, 128));
+        NIMG_TRY(map_3d(&tm.b[0], w1, f->n_experts, h, d, box));
+        NIMG_TRY(map_3d(&tm.b3[0], w3, f->n_experts, h, d, box));
+      }
+      if (has_s) {
+        NIMG_TRY(map_2d(&tm.a[1], xs, f->n_shared_rows, d, 128));
+        NIMG_TRY(map_3d(&tm.b[1], sw1, 1, hs, d, box));
+        NIMG_TRY(map_3d(&tm.b3[1], sw3, 1, hs, d, box));
+      }
+      if (!has_r) { tm.a[0] = tm.a[1]; tm.b[0] = tm.b[1]; tm.b3[0] = tm.b3[1]; }
+      if (!has_s) { tm.a[1] = tm.a[rb]; tm.b[1] = tm.b[rb]; tm.b3[1] = tm.b3[rb]; }
+      p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0};
+      p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0};
+      CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
+    }
+    // GEMM2: y = pre W2^T
+    {
+      GroupedParams p;
+      memset(&p, 0, sizeof(p));
+      const int bn = tc_bn_out(1), box = tc_b_box(1);
+      NIMG_TRY(fill_segments(p, f, off, ex, 128, (d + bn - 1) / bn, (d + bn - 1) / bn));
+      TmapSet tm;
+      memset(&tm, 0, sizeof(tm));
+      if (has_r) {
+        NIMG_TRY(map_2d(&tm.a[0], pre_r, f->n_rows, h, 128));
+        NIMG_TRY(map_3d(&tm.b[0], w2, f->n_experts, d, h, box));
+      }
+      if (has_s) {
+        NIMG_TRY(map_2d(&tm.a[1], pre_s, f->n_shared_rows, hs, 128));
+        NIMG_TRY(map_3d(&tm.b[1], sw2, 1, d, hs, box));
+      }
+      if (!has_r) { tm.a[0] = tm.a[1]; tm.b[0] = tm.b[1]; }
+      if (!has_s) { tm.a[1] = tm.a[0]; tm.b[1] = tm.b[0]; }
+      tm.b3[0] = tm.b[0];
+      tm.b3[1] = tm.b[1];
+      p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0};
+      p.bank[1] = GBank{ys, d, hs, d, (d + bn - 1) / bn, 0};
+      CUDA_TRY(launch_grouped_tc(1, tm, p, sms, st));
+    }
+    return NIMG_OK;
+  }
+
+  // SIMT path: fp32 pre / y
+  const bool bf = f->act_dtype == NIMG_BF16;
+  const int bm = simt_bm(), bn = simt_bn();
+  {
+    SimtParams p;
+    memset(&p, 0, sizeof(p));
+    NIMG_TRY(fill_segments(p, f, off, ex, bm, (h + bn - 1) / bn, (hs + bn - 1) / bn));
+    p.bank[0] = SimtBank{xr, d, w1, w3, reinterpret_cast<float*>(pre_r), h, d, h, (h + bn - 1) / bn, 0};
+    p.bank[1] = SimtBank{xs, d, sw1, sw3, reinterpret_cast<float*>(pre_s), hs, d, hs, (hs + bn - 1) / bn, 0};
+    CUDA_TRY(launch_grouped_simt(0, bf, p, st));
+  }
+  {
+    SimtParams p;
+    memset(&p, 0, sizeof(p));
+    NIMG_TRY(fill_segments(p, f, off, ex, bm, (d + bn - 1) / bn, (d + bn - 1) / bn));
+    p.bank[0] = SimtBank{pre_r, h, w2, nullptr, reinterpret_cast<float*>(yr), d, h, d, (d + bn - 1) / bn, 0};
+    p.bank[1] = SimtBank{pre_s, hs, sw2, nullptr, reinterpret_cast<float*>(ys), d, hs, d, (d + bn - 1) / bn, 0};
+    CUDA_TRY(launch_grouped_simt(1, bf, p, st));
+  }
+  return NIMG_OK;
+}
+
+int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, const float* w_r,
+               const nimg_route_out* o, void* ws, size_t ws_bytes, cudaStream_t st) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!o || !o->logits || !o->scores_bes || !o->token_flat || !o->gate_raw || !o->gates ||
+      !o->comb_rows || !o->comb_cnt)
+    return fail(NIMG_ERR_SHAPE, "null routing output pointer");
+  if (!x_norm || !t_emb || !w_r) return fail(NIMG_ERR_SHAPE, "null input pointer");
+  if (!ws || ws_bytes < route_ws_bytes(d)) return fail(NIMG_ERR_CONFIG, "workspace too small");
+  const int B = (int)d->B, S = (int)d->S, dd = (int)d->d, E = (int)d->E, cap = (int)d->cap;
+  const int64_t T = d->B * d->S;
+  RouteWs w = carve_route(d, ws);
+  CUDA_TRY(launch_router_tbias(t_emb, w_r, w.tb, B, dd, E, st));
+  CUDA_TRY(launch_router_scores(d->act_dtype == NIMG_BF16, x_norm, w_r, w.tb, o->logits,
+                                o->scores_bes, B, S, dd, E, st));
+  CUDA_TRY(cudaMemsetAsync(w.slot_of, 0xFF, (size_t)E * T * 2, st));
+  CUDA_TRY(launch_ec_select(o->scores_bes, o->token_flat, o->gate_raw, w.slot_of, B, S, E, cap, st));
+  // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
+  CUDA_TRY(launch_gate_norm(o->scores_bes, w.slot_of, o->gates, o->comb_rows, o->comb_cnt, B, S,
+                            E, cap, d->gate_eps, d->gate_scale, st));
+  return NIMG_OK;
+}
+
+nimg_ffn_desc layer_ffn_desc(const nimg_moe_desc* d) {
+  nimg_ffn_desc f;
+  memset(&f, 0, sizeof(f));
+  f.n_rows = d->E * d->B * d->cap;
+  f.n_shared_rows = d->B * d->S;
+  f.d = d->d;
+  f.h = d->h;
+  f.h_shared = d->h_shared;
+  f.n_experts = d->E;
+  f.act_dtype = d->act_dtype;
+  f.nseg = (int32_t)d->E;
+  return f;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* nimg_last_error(void) { return g_err.c_str(); }
+int nimg_abi_version(void) { return 1; }
+int nimg_device_sms(int* sms) {
+  if (!sms) return fail(NIMG_ERR_CONFIG, "null output");
+  return device_sms(sms);
+}
+
+int nimg_capacity_for(int64_t S, int64_t E, double C, int64_t* cap) {
+  if (!cap) return fail(NIMG_ERR_CONFIG, "null output");
+  if (S < 1 || E < 1 || !(C > 0))
+    return fail(NIMG_ERR_CONFIG, "invalid capacity arguments S=%lld E=%lld C=%g", (long long)S,
+                (long long)E, C);
+  const int64_t c = (int64_t)std::ceil(C * (double)S / (double)E);  // router.py:74 order
+  *cap = c < S ? c : S;
+  return NIMG_OK;
+}
+
+int nimg_route_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");
+  *bytes = route_ws_bytes(d);
+  return NIMG_OK;
+}
+
+int nimg_route(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, const float* w_r,
+               const nimg_route_out* out, void* ws, size_t ws_bytes, void* stream) {
+  return route_impl(d, x_norm, t_emb, w_r, out, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int nimg_gather_rows(const void* src, int64_t n_src_rows, int64_t row_bytes, const int32_t* idx,
+                     int64_t n_idx, void* dst, void* stream) {
+  if (n_idx < 0 || row_bytes < 0 || n_src_rows < 0) return fail(NIMG_ERR_SHAPE, "negative size");
+  if (n_idx == 0 || row_bytes == 0) return NIMG_OK;
+  if (!src || !idx || !dst) return fail(NIMG_ERR_SHAPE, "null pointer");
+  CUDA_TRY(launch_gather_rows(src, row_bytes, idx, n_idx, dst, (cudaStream_t)stream));
+  return NIMG_OK;
+}
+
+int nimg_ffn_path(const nimg_ffn_desc* f, int32_t* path, int32_t* y_dtype) {
+  if (!f || !path || !y_dtype) return fail(NIMG_ERR_CONFIG, "null argument");
+  const bool tc = ffn_use_tc(f);
+  *path = tc ? NIMG_PATH_TCGEN05 : NIMG_PATH_SIMT;
+  *y_dtype = tc ? NIMG_BF16 : NIMG_F32;
+  return NIMG_OK;
+}
+
+int nimg_ffn_workspace_bytes(const nimg_ffn_desc* f, size_t* bytes) {
+  if (!f || !bytes) return fail(NIMG_ERR_CONFIG, "null argument");
+  *bytes = ffn_ws_bytes(f);
+  return NIMG_OK;
+}
+
+int nimg_expert_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex, const void* xr,
+                    const void* w1, const void* w3, const void* w2, void* yr, const void* xs,
+                    const void* sw1, const void* sw3, const void* sw2, void* ys, void* ws,
+                    size_t ws_bytes, void* stream) {
+  return expert_ffn_impl(f, off, ex, xr, w1, w3, w2, yr, xs, sw1, sw3, sw2, ys, ws, ws_bytes,
+                         (cudaStream_t)stream);
+}
+
+int nimg_combine(int64_t T, int64_t d, int32_t y_dtype, int32_t out_dtype, const void* y_routed,
+                 const void* y_shared, const float* gates, const int32_t* comb_rows,
+                 const int32_t* comb_cnt, void* out, void* stream) {
+  if (T < 0 || d < 1) return fail(NIMG_ERR_SHAPE, "bad combine shape");
+  if (T == 0) return NIMG_OK;
+  if (!y_shared || !comb_cnt || !comb_rows || !out || !gates)
+    return fail(NIMG_ERR_SHAPE, "null pointer");
+  CUDA_TRY(launch_combine(y_dtype == NIMG_BF16, out_dtype == NIMG_BF16, y_routed, y_shared, gates,
+                          comb_rows, comb_cnt, out, T, (int)d, (cudaStream_t)stream));
+  return NIMG_OK;
+}
+
+int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");
+  const nimg_ffn_desc f = layer_ffn_desc(d);
+  int32_t path, ydt;
+  nimg_ffn_path(&f, &path, &ydt);
+  *bytes = route_ws_bytes(d) + align_up((size_t)f.n_rows * d->d * elt(d->act_dtype)) +
+           ffn_ws_bytes(&f) + align_up((size_t)f.n_rows * d->d * elt(ydt)) +
+           align_up((size_t)f.n_shared_rows * d->d * elt(ydt));
+  return NIMG_OK;
+}
+
+int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, size_t ws_bytes,
+                     void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  NIMG_TRY(check_moe_desc(d));
+  if (!p) return fail(NIMG_ERR_SHAPE, "null pointers");
+  size_t need = 0;
+  NIMG_TRY(nimg_moe_workspace_bytes(d, &need));
+  if (!ws || ws_bytes < need) return fail(NIMG_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  const nimg_ffn_desc f = layer_ffn_desc(d);
+  int32_t path, ydt;
+  nimg_ffn_path(&f, &path, &ydt);
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  void* route_ws = w;                 w += route_ws_bytes(d);
+  void* xg = w;                       w += align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
+  void* ffn_ws = w;                   w += ffn_ws_bytes(&f);
+  void* yr = w;                       w += align_up((size_t)f.n_rows * d->d * elt(ydt));
+  void* ys = w;
+
+  NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st));
+  CUDA_TRY(launch_gather_rows(p->x_mod, d->d * (int64_t)elt(d->act_dtype), p->route.token_flat,
+                              f.n_rows, xg, st));
+  int64_t off[kMaxSeg + 1];
+  if (f.nseg > kMaxSeg - 8) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
+  for (int e = 0; e <= f.nseg; ++e) off[e] = (int64_t)e * d->B * d->cap;  // moe.py:154
+  NIMG_TRY(expert_ffn_impl(&f, off, nullptr, xg, p->w1, p->w3, p->w2, yr, p->x_mod, p->sw1,
+                           p->sw3, p->sw2, ys, ffn_ws, ffn_ws_bytes(&f), st));
+  CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys, p->route.gates,
+                          p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d, st));
+  return NIMG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,257 @@
+// Grouped SwiGLU expert GEMMs on 5th-gen tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces the per-expert loop of grouped_forward / swiglu
+// (reference moe.py:115-135, moe.py:31-51): every routed expert segment (and
+// the shared expert, moe.py:160, as a second weight "bank") is one row group
+// of a persistent, warp-specialised kernel.
+//
+//   MODE 0 (GEMM1): pre[r, n] = SiLU(x W1^T) * (x W3^T)   -- dual-B tile: the
+//       W1 and W3 slices of one N block sit back to back in shared memory and
+//       one UMMA (M=128, N=2*112) accumulates both halves into TMEM; the
+//       epilogue applies SiLU*mul and writes bf16 `pre`.
+//   MODE 1 (GEMM2): y[r, n] = pre W2^T                     -- UMMA M=128, N=256.
+//
+// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA
+// issuer (one thread), warps 2..5 = epilogue (TMEM -> registers -> global).
+// Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a 2-deep TMEM
+// accumulator ring (tmem_full/tmem_empty), so the epilogue of tile i overlaps
+// the MMAs of tile i+1.
+#include "common.cuh"
+#include "nimg_internal.h"
+
+namespace nimg {
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 64;                    // 64 bf16 = one 128-B swizzle row
+constexpr int kThreads = 192;
+constexpr int kATileBytes = BM * BK * 2;  // 16 KB
+
+template <int MODE> struct Cfg;
+template <> struct Cfg<0> {
+  static constexpr int BN_OUT = 112;                 // output columns per tile
+  static constexpr int BN_MMA = 224;                 // W1 half + W3 half
+  static constexpr int B_BOX = 112;                  // rows per TMA box (each of W1, W3)
+  static constexpr int STAGES = 4;
+  static constexpr int kBTileBytes = BN_MMA * BK * 2;  // 28 KB
+};
+template <> struct Cfg<1> {
+  static constexpr int BN_OUT = 256;
+  static constexpr int BN_MMA = 256;
+  static constexpr int B_BOX = 256;
+  static constexpr int STAGES = 4;
+  static constexpr int kBTileBytes = BN_MMA * BK * 2;  // 32 KB
+};
+
+template <int MODE>
+constexpr int stage_bytes() { return kATileBytes + Cfg<MODE>::kBTileBytes; }
+template <int MODE>
+constexpr int smem_bytes() { return Cfg<MODE>::STAGES * stage_bytes<MODE>() + 1024 + 256; }
+
+struct TileInfo {
+  int bank, expert, a_row, rows_valid, n0, nk;
+};
+
+template <int MODE>
+NIMG_DEV void decode_tile(const GroupedParams& p, int t, TileInfo& ti) {
+  int lo = 0, hi = p.nseg - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p.seg_tile0[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const int bank = lo >= p.nseg0 ? 1 : 0;
+  const int ntn = p.bank[bank].ntn;
+  const int local = t - p.seg_tile0[lo];
+  const int m_blk = local / ntn;
+  const int n_blk = local - m_blk * ntn;
+  ti.bank = bank;
+  ti.expert = p.seg_expert[lo];
+  ti.a_row = p.seg_row0[lo] + m_blk * BM;
+  ti.rows_valid = min(BM, p.seg_rows[lo] - m_blk * BM);
+  ti.n0 = n_blk * Cfg<MODE>::BN_OUT;
+  ti.nk = (p.bank[bank].K + BK - 1) / BK;
+}
+
+NIMG_DEV float silu_mul(float a, float g) { return a / (1.0f + __expf(-a)) * g; }
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1)
+grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ GroupedParams p) {
+  using C = Cfg<MODE>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int SB = stage_bytes<MODE>();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+    fence_barrier_init();
+    for (int b = 0; b < 2; ++b) {
+      tma_prefetch_desc(&tm.a[b]);
+      tma_prefetch_desc(&tm.b[b]);
+      if (MODE == 0) tma_prefetch_desc(&tm.b3[b]);
+    }
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        TileInfo ti; decode_tile<MODE>(p, t, ti);
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SB;
+          uint8_t* sb = sa + kATileBytes;
+          mbar_arrive_expect_tx(&full[stage], SB);
+          tma_load_2d(sa, &tm.a[ti.bank], &full[stage], kb * BK, ti.a_row);
+          tma_load_3d(sb, &tm.b[ti.bank], &full[stage], kb * BK, ti.n0, ti.expert);
+          if (MODE == 0)
+            tma_load_3d(sb + C::B_BOX * BK * 2, &tm.b3[ti.bank], &full[stage], kb * BK, ti.n0,
+                        ti.expert);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = make_idesc_bf16(BM, C::BN_MMA);
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+        TileInfo ti; decode_tile<MODE>(p, t, ti);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * SB);
+          const uint32_t sb = sa + kATileBytes;
+          const uint64_t adesc = make_sdesc_k128(sa);
+          const uint64_t bdesc = make_sdesc_k128(sb);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // +32 B per K=16 step inside the 128-B swizzle atom (>>4 => +2)
+            umma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;            // TMEM lane quadrant this warp may access
+    const int r = q * 32 + lane;       // tile row == TMEM lane
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      TileInfo ti; decode_tile<MODE>(p, t, ti);
+      const GBank& bk = p.bank[ti.bank];
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const bool rv = r < ti.rows_valid;
+      bf16* orow = reinterpret_cast<bf16*>(bk.out) + (int64_t)(ti.a_row + r) * bk.out_ld + ti.n0;
+      if (MODE == 0) {
+#pragma unroll 1
+        for (int c = 0; c < C::BN_OUT / 16; ++c) {
+          uint32_t a[16], g[16];
+          tmem_ld16(tb + c * 16, a);
+          tmem_ld16(tb + C::B_BOX + c * 16, g);
+          tmem_ld_wait();
+          if (rv && ti.n0 + c * 16 < bk.N) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              pk[j] = pack_bf16x2(silu_mul(__uint_as_float(a[2 * j]), __uint_as_float(g[2 * j])),
+                                  silu_mul(__uint_as_float(a[2 * j + 1]), __uint_as_float(g[2 * j + 1])));
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < C::BN_OUT / 16; ++c) {
+          uint32_t a[16];
+          tmem_ld16(tb + c * 16, a);
+          tmem_ld_wait();
+          if (rv && ti.n0 + c * 16 < bk.N) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              pk[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------------ host side
+int tc_bn_out(int mode) { return mode == 0 ? tc::Cfg<0>::BN_OUT : tc::Cfg<1>::BN_OUT; }
+int tc_b_box(int mode) { return mode == 0 ? tc::Cfg<0>::B_BOX : tc::Cfg<1>::B_BOX; }
+
+cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& p, int num_sms,
+                              cudaStream_t stream) {
+  if (p.total_tiles <= 0) return cudaSuccess;
+  const int grid = p.total_tiles < num_sms ? p.total_tiles : num_sms;
+  if (mode == 0) {
+    constexpr int smem = tc::smem_bytes<0>();
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100<0>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    tc::grouped_gemm_sm100<0><<<grid, tc::kThreads, smem, stream>>>(tm, p);
+  } else {
+    constexpr int smem = tc::smem_bytes<1>();
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100<1>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    tc::grouped_gemm_sm100<1><<<grid, tc::kThreads, smem, stream>>>(tm, p);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace nimg

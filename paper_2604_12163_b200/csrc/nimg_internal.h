@@ -1,0 +1,89 @@
+// Internal (C++) declarations shared by the kernel translation units and the
+// C-ABI layer. Nothing here is part of the public ABI (include/nimg_moe.h).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace nimg {
+
+constexpr int kMaxSeg = 264;  // routed segments + shared; EP: R * E/R + 1
+
+// One weight bank of a grouped launch: bank 0 = routed experts (3-D weights
+// [E, N, K]), bank 1 = the shared expert (3-D with E = 1).
+struct GBank {
+  void* out;       // output rows (bank-local row index), row stride out_ld elements
+  int64_t out_ld;
+  int K;           // reduction length (d for GEMM1, h for GEMM2)
+  int N;           // output columns (h for GEMM1, d for GEMM2)
+  int ntn;         // N tiles
+  int pad_;
+};
+
+// Segments [0, nseg0) use bank 0, [nseg0, nseg) bank 1. Segment i covers rows
+// [seg_row0[i], seg_row0[i] + seg_rows[i]) of its bank's A / out tensors and
+// multiplies them by expert seg_expert[i] of that bank.
+struct GroupedParams {
+  GBank bank[2];
+  int nseg0, nseg, total_tiles, pad_;
+  int seg_tile0[kMaxSeg + 1];
+  int seg_row0[kMaxSeg];
+  int seg_rows[kMaxSeg];
+  int seg_expert[kMaxSeg];
+};
+
+struct __align__(64) TmapSet {
+  CUtensorMap a[2];   // A operand per bank: 2-D [rows, K]
+  CUtensorMap b[2];   // B operand per bank: 3-D [E, N, K] (W1 for GEMM1, W2 for GEMM2)
+  CUtensorMap b3[2];  // GEMM1 only: W3
+};
+
+// SIMT (CUDA-core) grouped path: fp32 parity mode and shapes the TMA path
+// cannot take. Pointers instead of tensor maps.
+struct SimtBank {
+  const void* a;     // [rows, K] activations (T_IN)
+  int64_t a_ld;
+  const void* w;     // [E, N, K]   (W1 or W2)
+  const void* w3;    // [E, N, K]   (W3, GEMM1 only)
+  float* out;        // [rows, N] fp32
+  int64_t out_ld;
+  int K, N, ntn, pad_;
+};
+struct SimtParams {
+  SimtBank bank[2];
+  int nseg0, nseg, total_tiles, pad_;
+  int seg_tile0[kMaxSeg + 1];
+  int seg_row0[kMaxSeg];
+  int seg_rows[kMaxSeg];
+  int seg_expert[kMaxSeg];
+};
+
+int tc_bn_out(int mode);
+int tc_b_box(int mode);
+cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& p, int num_sms,
+                              cudaStream_t stream);
+// in_bf16: activations/weights dtype (bf16 vs fp32); GEMM2 reads fp32 `pre`.
+int simt_bm();
+int simt_bn();
+cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream);
+
+// routing / data-movement kernels (route_kernels.cu)
+cudaError_t launch_router_tbias(const float* t_emb, const float* w_r, double* tb, int B, int d,
+                                int E, cudaStream_t s);
+cudaError_t launch_router_scores(bool x_bf16, const void* x_norm, const float* w_r,
+                                 const double* tb, float* logits, float* scores_bes, int B, int S,
+                                 int d, int E, cudaStream_t s);
+cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
+                             int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s);
+cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,
+                             int32_t* comb_rows, int32_t* comb_cnt, int B, int S, int E, int cap,
+                             float gate_eps, float gate_scale, cudaStream_t s);
+cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
+                               int64_t n_idx, void* dst, cudaStream_t s);
+// out[t] = fp32(fp32(sum_k fp32(Y[rows[k][t]] * gate)) + shared[t]) -- see combine kernel.
+cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
+                           const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
+                           void* out, int64_t T, int d, cudaStream_t s);
+
+}  // namespace nimg

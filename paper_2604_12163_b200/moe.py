@@ -1,0 +1,185 @@
+"""Sparse expert computation -- B200 operator API.
+
+Mirrors /root/reference/pkg/src/nimg/moe.py (names, dataclasses, argument
+meaning, exceptions). The whole layer -- routing, gather, the grouped SwiGLU
+GEMMs (tcgen05 in bf16, CUDA cores in fp32), the deterministic weighted
+combine and the shared expert -- is one call into libnimg_moe.so
+(`nimg_moe_forward`); grouped_forward / swiglu call `nimg_expert_ffn`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._tensors import nimg_dtype, ptr, stream_handle, to_device, workspace
+from .errors import ConfigError, ShapeError
+from .router import (RouterConfig, alloc_route_out, build_routing, capacity_for, make_desc,
+                     route_full, route_struct)
+
+__all__ = ["ShapeError", "swiglu", "swiglu_arrays", "swiglu_composed", "ExpertBank",
+           "GroupedBatch", "grouped_forward", "moe_forward"]
+
+
+@dataclass
+class ExpertBank:
+    """moe.py:73-94 -- routed expert weights plus the always-on shared expert.
+    w1, w3: (E, h, d); w2: (E, d, h); shared_w1/w3: (hs, d); shared_w2: (d, hs)."""
+    w1: object
+    w3: object
+    w2: object
+    shared_w1: object
+    shared_w3: object
+    shared_w2: object
+
+    @property
+    def n_experts(self) -> int:
+        return self.w1.shape[0]
+
+    def expert_weights(self, e: int):
+        return self.w1[e], self.w3[e], self.w2[e]
+
+    def on_device(self, dtype: torch.dtype) -> "ExpertBank":
+        """Device copies in the kernel dtype (no copy if already there)."""
+        return ExpertBank(*(to_device(w, dtype) for w in (self.w1, self.w3, self.w2, self.shared_w1,
+                                                          self.shared_w3, self.shared_w2)))
+
+
+@dataclass
+class GroupedBatch:
+    """moe.py:97-112 -- expert-concatenated rows with prefix-sum offsets."""
+    tokens: object            # (N_total, d)
+    offsets: np.ndarray       # (E+1,) non-decreasing, offsets[0] == 0
+    meta: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        off = np.asarray(self.offsets, dtype=np.int64)
+        if off.ndim != 1 or off[0] != 0 or np.any(np.diff(off) < 0):
+            raise ShapeError(f"invalid offsets {off}")
+        if off[-1] != self.tokens.shape[0]:
+            raise ShapeError(f"offsets end {off[-1]} != token count {self.tokens.shape[0]}")
+        self.offsets = off
+
+
+def _check_bank_shapes(w1, w3, w2, sw1, sw3, sw2, d):
+    E, h, dd = w1.shape
+    if dd != d or tuple(w3.shape) != (E, h, d) or tuple(w2.shape) != (E, d, h):
+        raise ShapeError(f"expert weight shapes w1={tuple(w1.shape)} w3={tuple(w3.shape)} "
+                         f"w2={tuple(w2.shape)} inconsistent with d={d}")
+    hs = sw1.shape[0]
+    if tuple(sw1.shape) != (hs, d) or tuple(sw3.shape) != (hs, d) or tuple(sw2.shape) != (d, hs):
+        raise ShapeError(f"shared weight shapes {tuple(sw1.shape)} {tuple(sw3.shape)} "
+                         f"{tuple(sw2.shape)} inconsistent with d={d}")
+    return E, h, hs
+
+
+def _ffn(x, offsets, experts, w1, w3, w2, out_dtype):
+    """Run nimg_expert_ffn over routed segments only; returns (N, d)."""
+    n, d = x.shape
+    E, h, _ = w1.shape
+    nseg = len(offsets) - 1
+    desc = _lib.FfnDesc(n_rows=n, n_shared_rows=0, d=d, h=h, h_shared=h, n_experts=E,
+                        act_dtype=nimg_dtype(x.dtype), nseg=nseg)
+    path, ydt = C.c_int32(), C.c_int32()
+    _lib.check(_lib.lib.nimg_ffn_path(C.byref(desc), C.byref(path), C.byref(ydt)))
+    y = torch.empty((n, d), dtype=torch.bfloat16 if ydt.value == _lib.NIMG_BF16 else torch.float32,
+                    device=x.device)
+    nbytes = C.c_size_t()
+    _lib.check(_lib.lib.nimg_ffn_workspace_bytes(C.byref(desc), C.byref(nbytes)))
+    ws = workspace(nbytes.value)
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    ex = np.ascontiguousarray(experts, dtype=np.int32)
+    _lib.check(_lib.lib.nimg_expert_ffn(
+        C.byref(desc), off.ctypes.data, ex.ctypes.data, ptr(x), ptr(w1), ptr(w3), ptr(w2), ptr(y),
+        None, None, None, None, None, ptr(ws), ws.numel(), stream_handle()))
+    return y if y.dtype == out_dtype else y.to(out_dtype)
+
+
+def swiglu(x, w1, w3, w2):
+    """moe.py:31-64 -- (SiLU(x W1^T) * (x W3^T)) W2^T on the GPU."""
+    xt = to_device(x)
+    act = xt.dtype
+    w1t, w3t, w2t = (to_device(w, act) for w in (w1, w3, w2))
+    n, d = xt.shape[-2], xt.shape[-1]
+    h = w1t.shape[0]
+    if tuple(w1t.shape) != (h, d) or tuple(w3t.shape) != (h, d) or tuple(w2t.shape) != (d, h):
+        raise ShapeError(f"swiglu weight shapes w1={tuple(w1t.shape)} w3={tuple(w3t.shape)} "
+                         f"w2={tuple(w2t.shape)} inconsistent with d={d}")
+    lead = xt.shape[:-1]
+    x2 = xt.reshape(-1, d)
+    y = _ffn(x2, [0, x2.shape[0]], [0], w1t[None], w3t[None], w2t[None], act)
+    return y.reshape(*lead, d)
+
+
+def swiglu_arrays(x, w1, w3, w2):
+    """moe.py:20-28 -- same gated-linear forward on raw arrays (GPU)."""
+    return swiglu(x, w1, w3, w2)
+
+
+def swiglu_composed(x, w1, w3, w2):
+    """moe.py:67-70 -- value-identical (within rounding) to swiglu."""
+    return swiglu(x, w1, w3, w2)
+
+
+def grouped_forward(batch: GroupedBatch, bank: ExpertBank):
+    """moe.py:115-135 -- segment e through expert e; output keeps row order."""
+    E = bank.n_experts
+    if len(batch.offsets) != E + 1:
+        raise ShapeError(f"offsets length {len(batch.offsets)} != E+1 ({E + 1})")
+    x = to_device(batch.tokens)
+    act = x.dtype
+    w1, w3, w2 = (to_device(w, act) for w in (bank.w1, bank.w3, bank.w2))
+    E_, h, d = w1.shape
+    if d != x.shape[1] or tuple(w3.shape) != (E, h, d) or tuple(w2.shape) != (E, d, h):
+        raise ShapeError("expert weight shapes inconsistent with tokens")
+    if x.shape[0] == 0:
+        return torch.zeros((0, x.shape[1]), dtype=act, device=x.device)
+    return _ffn(x, batch.offsets, np.arange(E, dtype=np.int32), w1, w3, w2, act)
+
+
+def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_r,
+                return_routing: bool = False):
+    """moe.py:138-164 -- route on x_norm + t_emb, experts on x_mod.
+
+    Returns (B, S, d) in the activation dtype of x_mod (fp32 or bf16); with
+    return_routing, (out, decisions, routing) like the reference.
+    """
+    B, S, d = x.shape
+    cfg.validate_weight(w_r)
+    xm = to_device(x_mod)
+    act = xm.dtype
+    xn = to_device(x_norm, act)
+    if tuple(xm.shape) != (B, S, d) or tuple(xn.shape) != (B, S, d):
+        raise ShapeError(f"x_norm {tuple(xn.shape)} / x_mod {tuple(xm.shape)} != {(B, S, d)}")
+    te = to_device(t_emb, torch.float32)
+    wr = to_device(w_r, torch.float32)
+    if tuple(te.shape) != (B, d):
+        raise ConfigError(f"t_emb shape {tuple(te.shape)}, expected {(B, d)}")
+    E = cfg.n_experts
+    if bank.n_experts != E:
+        raise ConfigError(f"bank has {bank.n_experts} experts, router {E}")
+    cap = capacity_for(S, E, cfg.capacity_factor)
+    if cap < 1:
+        raise ConfigError("computed capacity is zero")
+    w = bank.on_device(act)
+    _, h, hs = _check_bank_shapes(w.w1, w.w3, w.w2, w.shared_w1, w.shared_w3, w.shared_w2, d)
+
+    desc = make_desc(B, S, d, E, cap, h, hs, cfg, act)
+    nbytes = C.c_size_t()
+    _lib.check(_lib.lib.nimg_moe_workspace_bytes(C.byref(desc), C.byref(nbytes)))
+    ws = workspace(nbytes.value)
+    out = torch.empty((B, S, d), dtype=act, device=xm.device)
+    r = alloc_route_out(B, S, E, cap, xm.device)
+    ptrs = _lib.MoePtrs(ptr(xn), ptr(xm), ptr(te), ptr(wr), ptr(w.w1), ptr(w.w3), ptr(w.w2),
+                        ptr(w.shared_w1), ptr(w.shared_w3), ptr(w.shared_w2), ptr(out),
+                        route_struct(r))
+    _lib.check(_lib.lib.nimg_moe_forward(C.byref(desc), C.byref(ptrs), ptr(ws), ws.numel(),
+                                         stream_handle()))
+    if return_routing:
+        decisions, routing = build_routing(r, B, S, E, cap)
+        return out, decisions, routing
+    return out

@@ -1,0 +1,89 @@
+"""CPU-side checks of the C ABI: the library loads without a GPU, exports every
+entry point include/nimg_moe.h declares, and its host-only functions
+(capacity, workspace sizing, validation -> error codes) behave like the
+reference's host logic."""
+
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from oracle import nimg_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_2604_12163_b200 import _lib as L
+    return L
+
+
+def test_header_declares_exactly_the_exported_symbols():
+    L = _lib()
+    hdr = open(os.path.join(ROOT, "include", "nimg_moe.h")).read()
+    declared = set(re.findall(r"\b(nimg_[a-z0-9_]+)\s*\(", hdr))
+    assert declared == set(L.EXPORTS)
+    for name in declared:
+        assert hasattr(L.lib, name), name
+
+
+def test_capacity_for_matches_reference_host_logic():
+    L = _lib()
+    out = C.c_int64()
+    for S, E, Cf in [(256, 64, 8.0), (1024, 64, 4.0), (5, 64, 8.0), (4, 2, 100.0), (4032, 64, 2.0),
+                     (3840, 64, 2.0), (4096, 64, 8.0), (37, 5, 1.7)]:
+        assert L.lib.nimg_capacity_for(S, E, Cf, C.byref(out)) == 0
+        assert out.value == O.capacity_for(S, E, Cf)
+    assert L.lib.nimg_capacity_for(0, 2, 1.0, C.byref(out)) == L.NIMG_ERR_CONFIG
+    assert L.lib.nimg_capacity_for(4, 2, 0.0, C.byref(out)) == L.NIMG_ERR_CONFIG
+    assert b"invalid capacity" in L.lib.nimg_last_error()
+
+
+def test_workspace_and_validation_codes():
+    L = _lib()
+    d = L.MoeDesc(B=16, S=1024, d=2048, E=64, cap=64, h=1344, h_shared=1344, gate_scale=1.0,
+                  gate_eps=1e-6, act_dtype=L.NIMG_BF16, reserved=0)
+    n = C.c_size_t()
+    assert L.lib.nimg_moe_workspace_bytes(C.byref(d), C.byref(n)) == 0
+    R_rows, T = 64 * 16 * 64, 16 * 1024
+    # gathered rows + pre (routed+shared) + y (routed+shared), bf16, plus routing scratch
+    assert n.value >= 2 * (R_rows * 2048 + (R_rows + T) * 1344 + (R_rows + T) * 2048)
+    bad = L.MoeDesc(**{f: getattr(d, f) for f, _ in L.MoeDesc._fields_})
+    bad.gate_eps = 0.0
+    assert L.lib.nimg_moe_workspace_bytes(C.byref(bad), C.byref(n)) == L.NIMG_ERR_CONFIG
+    bad.gate_eps = 1e-6
+    bad.cap = 0
+    assert L.lib.nimg_moe_workspace_bytes(C.byref(bad), C.byref(n)) == L.NIMG_ERR_CONFIG
+    bad.cap = 2048
+    assert L.lib.nimg_moe_workspace_bytes(C.byref(bad), C.byref(n)) == L.NIMG_ERR_CONFIG
+
+
+def test_ffn_path_selection():
+    L = _lib()
+    f = L.FfnDesc(n_rows=1024, n_shared_rows=0, d=2048, h=1344, h_shared=1344, n_experts=64,
+                  act_dtype=L.NIMG_BF16, nseg=64)
+    p, y = C.c_int32(), C.c_int32()
+    assert L.lib.nimg_ffn_path(C.byref(f), C.byref(p), C.byref(y)) == 0
+    assert (p.value, y.value) == (L.NIMG_PATH_TCGEN05, L.NIMG_BF16)
+    f.act_dtype = L.NIMG_F32
+    L.lib.nimg_ffn_path(C.byref(f), C.byref(p), C.byref(y))
+    assert (p.value, y.value) == (L.NIMG_PATH_SIMT, L.NIMG_F32)
+    f.act_dtype, f.h = L.NIMG_BF16, 20
+    L.lib.nimg_ffn_path(C.byref(f), C.byref(p), C.byref(y))
+    assert p.value == L.NIMG_PATH_SIMT
+
+
+def test_python_api_mirrors_reference_host_functions():
+    from paper_2604_12163_b200 import router as R
+    assert R.capacity_for(1024, 64, 4.0) == 64
+    assert R.capacity_schedule(5, R.StageId.S1024) == 2.0
+    assert R.capacity_schedule(0, R.StageId.S256) is R.DENSE
+    with pytest.raises(IndexError):
+        R.capacity_schedule(32, R.StageId.S256)
+    with pytest.raises(R.ConfigError):
+        R.RouterConfig(d_model=4, n_experts=2, capacity_factor=0.0)
+    import numpy as np
+    from paper_2604_12163_b200 import moe as M
+    with pytest.raises(M.ShapeError):
+        M.GroupedBatch(np.zeros((3, 2)), np.array([0, 2, 1]))

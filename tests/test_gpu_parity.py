@@ -1,0 +1,248 @@
+"""GPU parity: the CUDA path (through the operator API -> C ABI) against the
+reference's golden vectors and the CPU oracle.
+
+Bars (BASELINE.json north_star): expert selection indices, token permutation
+and fp32 router scores/gates bit-exact; layer output Frobenius rel-err
+<= 1e-4 in fp32 mode and <= 2e-2 in bf16 mode.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import nimg_oracle as O
+from oracle.workloads import make_layer_inputs
+from tests import golden_cases as G
+from tests.gpu_helpers import TOL_BF16, TOL_FP32, bank_of, np_of, rel_fro, to_gpu
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_12163_b200 import _lib as L  # fails loudly if the .so is missing
+    return L
+
+
+def _route(inp, p):
+    from paper_2604_12163_b200 import router as R
+    g = to_gpu(inp, p["mode"])
+    cfg = R.RouterConfig(d_model=p["d"], n_experts=p["E"], capacity_factor=p["C"],
+                         gate_scale=p.get("gate_scale", 1.0))
+    return R.route_full(g["x_norm"], g["t_emb"], g["w_r"], cfg)
+
+
+def _check_routing(decisions, routing, exp, B):
+    np.testing.assert_array_equal(np_of(routing["logits"]), exp["logits"])
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), exp["token_flat"])
+    np.testing.assert_array_equal(np_of(routing["gates"]), exp["gates"])
+    np.testing.assert_array_equal(np.stack([d.top_indices for d in decisions]), exp["top"])
+    np.testing.assert_array_equal(np.stack([d.affinity for d in decisions]), exp["affinity"])
+    assert routing["capacity"] == int(exp["capacity"])
+
+
+@pytest.mark.parametrize("name", G.names("route"))
+def test_route_bitexact_vs_reference_golden(name):
+    kind, p, inp, exp = G.case(name)
+    decisions, routing = _route(inp, p)
+    _check_routing(decisions, routing, exp, p["B"])
+
+
+@pytest.mark.parametrize("name", G.names("moe"))
+def test_moe_forward_vs_reference_golden(name):
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    kind, p, inp, exp = G.case(name)
+    g = to_gpu(inp, p["mode"])
+    cfg = R.RouterConfig(d_model=p["d"], n_experts=p["E"], capacity_factor=p["C"],
+                         gate_scale=p.get("gate_scale", 1.0))
+    out, decisions, routing = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg,
+                                            bank_of(g), g["w_r"], return_routing=True)
+    _check_routing(decisions, routing, exp, p["B"])
+    err = rel_fro(np_of(out), exp["out"])
+    tol = TOL_FP32 if p["mode"] == "fp32" else TOL_BF16
+    assert err <= tol, f"{name}: rel-err {err:.3e} > {tol}"
+
+
+# ---------------------------------------------------------------- KATs
+def test_uniform_logits_tie_break_by_index():            # test_router.py:48-58
+    from paper_2604_12163_b200 import router as R
+    rng = np.random.default_rng(0)
+    for S, E, C in ((6, 2, 1.0), (1024, 64, 4.0), (4096, 64, 2.0)):
+        d = 8
+        cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+        xn = torch.tensor(rng.normal(size=(2, S, d)), dtype=torch.float32).cuda()
+        te = torch.tensor(rng.normal(size=(2, d)), dtype=torch.float32).cuda()
+        wr = torch.zeros((2 * d, E), dtype=torch.float32).cuda()
+        decs = R.route(xn, te, wr, cfg)
+        cap = R.capacity_for(S, E, C)
+        for dec in decs:
+            for e in range(E):
+                np.testing.assert_array_equal(dec.top_indices[e], np.arange(cap))
+            np.testing.assert_allclose(dec.affinity, 1.0 / E, atol=1e-7)
+
+
+def test_full_capacity_gates_sum_to_one():               # test_router.py:61-75
+    from paper_2604_12163_b200 import router as R
+    rng = np.random.default_rng(1)
+    cfg = R.RouterConfig(d_model=4, n_experts=2, capacity_factor=2.0)
+    wr = torch.tensor(rng.normal(size=(8, 2)), dtype=torch.float32).cuda()
+    xn = torch.tensor(rng.normal(size=(1, 4, 4)), dtype=torch.float32).cuda()
+    te = torch.tensor(rng.normal(size=(1, 4)), dtype=torch.float32).cuda()
+    (dec,) = R.route(xn, te, wr, cfg)
+    assert dec.capacity == 4
+    for e in range(2):
+        np.testing.assert_array_equal(np.sort(dec.top_indices[e]), np.arange(4))
+    per_tok = np.zeros(4)
+    np.add.at(per_tok, dec.top_indices.reshape(-1), dec.gates.reshape(-1))
+    np.testing.assert_allclose(per_tok, 1.0, atol=1e-5)
+
+
+def test_router_weight_shape_and_config_errors():       # test_router.py:152-155, router.py:45-56
+    from paper_2604_12163_b200 import router as R
+    cfg = R.RouterConfig(d_model=4, n_experts=2, capacity_factor=1.0)
+    with pytest.raises(R.ConfigError):
+        cfg.validate_weight(torch.zeros((4, 2)))
+    with pytest.raises(R.ConfigError):
+        R.RouterConfig(d_model=4, n_experts=0, capacity_factor=1.0)
+    with pytest.raises(R.ConfigError):
+        R.route(torch.zeros((1, 4, 4)), torch.zeros((1, 4)), torch.zeros((4, 2)), cfg)
+
+
+def test_swiglu_scalar_reduction_and_zero_input():       # test_moe.py:19-33
+    from paper_2604_12163_b200 import moe as M
+    for x in (-1.3, 0.0, 0.7, 2.5):
+        one = torch.ones((1, 1))
+        out = M.swiglu(torch.tensor([[x]], dtype=torch.float32), one, one, one)
+        np.testing.assert_allclose(out.item(), x / (1 + np.exp(-x)) * x, rtol=1e-6)
+    rng = np.random.default_rng(0)
+    w1, w3, w2 = (torch.tensor(rng.normal(size=s), dtype=torch.float32) for s in ((3, 2), (3, 2), (2, 3)))
+    out = M.swiglu(torch.zeros((4, 2)), w1, w3, w2)
+    assert torch.all(out == 0)
+    with pytest.raises(M.ShapeError):
+        M.swiglu(torch.zeros((2, 3)), torch.zeros((4, 3)), torch.zeros((4, 2)), torch.zeros((3, 4)))
+
+
+def test_grouped_forward_matches_loop_oracle_and_empty_segments():   # test_moe.py:69-112
+    from paper_2604_12163_b200 import moe as M
+    rng = np.random.default_rng(5)
+    for mode, (E, h, d), counts in (("fp32", (3, 4, 5), [2, 0, 3]),
+                                    ("fp32", (4, 48, 64), [130, 0, 0, 257]),
+                                    ("bf16", (4, 224, 256), [300, 0, 129, 1])):
+        w = {k: rng.normal(size=s).astype(np.float32) * 0.05 for k, s in
+             (("w1", (E, h, d)), ("w3", (E, h, d)), ("w2", (E, d, h)))}
+        toks = rng.normal(size=(sum(counts), d)).astype(np.float32)
+        if mode == "bf16":
+            from oracle.workloads import bf16_round
+            w = {k: bf16_round(v) for k, v in w.items()}
+            toks = bf16_round(toks)
+        off = np.concatenate([[0], np.cumsum(counts)])
+        act = torch.bfloat16 if mode == "bf16" else torch.float32
+        bank = M.ExpertBank(*(torch.tensor(w[k]).cuda().to(act) for k in ("w1", "w3", "w2")),
+                            None, None, None)
+        y = M.grouped_forward(M.GroupedBatch(torch.tensor(toks).cuda().to(act), off), bank)
+        ref = O.grouped_forward(toks, off, w["w1"], w["w3"], w["w2"])
+        tol = TOL_FP32 if mode == "fp32" else TOL_BF16
+        assert rel_fro(np_of(y), ref) <= tol
+    with pytest.raises(M.ShapeError):
+        M.GroupedBatch(torch.zeros((3, 2)), np.array([0, 2, 1]))
+    with pytest.raises(M.ShapeError):
+        M.GroupedBatch(torch.zeros((3, 2)), np.array([0, 1, 2]))
+
+
+def test_zero_w2_gives_shared_only_and_single_expert():   # test_moe.py:147-176
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    rng = np.random.default_rng(6)
+    d, E, h, S = 4, 2, 4, 6
+    f = lambda *s: rng.normal(size=s).astype(np.float32)
+    w1, w3, w2 = f(E, h, d), f(E, h, d), np.zeros((E, d, h), np.float32)
+    s1, s3, s2 = f(h, d), f(h, d), f(d, h)
+    xm, xn, te, wr = f(1, S, d), f(1, S, d), f(1, d), f(2 * d, E)
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=1.0)
+    T = lambda a: torch.tensor(a).cuda()
+    out = M.moe_forward(T(xm), T(xn), T(xm), T(te), cfg,
+                        M.ExpertBank(*(T(a) for a in (w1, w3, w2, s1, s3, s2))), T(wr))
+    shared = O.swiglu_arrays(xm.reshape(-1, d), s1, s3, s2)
+    assert rel_fro(np_of(out).reshape(-1, d), shared) <= TOL_FP32
+    # single expert, full capacity: shared + alpha/(1+eps) * expert
+    alpha = 1.7
+    w1, w3, w2 = f(1, 5, 3), f(1, 5, 3), f(1, 3, 5)
+    s1, s3, s2 = f(5, 3), f(5, 3), f(3, 5)
+    xm, xn, te, wr = f(1, 4, 3), f(1, 4, 3), f(1, 3), f(6, 1)
+    cfg = R.RouterConfig(d_model=3, n_experts=1, capacity_factor=1.0, gate_scale=alpha)
+    out = M.moe_forward(T(xm), T(xn), T(xm), T(te), cfg,
+                        M.ExpertBank(*(T(a) for a in (w1, w3, w2, s1, s3, s2))), T(wr))
+    flat = xm.reshape(-1, 3)
+    expect = O.swiglu_arrays(flat, s1, s3, s2).astype(np.float64) + \
+        alpha / (1 + 1e-6) * O.swiglu_arrays(flat, w1[0], w3[0], w2[0])
+    assert rel_fro(np_of(out).reshape(-1, 3), expect) <= TOL_FP32
+
+
+def test_decoupling_and_determinism_and_permutation():    # test_moe.py:194-217, test_router.py:137-149
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    inp = make_layer_inputs(10, 3, 128, 256, 8, 112, mode="bf16")
+    g = to_gpu(inp, "bf16")
+    cfg = R.RouterConfig(d_model=256, n_experts=8, capacity_factor=2.0)
+    bank = bank_of(g)
+    o1, d1, r1 = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg, bank, g["w_r"],
+                               return_routing=True)
+    o1b = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg, bank, g["w_r"])
+    assert torch.equal(o1, o1b)                      # bitwise repeatable
+    x10 = (g["x_mod"].float() * 10).to(torch.bfloat16)
+    o2, d2, r2 = M.moe_forward(x10, g["x_norm"], x10, g["t_emb"], cfg, bank, g["w_r"],
+                               return_routing=True)
+    for a, b in zip(d1, d2):
+        np.testing.assert_array_equal(a.top_indices, b.top_indices)
+        np.testing.assert_array_equal(a.gates, b.gates)
+    assert not torch.allclose(o1.float(), o2.float())
+    perm = torch.tensor([2, 0, 1]).cuda()
+    op = M.moe_forward(g["x_mod"][perm], g["x_norm"][perm], g["x_mod"][perm], g["t_emb"][perm],
+                       cfg, bank, g["w_r"])
+    assert torch.equal(op, o1[perm])
+
+
+# ---------------------------------------------------------------- full size
+@pytest.mark.parametrize("B,S,C,seed", [(16, 1024, 4.0, 2), (4, 4096, 2.0, 4)])
+def test_full_width_layer_vs_oracle_and_properties(B, S, C, seed):
+    """cfg2 / 1024px shapes at full width (d=2048, h=1344, E=64) in bf16.
+    Routing for every sample is checked bit-exactly against the oracle's
+    router; the layer output of sample 0 against the oracle's full layer;
+    plus size-independent properties over the whole batch."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    d, h, E = 2048, 1344, 64
+    gen = torch.Generator(device="cuda").manual_seed(seed)
+    rn = lambda *s, std=1.0: (torch.randn(*s, generator=gen, device="cuda") * std)
+    tn = lambda *s, std: torch.clamp(rn(*s, std=std), -2 * std, 2 * std)
+    x = rn(B, S, d)
+    xn = (x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6) / np.sqrt(18)).to(torch.bfloat16)
+    xm = (xn.float() * (1 + 0.1 * rn(B, 1, d))).to(torch.bfloat16)
+    te = rn(B, d)
+    wr = tn(2 * d, E, std=0.006)
+    ws = [tn(*s, std=0.02).to(torch.bfloat16) for s in ((E, h, d), (E, h, d), (E, d, h), (h, d), (h, d), (d, h))]
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    out, decisions, routing = M.moe_forward(xm, xn, xm, te, cfg, M.ExpertBank(*ws), wr,
+                                            return_routing=True)
+    cap = routing["capacity"]
+    xn_np, te_np, wr_np = np_of(xn), np_of(te), np_of(wr)
+    # --- routing of every sample, bit-exact against the oracle router
+    r = O.route_full(xn_np, te_np, wr_np, n_experts=E, capacity_factor=C)
+    np.testing.assert_array_equal(np_of(routing["logits"]), r["logits"])
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), r["token_flat"])
+    np.testing.assert_array_equal(np_of(routing["gates"]), r["gates"])
+    # --- properties: exact utilisation, ordering, gate identity
+    top = np.stack([dd.top_indices for dd in decisions])            # (B,E,cap)
+    aff = np.stack([dd.affinity for dd in decisions])
+    for b in range(B):
+        for e in range(E):
+            assert len(np.unique(top[b, e])) == cap
+    assert np.all(np.diff(aff, axis=-1) <= 0)                       # score descending
+    # --- full layer output of sample 0 against the oracle layer
+    w_np = [np_of(w) for w in ws]
+    o_ref = O.moe_forward(xn_np[:1], np_of(xm)[:1], te_np[:1], wr_np, *w_np, capacity_factor=C)
+    err = rel_fro(np_of(out[:1]), o_ref)
+    assert err <= TOL_BF16, f"rel-err {err:.3e}"
