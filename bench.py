@@ -1,0 +1,347 @@
+"""Benchmark: expert-choice MoE layer tokens/s (+ expert-GEMM TFLOP/s, roofline).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N=1 workload = BASELINE.json configs[1] ("cfg2"): one expert-choice MoE layer at
+full Nucleus-Image width (d=2048, h=1344, 64 routed experts + shared expert),
+512px = S=1024 tokens/sample, batch 16, capacity factor 4 (the S512 stage,
+router.py:91-92), bf16 activations/weights, fp32 router. A step = one full
+layer forward (router -> select -> gates -> gather -> grouped SwiGLU GEMMs ->
+combine + shared expert). Synthetic seeded inputs, random-init weights.
+
+N>1 (torchrun): expert parallel over NCCL (see paper_2604_12163_b200/ep.py),
+BASELINE configs[3] shape: S=4096, global batch 32, C=2, 64/N experts per GPU.
+
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Expert-choice MoE layer tokens/s; expert GEMM TFLOP/s % of B200 bf16 peak"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+CFG2 = dict(name="cfg2", B=16, S=1024, d=2048, h=1344, E=64, C=4.0, layer=17, seed=2)
+CFG4 = dict(name="cfg4", B=32, S=4096, d=2048, h=1344, E=64, C=2.0, layer=17, seed=4)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j, "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+def work_counts(c):
+    """Algorithmic work per layer step."""
+    B, S, d, h, E = c["B"], c["S"], c["d"], c["h"], c["E"]
+    cap = min(math.ceil(c["C"] * S / E), S)
+    T = B * S
+    R = E * B * cap
+    flops_g1 = 4.0 * d * h * (R + T)           # x W1^T and x W3^T
+    flops_g2 = 2.0 * d * h * (R + T)           # pre W2^T
+    return dict(cap=cap, T=T, R=R, flops_g1=flops_g1, flops_g2=flops_g2,
+                flops_router=2.0 * T * d * E + 2.0 * B * d * E,
+                # algorithmic HBM bytes (bf16 acts, fp32 scores, int32 idx)
+                bytes_router=T * d * 2 + T * E * 4 * 2,
+                bytes_gather=R * d * 2 * 2,
+                bytes_combine=(R + 2 * T) * d * 2 + T * E * 4,
+                bytes_weights=3.0 * d * h * (E + 1) * 2)
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 7:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------- inputs
+def make_inputs(c, dev, B=None):
+    """Seeded synthetic layer inputs on the GPU (recipe of oracle/workloads.py)."""
+    import torch
+    B = c["B"] if B is None else B
+    S, d, h, E = c["S"], c["d"], c["h"], c["E"]
+    g = torch.Generator(device=dev).manual_seed(c["seed"])
+    rn = lambda *s, std=1.0: torch.randn(*s, generator=g, device=dev) * std
+    tn = lambda *s, std: torch.clamp(rn(*s, std=std), -2 * std, 2 * std)
+    x = rn(B, S, d)
+    xn = x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6) / math.sqrt(c["layer"] + 1)
+    xm = xn * (1 + 0.1 * rn(B, 1, d))
+    del x
+    bf = torch.bfloat16
+    w = dict(x_norm=xn.to(bf), x_mod=xm.to(bf), t_emb=rn(B, d), w_r=tn(2 * d, E, std=0.006),
+             w1=tn(E, h, d, std=0.02).to(bf), w3=tn(E, h, d, std=0.02).to(bf),
+             w2=tn(E, d, h, std=0.02).to(bf), sw1=tn(h, d, std=0.02).to(bf),
+             sw3=tn(h, d, std=0.02).to(bf), sw2=tn(d, h, std=0.02).to(bf))
+    return w
+
+
+# ----------------------------------------------------------------- CPU baselines
+def cpu_layer_sample(c, budget_s: float, max_samples: int):
+    """Time the oracle port of the reference's moe_forward (moe.py:138-164)
+    one sample at a time (routing is per sample, router.py:127) on host cores."""
+    import numpy as np
+    import torch
+    from oracle import nimg_oracle as O
+    inp = make_inputs(c, "cuda" if torch.cuda.is_available() else "cpu", B=max_samples)
+    a = {k: v.float().cpu().numpy() for k, v in inp.items()}
+    del inp
+    times, tokens = [], 0
+    t_all = time.perf_counter()
+    for b in range(max_samples):
+        t0 = time.perf_counter()
+        O.moe_forward(a["x_norm"][b:b + 1], a["x_mod"][b:b + 1], a["t_emb"][b:b + 1], a["w_r"],
+                      a["w1"], a["w3"], a["w2"], a["sw1"], a["sw3"], a["sw2"],
+                      capacity_factor=c["C"])
+        times.append(time.perf_counter() - t0)
+        tokens += c["S"]
+        if time.perf_counter() - t_all > budget_s:
+            break
+    return tokens / sum(times), len(times), times
+
+
+def run_reference_arm(args, c):
+    """--impl reference: the reference's CPU MoE path (oracle port; the
+    reference is pure Python and cannot be compiled) on all host threads."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+    from oracle import nimg_oracle as O
+    cores = os.cpu_count()
+    inp = make_inputs(c, "cuda" if torch.cuda.is_available() else "cpu", B=1)
+    a = {k: v.float().cpu().numpy() for k, v in inp.items()}
+    step = lambda: O.moe_forward(a["x_norm"], a["x_mod"], a["t_emb"], a["w_r"], a["w1"], a["w3"],
+                                 a["w2"], a["sw1"], a["sw3"], a["sw2"], capacity_factor=c["C"])
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    val = args.steps * c["S"] / dt
+    sample = f"1 sample (S={c['S']} tokens) of {c['name']} per step, fp32 oracle port (f64 compute)"
+    line = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(c), "l2": "n/a (CPU)"},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(c):
+    return (f"{c['name']}: expert-choice MoE layer d={c['d']} h={c['h']} E={c['E']} C={c['C']} "
+            f"S={c['S']} B={c['B']}")
+
+
+# ----------------------------------------------------------------- ours, 1 GPU
+def run_single(args, c, peaks, peak_kind):
+    import ctypes as C
+    import torch
+    from paper_2604_12163_b200 import _lib
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    inp = make_inputs(c, dev)
+    cfg = R.RouterConfig(d_model=c["d"], n_experts=c["E"], capacity_factor=c["C"])
+    bank = M.ExpertBank(inp["w1"], inp["w3"], inp["w2"], inp["sw1"], inp["sw3"], inp["sw2"])
+    plan = M.MoEPlan(cfg, bank, c["B"], c["S"], torch.bfloat16)
+    fwd = lambda: plan.forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"])
+    wc = work_counts(c)
+
+    for _ in range(max(args.warmup, 3)):
+        fwd()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K back-to-back layer steps (working set >> L2)
+    clk = ClockSampler(0)
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        fwd()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    value = wc["T"] / (ms * 1e-3)
+
+    # ---- per-stage times (stage events recorded by the library on the stream)
+    n_ev = 6
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    for row in evs:
+        for e in row:
+            e.record()  # torch creates the underlying cudaEvent_t lazily
+    torch.cuda.synchronize()
+    stage_ms = [0.0] * (n_ev - 1)
+    for k in range(args.steps):
+        arr = (C.c_void_p * n_ev)(*[e.cuda_event for e in evs[k]])
+        _lib.check(_lib.lib.nimg_profile_events(arr, n_ev))
+        fwd()
+    _lib.check(_lib.lib.nimg_profile_events(None, 0))
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        for i in range(n_ev - 1):
+            stage_ms[i] += evs[k][i].elapsed_time(evs[k][i + 1]) / args.steps
+    names = ["route", "gather", "gemm1_swiglu", "gemm2", "combine"]
+    stages = dict(zip(names, stage_ms))
+    hbm = peaks["hbm_gbs"]
+    tf_peak = peaks["bf16_tflops"]
+    g1_tf = wc["flops_g1"] / (stages["gemm1_swiglu"] * 1e-3) / 1e12
+    g2_tf = wc["flops_g2"] / (stages["gemm2"] * 1e-3) / 1e12
+    ffn_tf = (wc["flops_g1"] + wc["flops_g2"]) / ((stages["gemm1_swiglu"] + stages["gemm2"]) * 1e-3) / 1e12
+    stage_detail = {
+        "route_ms": stages["route"], "gather_ms": stages["gather"],
+        "gemm1_ms": stages["gemm1_swiglu"], "gemm2_ms": stages["gemm2"],
+        "combine_ms": stages["combine"],
+        "gemm1_tflops": g1_tf, "gemm2_tflops": g2_tf,
+        "gather_gbs": wc["bytes_gather"] / (stages["gather"] * 1e-3) / 1e9,
+        "combine_gbs": wc["bytes_combine"] / (stages["combine"] * 1e-3) / 1e9,
+    }
+
+    # ---- e2e through the public API with host buffers
+    e2e = run_e2e(args, c, inp, cfg, bank)
+
+    # ---- CPU baseline (oracle port), bounded sample
+    cpu = None
+    if not args.no_cpu_baseline:
+        val, n, _ = cpu_layer_sample(c, budget_s=args.cpu_budget, max_samples=4)
+        cpu = {"value": val, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"{n} sample(s) x S={c['S']} tokens of {c['name']} through the oracle "
+                         f"port of moe_forward (f64 compute, OpenBLAS threads = all cores)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded randn, random-init weights)",
+        "config": {"workload": workload_name(c), "capacity": wc["cap"], "routed_rows": wc["R"],
+                   "tokens": wc["T"], "parallelism": "single GPU",
+                   "l2": "inputs larger than L2 (1.07 GB expert weights + 134 MB activations per step)"},
+        "expert_gemm_tflops": ffn_tf,
+        "expert_gemm_frac_of_peak": ffn_tf / tf_peak,
+        "roofline": {"bound": "tensor", "kernel": "grouped_gemm_sm100<0> (GEMM1 dual-B SwiGLU)",
+                     "achieved": g1_tf, "peak": tf_peak, "unit": "TFLOP/s",
+                     "frac": g1_tf / tf_peak, "traffic": args.traffic,
+                     "peak_source": f"{peak_kind} bf16_tflops (burst)",
+                     "algorithmic": f"4*d*h*(R_rows+T) = {wc['flops_g1']:.4g} FLOP per launch"},
+        "stages": stage_detail,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 8 * args.steps,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, c, inp, cfg, bank):
+    """Same metric through the public API (moe.moe_forward) with pinned host
+    inputs copied in and the layer output copied out every step."""
+    import torch
+    from paper_2604_12163_b200 import moe as M
+    host = {k: inp[k].cpu().pin_memory() for k in ("x_norm", "x_mod", "t_emb")}
+    out_h = torch.empty(inp["x_mod"].shape, dtype=inp["x_mod"].dtype).pin_memory()
+    w_r = inp["w_r"]
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    d2h = out_h.numel() * out_h.element_size()
+
+    def step():
+        dv = {k: v.cuda(non_blocking=True) for k, v in host.items()}
+        y = M.moe_forward(dv["x_mod"], dv["x_norm"], dv["x_mod"], dv["t_emb"], cfg, bank, w_r)
+        out_h.copy_(y, non_blocking=True)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    T = c["B"] * c["S"]
+    return {"value": T / (ms * 1e-3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": ms}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, choices=["cfg2", "cfg4"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per GEMM1 launch, if captured")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    c = dict(CFG2 if (args.config or ("cfg2" if world == 1 else "cfg4")) == "cfg2" else CFG4)
+    if args.impl == "reference":
+        run_reference_arm(args, c)
+        return
+    peaks, kind = load_peaks()
+    if world > 1:
+        from paper_2604_12163_b200 import ep
+        ep.bench_main(args, c, peaks, kind)
+        return
+    run_single(args, c, peaks, kind)
+
+
+if __name__ == "__main__":
+    main()

@@ -60,7 +60,7 @@ typedef struct nimg_route_out {
   int32_t* token_flat; /* (E*B*cap) int32     routing["token_flat"]          */
   float* gate_raw;     /* (E*B*cap) fp32      RouterDecision.affinity         */
   float* gates;        /* (E*B*cap) fp32      routing["gates"]               */
-  int32_t* comb_rows;  /* (E,B*S) int32       per token: routed rows, expert-ascending */
+  int32_t* comb_rows;  /* (B*S,E) int32       per token: routed rows, expert-ascending */
   int32_t* comb_cnt;   /* (B*S) int32         number of experts that picked the token */
 } nimg_route_out;
 
@@ -91,6 +91,12 @@ const char* nimg_last_error(void);
 int nimg_abi_version(void);
 /* Number of SMs the persistent kernels size their grid by (device of stream). */
 int nimg_device_sms(int* sms);
+
+/* Profiling hook: up to 8 cudaEvent_t (as void*) recorded on the launch stream
+ * by nimg_moe_forward at its stage boundaries: [0] start, [1] routed,
+ * [2] gathered, [3] GEMM1 done, [4] GEMM2 done, [5] combined. n = 0 turns it
+ * off. Thread-local; no reference counterpart (instrumentation only). */
+int nimg_profile_events(void* const* events, int32_t n);
 
 /* router.py:70-74  capacity_for(S, E, C) = min(ceil(C*S/E), S) */
 int nimg_capacity_for(int64_t S, int64_t E, double C, int64_t* cap);
@@ -131,9 +137,9 @@ int nimg_expert_ffn(const nimg_ffn_desc* desc, const int64_t* seg_offsets,
 /* moe.py:156-161 + tensor.py:366-378: out[t] = round(f64(fp32(sum_k
  * fp32(y_routed[rows_k] * gates[rows_k]))) + f64(y_shared[t])), experts in
  * ascending order (deterministic; same bits for any expert-parallel split). */
-int nimg_combine(int64_t T, int64_t d, int32_t y_dtype, int32_t out_dtype, const void* y_routed,
-                 const void* y_shared, const float* gates, const int32_t* comb_rows,
-                 const int32_t* comb_cnt, void* out, void* stream);
+int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_dtype,
+                 const void* y_routed, const void* y_shared, const float* gates,
+                 const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream);
 
 #ifdef __cplusplus
 }

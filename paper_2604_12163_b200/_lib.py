@@ -22,7 +22,7 @@ EXPORTS = (
     "nimg_last_error", "nimg_abi_version", "nimg_device_sms", "nimg_capacity_for",
     "nimg_moe_workspace_bytes", "nimg_moe_forward", "nimg_route_workspace_bytes", "nimg_route",
     "nimg_gather_rows", "nimg_ffn_path", "nimg_ffn_workspace_bytes", "nimg_expert_ffn",
-    "nimg_combine",
+    "nimg_combine", "nimg_profile_events",
 )
 
 
@@ -73,7 +73,8 @@ def _load():
         "nimg_ffn_workspace_bytes": ([C.POINTER(FfnDesc), C.POINTER(SZ)], C.c_int),
         "nimg_expert_ffn": ([C.POINTER(FfnDesc), P, P, P, P, P, P, P, P, P, P, P, P, P, SZ, P],
                             C.c_int),
-        "nimg_combine": ([I64, I64, I32, I32, P, P, P, P, P, P, P], C.c_int),
+        "nimg_combine": ([I64, I64, I64, I32, I32, P, P, P, P, P, P, P], C.c_int),
+        "nimg_profile_events": ([C.POINTER(C.c_void_p), I32], C.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

@@ -18,6 +18,13 @@ using namespace nimg;
 namespace {
 
 thread_local std::string g_err;
+// Optional stage events (nimg_profile_events): recorded on the launch stream
+// at the stage boundaries of nimg_moe_forward. Null = off.
+thread_local cudaEvent_t g_events[8];
+thread_local int g_nevents = 0;
+inline void mark(int i, cudaStream_t st) {
+  if (i < g_nevents && g_events[i]) cudaEventRecord(g_events[i], st);
+}
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -133,16 +140,20 @@ int check_moe_desc(const nimg_moe_desc* d) {
 
 struct RouteWs {
   double* tb;
+  double* wd;
   int16_t* slot_of;
 };
 size_t route_ws_bytes(const nimg_moe_desc* d) {
-  return align_up((size_t)d->B * d->E * 8) + align_up((size_t)d->E * d->B * d->S * 2);
+  return align_up((size_t)d->B * d->E * 8) + align_up(router_wd_bytes((int)d->d, (int)d->E)) +
+         align_up((size_t)d->E * d->B * d->S * 2);
 }
 RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
   RouteWs r;
   r.tb = reinterpret_cast<double*>(p);
   p += align_up((size_t)d->B * d->E * 8);
+  r.wd = reinterpret_cast<double*>(p);
+  p += align_up(router_wd_bytes((int)d->d, (int)d->E));
   r.slot_of = reinterpret_cast<int16_t*>(p);
   return r;
 }
@@ -263,6 +274,7 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0};
       p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0};
       CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
+      mark(3, st);
     }
     // GEMM2: y = pre W2^T
     {
@@ -301,6 +313,7 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
     p.bank[0] = SimtBank{xr, d, w1, w3, reinterpret_cast<float*>(pre_r), h, d, h, (h + bn - 1) / bn, 0};
     p.bank[1] = SimtBank{xs, d, sw1, sw3, reinterpret_cast<float*>(pre_s), hs, d, hs, (hs + bn - 1) / bn, 0};
     CUDA_TRY(launch_grouped_simt(0, bf, p, st));
+    mark(3, st);
   }
   {
     SimtParams p;
@@ -324,9 +337,8 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
   const int B = (int)d->B, S = (int)d->S, dd = (int)d->d, E = (int)d->E, cap = (int)d->cap;
   const int64_t T = d->B * d->S;
   RouteWs w = carve_route(d, ws);
-  CUDA_TRY(launch_router_tbias(t_emb, w_r, w.tb, B, dd, E, st));
-  CUDA_TRY(launch_router_scores(d->act_dtype == NIMG_BF16, x_norm, w_r, w.tb, o->logits,
-                                o->scores_bes, B, S, dd, E, st));
+  CUDA_TRY(launch_router(d->act_dtype == NIMG_BF16, x_norm, t_emb, w_r, w.tb, w.wd, o->logits,
+                         o->scores_bes, B, S, dd, E, st));
   CUDA_TRY(cudaMemsetAsync(w.slot_of, 0xFF, (size_t)E * T * 2, st));
   CUDA_TRY(launch_ec_select(o->scores_bes, o->token_flat, o->gate_raw, w.slot_of, B, S, E, cap, st));
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
@@ -414,15 +426,15 @@ int nimg_expert_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
                          (cudaStream_t)stream);
 }
 
-int nimg_combine(int64_t T, int64_t d, int32_t y_dtype, int32_t out_dtype, const void* y_routed,
-                 const void* y_shared, const float* gates, const int32_t* comb_rows,
-                 const int32_t* comb_cnt, void* out, void* stream) {
-  if (T < 0 || d < 1) return fail(NIMG_ERR_SHAPE, "bad combine shape");
+int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_dtype,
+                 const void* y_routed, const void* y_shared, const float* gates,
+                 const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream) {
+  if (T < 0 || d < 1 || E < 1) return fail(NIMG_ERR_SHAPE, "bad combine shape");
   if (T == 0) return NIMG_OK;
   if (!y_shared || !comb_cnt || !comb_rows || !out || !gates)
     return fail(NIMG_ERR_SHAPE, "null pointer");
   CUDA_TRY(launch_combine(y_dtype == NIMG_BF16, out_dtype == NIMG_BF16, y_routed, y_shared, gates,
-                          comb_rows, comb_cnt, out, T, (int)d, (cudaStream_t)stream));
+                          comb_rows, comb_cnt, out, T, (int)d, (int)E, (cudaStream_t)stream));
   return NIMG_OK;
 }
 
@@ -456,16 +468,29 @@ int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, s
   void* yr = w;                       w += align_up((size_t)f.n_rows * d->d * elt(ydt));
   void* ys = w;
 
+  mark(0, st);
   NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st));
+  mark(1, st);
   CUDA_TRY(launch_gather_rows(p->x_mod, d->d * (int64_t)elt(d->act_dtype), p->route.token_flat,
                               f.n_rows, xg, st));
+  mark(2, st);
   int64_t off[kMaxSeg + 1];
   if (f.nseg > kMaxSeg - 8) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
   for (int e = 0; e <= f.nseg; ++e) off[e] = (int64_t)e * d->B * d->cap;  // moe.py:154
   NIMG_TRY(expert_ffn_impl(&f, off, nullptr, xg, p->w1, p->w3, p->w2, yr, p->x_mod, p->sw1,
                            p->sw3, p->sw2, ys, ffn_ws, ffn_ws_bytes(&f), st));
+  mark(4, st);
   CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys, p->route.gates,
-                          p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d, st));
+                          p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,
+                          (int)d->E, st));
+  mark(5, st);
+  return NIMG_OK;
+}
+
+int nimg_profile_events(void* const* events, int32_t n) {
+  if (n < 0 || n > 8 || (n > 0 && !events)) return fail(NIMG_ERR_CONFIG, "bad event list");
+  for (int i = 0; i < n; ++i) g_events[i] = (cudaEvent_t)events[i];
+  g_nevents = n;
   return NIMG_OK;
 }
 

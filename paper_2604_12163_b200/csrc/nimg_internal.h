@@ -69,11 +69,11 @@ int simt_bn();
 cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream);
 
 // routing / data-movement kernels (route_kernels.cu)
-cudaError_t launch_router_tbias(const float* t_emb, const float* w_r, double* tb, int B, int d,
-                                int E, cudaStream_t s);
-cudaError_t launch_router_scores(bool x_bf16, const void* x_norm, const float* w_r,
-                                 const double* tb, float* logits, float* scores_bes, int B, int S,
-                                 int d, int E, cudaStream_t s);
+// router prep (t-half bias + f64 copy of W_r[:d]) and FP64 scores kernel
+cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
+                          double* tb, double* wd, float* logits, float* scores_bes, int B, int S,
+                          int d, int E, cudaStream_t s);
+size_t router_wd_bytes(int d, int E);
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s);
 cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,
@@ -84,6 +84,6 @@ cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t
 // out[t] = fp32(fp32(sum_k fp32(Y[rows[k][t]] * gate)) + shared[t]) -- see combine kernel.
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
-                           void* out, int64_t T, int d, cudaStream_t s);
+                           void* out, int64_t T, int d, int E, cudaStream_t s);
 
 }  // namespace nimg

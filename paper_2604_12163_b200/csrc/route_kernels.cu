@@ -1,6 +1,7 @@
 // Routing and data-movement kernels of the expert-choice MoE layer.
 //
-//   router_tbias   t_emb . W_r[d:]  per sample, f64            (router.py:120-122, t half)
+//   router_prep    t_emb . W_r[d:] per sample in f64 (router.py:120-122, t half)
+//                  and an f64 copy of W_r[:d]
 //   router_scores  x_norm . W_r[:d] + tbias in f64 -> fp32 logits; f64 softmax
 //                  in numpy's exact summation order -> fp32 scores (router.py:122-123,
 //                  tensor.py:280-287, 467-473). HBM-light, FP64-pipe bound.
@@ -44,157 +45,265 @@ __device__ double np_pairwise_sum(const double* a, int n) {
   return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
 }
 
-// ------------------------------------------------------------------ t bias
-// tb[b, e] = sum_k t_emb[b, k] * W_r[d + k, e] in f64. Block = (b, 32 experts),
-// 8 k-slices per expert folded in a fixed order.
-__global__ void router_tbias_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
-                                    double* __restrict__ tb, int d, int E) {
+// ------------------------------------------------------------------ router prep
+// (a) wd[k, e] = f64(W_r[k, e]) for the x half (k < d), E padded to EP;
+// (b) tb[b, e] = sum_k t_emb[b, k] * W_r[d + k, e] in f64 (the t half of the
+//     concatenated router input, router.py:120-122). Block (b, 32 experts),
+//     8 k-slices per expert folded in a fixed order.
+__global__ void router_prep_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
+                                   double* __restrict__ tb, double* __restrict__ wd, int B, int d,
+                                   int E, int EP) {
+  if (blockIdx.x >= B) {
+    const int64_t n = (int64_t)d * EP;
+    for (int64_t i = (int64_t)(blockIdx.x - B) * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)(gridDim.x - B) * blockDim.x) {
+      const int64_t k = i / EP;
+      const int e = (int)(i % EP);
+      wd[i] = e < E ? (double)w_r[k * E + e] : 0.0;
+    }
+    return;
+  }
   __shared__ double part[8][32];
   const int b = blockIdx.x;
   const int el = threadIdx.x & 31, ks = threadIdx.x >> 5;
-  const int e = blockIdx.y * 32 + el;
-  double acc = 0.0;
-  if (e < E) {
-    const float* t = t_emb + (int64_t)b * d;
-    const float* w = w_r + (int64_t)d * E + e;
-    for (int k = ks; k < d; k += 8) acc = fma((double)t[k], (double)w[(int64_t)k * E], acc);
-  }
-  part[ks][el] = acc;
-  __syncthreads();
-  if (ks == 0 && e < E) {
-    double s = part[0][el];
-    for (int j = 1; j < 8; ++j) s += part[j][el];
-    tb[(int64_t)b * E + e] = s;
+  for (int e0 = 0; e0 < E; e0 += 32) {
+    const int e = e0 + el;
+    double acc = 0.0;
+    if (e < E) {
+      const float* t = t_emb + (int64_t)b * d;
+      const float* w = w_r + (int64_t)d * E + e;
+#pragma unroll 8
+      for (int k = ks; k < d; k += 8) acc = fma((double)t[k], (double)w[(int64_t)k * E], acc);
+    }
+    part[ks][el] = acc;
+    __syncthreads();
+    if (ks == 0 && e < E) {
+      double s = part[0][el];
+      for (int j = 1; j < 8; ++j) s += part[j][el];
+      tb[(int64_t)b * E + e] = s;
+    }
+    __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ router
-// CTA = TM tokens x all E experts; thread = 4 tokens x 4 experts of f64
-// accumulators. K staged through smem in KC-chunks as f64.
+// FP64-pipe bound GEMM-let: logits[t, e] = sum_k x[t, k] * W[k, e] + tb[b, e].
+// CTA = TM tokens x EP experts, thread = 4 tokens (strided by TG) x 8 experts
+// (pairs strided by 2*EG) of f64 accumulators, so every shared load of a warp
+// is a single conflict-free wavefront. K is staged in KC-chunks, double
+// buffered: W (pre-converted f64) by cp.async, x by a register prefetch that
+// is converted to f64 once per element.
 constexpr int RT_THREADS = 128;
 constexpr int RT_KC = 32;
+constexpr int RT_XS = RT_KC + 2;  // x row stride (doubles): 272 B == 16 mod 128
 
 struct RouterGeom {
-  int EG, TG, TM, EP;
+  int EG, TG, TM, EP, NT;
 };
 __host__ __device__ inline RouterGeom router_geom(int E) {
   RouterGeom g;
-  g.EG = (E + 3) / 4;
+  g.EG = (E + 7) / 8;
+  g.EP = g.EG * 8;
   g.TG = RT_THREADS / g.EG;
+  if (g.TG > 16) g.TG = 16;
+  if (g.TG < 1) g.TG = 1;
   g.TM = g.TG * 4;
-  g.EP = g.EG * 4;
+  g.NT = g.EG * g.TG;
   return g;
 }
+__host__ __device__ inline size_t router_stage_bytes(const RouterGeom& g) {
+  return (size_t)RT_KC * g.EP * 8 + (size_t)g.TM * RT_XS * 8;
+}
 __host__ __device__ inline size_t router_smem(int E) {
-  RouterGeom g = router_geom(E);
-  size_t loop = (size_t)RT_KC * g.TM * 8 + (size_t)RT_KC * g.EP * 8;
-  size_t post = (size_t)g.TM * E * 8 + (size_t)g.TM * E * 4;  // ex (f64) + sc (f32)
-  size_t r1 = loop > post ? loop : post;
-  return r1 + (size_t)g.TM * E * 4 /*lg*/ + (size_t)g.TM * 16 /*mx, sum*/;
+  const RouterGeom g = router_geom(E);
+  const size_t stage = 2 * router_stage_bytes(g);
+  const size_t post = (size_t)g.TM * E * (8 + 4 + 4);  // ex (f64) + sc + lg (f32)
+  return (stage > post ? stage : post) + (size_t)g.TM * 16;
 }
 
+NIMG_DEV void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+NIMG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> NIMG_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename TX> struct XVec;
+template <> struct XVec<bf16> { static constexpr int N = 8; };
+template <> struct XVec<float> { static constexpr int N = 4; };
+
 template <typename TX>
+NIMG_DEV void cvt_store_x(double* dst, const uint4& v) {
+  if constexpr (sizeof(TX) == 2) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const double lo = (double)__uint_as_float(w[q] << 16);
+      const double hi = (double)__uint_as_float(w[q] & 0xFFFF0000u);
+      *reinterpret_cast<double2*>(dst + 2 * q) = make_double2(lo, hi);
+    }
+  } else {
+    *reinterpret_cast<double2*>(dst) = make_double2((double)__uint_as_float(v.x), (double)__uint_as_float(v.y));
+    *reinterpret_cast<double2*>(dst + 2) = make_double2((double)__uint_as_float(v.z), (double)__uint_as_float(v.w));
+  }
+}
+
+template <typename TX, bool VEC>
 __global__ void __launch_bounds__(RT_THREADS)
-router_scores_kernel(const TX* __restrict__ x, const float* __restrict__ w_r,
+router_scores_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
                      const double* __restrict__ tb, float* __restrict__ logits,
                      float* __restrict__ scores_bes, int B, int S, int d, int E) {
   extern __shared__ __align__(16) uint8_t sm[];
   const RouterGeom g = router_geom(E);
+  constexpr int XV = XVec<TX>::N;            // elements per 16-B vector
+  constexpr int VPR = RT_KC / XV;            // vectors per token row per chunk
   const int64_t T = (int64_t)B * S;
   const int64_t t0 = (int64_t)blockIdx.x * g.TM;
-  double* xs = reinterpret_cast<double*>(sm);            // [KC][TM]
-  double* ws = xs + RT_KC * g.TM;                        // [KC][EP]
-  const size_t r1 = router_smem(E) - (size_t)g.TM * E * 4 - (size_t)g.TM * 16;
-  float* lg = reinterpret_cast<float*>(sm + r1);         // [TM][E]
-  double* mx = reinterpret_cast<double*>(sm + r1 + (size_t)g.TM * E * 4);
-  double* sum = mx + g.TM;
-  double* ex = reinterpret_cast<double*>(sm);            // [TM][E]  (reuses loop region)
-  float* sc = reinterpret_cast<float*>(sm + (size_t)g.TM * E * 8);  // [TM][E]
+  const size_t SB = router_stage_bytes(g);
+  auto wsb = [&](int buf) { return reinterpret_cast<double*>(sm + buf * SB); };
+  auto xsb = [&](int buf) { return reinterpret_cast<double*>(sm + buf * SB + (size_t)RT_KC * g.EP * 8); };
 
   const int tid = threadIdx.x;
-  const bool active = tid < g.TG * g.EG;
+  const bool active = tid < g.NT;
   const int tg = active ? tid / g.EG : 0, eg = active ? tid % g.EG : 0;
+  const int nvec_x = g.TM * VPR;             // x vectors per chunk
+  const int nvec_w = RT_KC * g.EP / 2;       // 16-B W vectors per chunk
+  const int nc = (d + RT_KC - 1) / RT_KC;
 
-  double acc[4][4];
+  // x prefetch registers: TM <= 64 tokens x RT_KC / XV vectors over RT_THREADS threads
+  constexpr int XR = 64 * RT_KC / XV / RT_THREADS;
+  uint4 xr[XR];
+  auto load_x = [&](int c) {
+    const int k0 = c * RT_KC;
+#pragma unroll
+    for (int r = 0; r < XR; ++r) {
+      const int i = tid + r * RT_THREADS;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (i < nvec_x) {
+        const int tok = i / VPR, kv = i % VPR;
+        const int64_t t = t0 + tok;
+        const int k = k0 + kv * XV;
+        if (t < T) {
+          if (VEC) {
+            if (k < d) v = __ldg(reinterpret_cast<const uint4*>(x + t * d + k));
+          } else {
+            TX tmp[XV];
+#pragma unroll
+            for (int q = 0; q < XV; ++q) tmp[q] = (k + q < d) ? x[t * d + k + q] : from_f32<TX>(0.f);
+            v = *reinterpret_cast<uint4*>(tmp);
+          }
+        }
+      }
+      xr[r] = v;
+    }
+  };
+  auto store_x = [&](int buf) {
+    double* xs = xsb(buf);
+#pragma unroll
+    for (int r = 0; r < XR; ++r) {
+      const int i = tid + r * RT_THREADS;
+      if (i < nvec_x) {
+        const int tok = i / VPR, kv = i % VPR;
+        cvt_store_x<TX>(xs + tok * RT_XS + kv * XV, xr[r]);
+      }
+    }
+  };
+  auto load_w = [&](int c, int buf) {
+    const int k0 = c * RT_KC;
+    double* ws = wsb(buf);
+    for (int i = tid; i < nvec_w; i += RT_THREADS) {
+      const int kk = (2 * i) / g.EP, e = (2 * i) % g.EP;
+      if (k0 + kk < d) cp_async16(ws + kk * g.EP + e, wd + (int64_t)(k0 + kk) * g.EP + e);
+      else *reinterpret_cast<double2*>(ws + kk * g.EP + e) = make_double2(0.0, 0.0);
+    }
+  };
+
+  double acc[4][8];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
 
-  for (int k0 = 0; k0 < d; k0 += RT_KC) {
-    for (int i = tid; i < g.TM * RT_KC; i += RT_THREADS) {
-      const int tok = i / RT_KC, kk = i % RT_KC;
-      const int64_t t = t0 + tok;
-      double v = 0.0;
-      if (t < T && k0 + kk < d) v = (double)to_f32(x[t * d + k0 + kk]);
-      xs[kk * g.TM + tok] = v;
+  load_x(0);
+  load_w(0, 0);
+  cp_async_commit();
+  store_x(0);
+  for (int c = 0; c < nc; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nc) {
+      load_x(c + 1);
+      load_w(c + 1, buf ^ 1);
     }
-    for (int i = tid; i < RT_KC * g.EP; i += RT_THREADS) {
-      const int kk = i / g.EP, e = i % g.EP;
-      double v = 0.0;
-      if (e < E && k0 + kk < d) v = (double)w_r[(int64_t)(k0 + kk) * E + e];
-      ws[kk * g.EP + e] = v;
-    }
+    cp_async_commit();
+    cp_async_wait<1>();
     __syncthreads();
     if (active) {
-      const int kmax = min(RT_KC, d - k0);
-      for (int kk = 0; kk < kmax; ++kk) {
-        const double2 xa = *reinterpret_cast<const double2*>(&xs[kk * g.TM + tg * 4]);
-        const double2 xb = *reinterpret_cast<const double2*>(&xs[kk * g.TM + tg * 4 + 2]);
-        const double2 wa = *reinterpret_cast<const double2*>(&ws[kk * g.EP + eg * 4]);
-        const double2 wb = *reinterpret_cast<const double2*>(&ws[kk * g.EP + eg * 4 + 2]);
-        const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
-        const double wv[4] = {wa.x, wa.y, wb.x, wb.y};
+      const double* xs = xsb(buf);
+      const double* ws = wsb(buf);
+#pragma unroll 4
+      for (int kk = 0; kk < RT_KC; kk += 2) {
+        double2 xv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          xv[i] = *reinterpret_cast<const double2*>(xs + (tg + g.TG * i) * RT_XS + kk);
+        double2 w0[4], w1[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          w0[q] = *reinterpret_cast<const double2*>(ws + kk * g.EP + 2 * eg + 2 * g.EG * q);
+          w1[q] = *reinterpret_cast<const double2*>(ws + (kk + 1) * g.EP + 2 * eg + 2 * g.EG * q);
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(xv[i], wv[j], acc[i][j]);
+          for (int q = 0; q < 4; ++q) {
+            acc[i][2 * q] = fma(xv[i].x, w0[q].x, acc[i][2 * q]);
+            acc[i][2 * q + 1] = fma(xv[i].x, w0[q].y, acc[i][2 * q + 1]);
+            acc[i][2 * q] = fma(xv[i].y, w1[q].x, acc[i][2 * q]);
+            acc[i][2 * q + 1] = fma(xv[i].y, w1[q].y, acc[i][2 * q + 1]);
+          }
       }
     }
+    if (c + 1 < nc) store_x(buf ^ 1);
     __syncthreads();
   }
 
-  // logits = fp32(x-part + t-part)   (matmul f64 -> fp32, tensor.py:286-287)
+  // ---- epilogue (reuses the staging smem): fp32 logits, f64 softmax
+  double* ex = reinterpret_cast<double*>(sm);                           // [TM][E]
+  float* sc = reinterpret_cast<float*>(sm + (size_t)g.TM * E * 8);      // [TM][E]
+  float* lg = sc + (size_t)g.TM * E;                                    // [TM][E]
+  double* mx = reinterpret_cast<double*>(sm + (router_smem(E) - (size_t)g.TM * 16));
+  double* sum = mx + g.TM;
   if (active) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int tok = tg * 4 + i;
+      const int tok = tg + g.TG * i;
       const int64_t t = t0 + tok;
       if (t >= T) continue;
-      const int b = (int)(t / S);
+      const int64_t b = t / S;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int e = eg * 4 + j;
-        if (e < E) lg[tok * E + e] = (float)(acc[i][j] + tb[(int64_t)b * E + e]);
+      for (int j = 0; j < 8; ++j) {
+        const int e = 2 * eg + 2 * g.EG * (j >> 1) + (j & 1);
+        // matmul f64 -> fp32 (tensor.py:286-287)
+        if (e < E) lg[tok * E + e] = (float)(acc[i][j] + tb[b * E + e]);
       }
     }
   }
   __syncthreads();
-  // row max (exact in any order)
   for (int tok = tid; tok < g.TM; tok += RT_THREADS) {
     double m = -INFINITY;
     for (int e = 0; e < E; ++e) m = fmax(m, (double)lg[tok * E + e]);
     mx[tok] = m;
   }
   __syncthreads();
-  for (int i = tid; i < g.TM * E; i += RT_THREADS) {
-    const int tok = i / E;
-    ex[i] = exp((double)lg[i] - mx[tok]);
-  }
+  for (int i = tid; i < g.TM * E; i += RT_THREADS) ex[i] = exp((double)lg[i] - mx[i / E]);
   __syncthreads();
   for (int tok = tid; tok < g.TM; tok += RT_THREADS) sum[tok] = np_pairwise_sum(ex + tok * E, E);
   __syncthreads();
-  for (int i = tid; i < g.TM * E; i += RT_THREADS) {
-    const int tok = i / E;
-    sc[i] = (float)(ex[i] / sum[tok]);
-  }
+  for (int i = tid; i < g.TM * E; i += RT_THREADS) sc[i] = (float)(ex[i] / sum[i / E]);
   __syncthreads();
-  // logits (B,S,E): contiguous run of TM*E floats
   for (int i = tid; i < g.TM * E; i += RT_THREADS) {
     const int64_t t = t0 + i / E;
     if (t < T) logits[t * E + (i % E)] = lg[i];
   }
-  // scores transposed to (B,E,S): coalesced along tokens
   for (int i = tid; i < g.TM * E; i += RT_THREADS) {
     const int e = i / g.TM, tok = i % g.TM;
     const int64_t t = t0 + tok;
@@ -358,42 +467,54 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
     const int64_t o = ((int64_t)e * B + b) * cap + j;
     token_flat[o] = (int32_t)((int64_t)b * S + idx);
     gate_raw[o] = col[idx];
-    slot_of[(int64_t)e * T + (int64_t)b * S + idx] = (int16_t)j;
+    slot_of[((int64_t)b * S + idx) * E + e] = (int16_t)j;
   }
 }
 
 // ------------------------------------------------------------------ gates
-// Per token (router.py:137-143): totals = fp32(sum_e f64(raw)) in expert order
-// (np.add.at order), den = fp32(f64(tot) + f64(fp32 eps)),
-// gate = fp32(f64(fp32(f64(raw) / f64(den))) * f64(fp32 alpha)).
-__global__ void gate_norm_kernel(const float* __restrict__ scores_bes,
-                                 const int16_t* __restrict__ slot_of, float* __restrict__ gates,
-                                 int32_t* __restrict__ comb_rows, int32_t* __restrict__ comb_cnt,
-                                 int B, int S, int E, int cap, float eps32, float alpha32) {
+// Warp per token (router.py:137-143): the experts that picked the token, in
+// ascending order (ballot + prefix), totals = fp32(sequential f64 sum in that
+// order -- np.add.at order), den = fp32(f64(tot) + f64(fp32 eps)),
+// gate = fp32(f64(fp32(f64(raw) / f64(den))) * f64(fp32 alpha)). Also emits
+// the per-token combine list (rows of the expert-major flat order).
+constexpr int GN_WARPS = 8;
+__global__ void __launch_bounds__(GN_WARPS * 32)
+gate_norm_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict__ slot_of,
+                 float* __restrict__ gates, int32_t* __restrict__ comb_rows,
+                 int32_t* __restrict__ comb_cnt, int B, int S, int E, int cap, float eps32,
+                 float alpha32) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* raw_l = reinterpret_cast<float*>(sm) + (size_t)warp * E;
+  int32_t* row_l = reinterpret_cast<int32_t*>(sm + (size_t)GN_WARPS * E * 4) + (size_t)warp * E;
   const int64_t T = (int64_t)B * S;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t t = (int64_t)blockIdx.x * GN_WARPS + warp;
   if (t >= T) return;
   const int64_t b = t / S, s = t % S;
-  double tot = 0.0;
   int cnt = 0;
-  for (int e = 0; e < E; ++e) {
-    const int j = slot_of[(int64_t)e * T + t];
+  for (int e0 = 0; e0 < E; e0 += 32) {
+    const int e = e0 + lane;
+    const int j = e < E ? (int)slot_of[t * E + e] : -1;
+    const unsigned m = __ballot_sync(0xffffffffu, j >= 0);
     if (j >= 0) {
-      tot += (double)scores_bes[(b * E + e) * S + s];
-      comb_rows[(int64_t)cnt * T + t] = (int32_t)(((int64_t)e * B + b) * cap + j);
-      ++cnt;
+      const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+      raw_l[pos] = scores_bes[(b * E + e) * S + s];
+      row_l[pos] = (int32_t)(((int64_t)e * B + b) * cap + j);
     }
+    cnt += __popc(m);
   }
-  comb_cnt[t] = cnt;
-  const float tot32 = (float)tot;
+  __syncwarp();
+  double tot = 0.0;
+  if (lane == 0)
+    for (int k = 0; k < cnt; ++k) tot += (double)raw_l[k];
+  const float tot32 = __shfl_sync(0xffffffffu, (float)tot, 0);
   const float den = (float)((double)tot32 + (double)eps32);
-  for (int k = 0; k < cnt; ++k) {
-    const int32_t row = comb_rows[(int64_t)k * T + t];
-    const int e = (int)(row / ((int64_t)B * cap));
-    const float raw = scores_bes[(b * E + e) * S + s];
-    const float q = (float)((double)raw / (double)den);
-    gates[row] = (float)((double)q * (double)alpha32);
+  for (int k = lane; k < cnt; k += 32) {
+    const float q = (float)((double)raw_l[k] / (double)den);
+    gates[row_l[k]] = (float)((double)q * (double)alpha32);
+    comb_rows[t * E + k] = row_l[k];
   }
+  if (lane == 0) comb_cnt[t] = cnt;
 }
 
 // ------------------------------------------------------------------ gather
@@ -425,64 +546,95 @@ __global__ void gather_rows_byte_kernel(const uint8_t* __restrict__ src, int64_t
 // ------------------------------------------------------------------ combine
 // moe.py:156-161 with the reference's rounding chain: gated = fp32(Y*gate),
 // combined = fp32(sum over selecting experts in ascending order, f64),
-// out = round(f64(combined) + f64(shared)).
+// out = round(f64(combined) + f64(shared)). Warp per token; the token's row
+// list and gates are staged in smem, then every lane streams VEC-element
+// vectors of all its rows (independent loads -> memory-level parallelism).
+constexpr int CB_WARPS = 8;
 template <typename TY, typename TO, int VEC>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(CB_WARPS * 32)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
-               TO* __restrict__ out, int64_t T, int d) {
-  const int64_t t = blockIdx.x;
+               TO* __restrict__ out, int64_t T, int d, int E) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* rows = reinterpret_cast<int32_t*>(sm) + (size_t)warp * E;
+  float* gl = reinterpret_cast<float*>(sm + (size_t)CB_WARPS * E * 4) + (size_t)warp * E;
+  const int64_t t = (int64_t)blockIdx.x * CB_WARPS + warp;
+  if (t >= T) return;
   const int cnt = comb_cnt[t];
-  for (int c = threadIdx.x * VEC; c < d; c += blockDim.x * VEC) {
+  for (int k = lane; k < cnt; k += 32) {
+    const int32_t r = comb_rows[t * E + k];
+    rows[k] = r;
+    gl[k] = gates[r];
+  }
+  __syncwarp();
+  for (int c = lane * VEC; c < d; c += 32 * VEC) {
     double acc[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-    for (int k = 0; k < cnt; ++k) {
-      const int32_t row = comb_rows[(int64_t)k * T + t];
-      const float gte = gates[row];
-      const TY* y = yr + (int64_t)row * d + c;
+    int k = 0;
+    for (; k + 2 <= cnt; k += 2) {
+      TY y0[VEC], y1[VEC];
+      const TY* p0 = yr + (int64_t)rows[k] * d + c;
+      const TY* p1 = yr + (int64_t)rows[k + 1] * d + c;
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[v] += (double)(to_f32(y[v]) * gte);
+      for (int v = 0; v < VEC; ++v) { y0[v] = p0[v]; y1[v] = p1[v]; }
+      const float g0 = gl[k], g1 = gl[k + 1];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) {
+        acc[v] += (double)(to_f32(y0[v]) * g0);
+        acc[v] += (double)(to_f32(y1[v]) * g1);
+      }
+    }
+    for (; k < cnt; ++k) {
+      const TY* p = yr + (int64_t)rows[k] * d + c;
+      const float gk = gl[k];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) acc[v] += (double)(to_f32(p[v]) * gk);
     }
     const TY* sh = ys + t * d + c;
     TO* o = out + t * d + c;
+    TO res[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       const float comb = (float)acc[v];
-      o[v] = from_f32<TO>((float)((double)comb + (double)to_f32(sh[v])));
+      res[v] = from_f32<TO>((float)((double)comb + (double)to_f32(sh[v])));
     }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) o[v] = res[v];
   }
 }
 
 // ------------------------------------------------------------------ launchers
-cudaError_t launch_router_tbias(const float* t_emb, const float* w_r, double* tb, int B, int d,
-                                int E, cudaStream_t s) {
-  dim3 grid(B, (E + 31) / 32);
-  router_tbias_kernel<<<grid, 256, 0, s>>>(t_emb, w_r, tb, d, E);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_router_scores(bool x_bf16, const void* x_norm, const float* w_r,
-                                 const double* tb, float* logits, float* scores_bes, int B, int S,
-                                 int d, int E, cudaStream_t s) {
+cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
+                          double* tb, double* wd, float* logits, float* scores_bes, int B, int S,
+                          int d, int E, cudaStream_t s) {
   const RouterGeom g = router_geom(E);
+  router_prep_kernel<<<B + 64, 256, 0, s>>>(t_emb, w_r, tb, wd, B, d, E, g.EP);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
   const int64_t T = (int64_t)B * S;
   const int grid = (int)((T + g.TM - 1) / g.TM);
   const size_t smem = router_smem(E);
-  cudaError_t err;
+  const bool vec = (d % 8 == 0) && ((uintptr_t)x_norm % 16 == 0);
+#define NIMG_ROUTER_LAUNCH(TX, V)                                                              \
+  do {                                                                                         \
+    err = cudaFuncSetAttribute(router_scores_kernel<TX, V>,                                    \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    if (err != cudaSuccess) return err;                                                        \
+    router_scores_kernel<TX, V><<<grid, RT_THREADS, smem, s>>>(                                \
+        reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d, E);          \
+  } while (0)
   if (x_bf16) {
-    err = cudaFuncSetAttribute(router_scores_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    router_scores_kernel<bf16><<<grid, RT_THREADS, smem, s>>>(
-        reinterpret_cast<const bf16*>(x_norm), w_r, tb, logits, scores_bes, B, S, d, E);
+    if (vec) NIMG_ROUTER_LAUNCH(bf16, true); else NIMG_ROUTER_LAUNCH(bf16, false);
   } else {
-    err = cudaFuncSetAttribute(router_scores_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    router_scores_kernel<float><<<grid, RT_THREADS, smem, s>>>(
-        reinterpret_cast<const float*>(x_norm), w_r, tb, logits, scores_bes, B, S, d, E);
+    if (vec && d % 4 == 0) NIMG_ROUTER_LAUNCH(float, true); else NIMG_ROUTER_LAUNCH(float, false);
   }
+#undef NIMG_ROUTER_LAUNCH
   return cudaGetLastError();
 }
+
+size_t router_wd_bytes(int d, int E) { return (size_t)d * router_geom(E).EP * 8; }
 
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s) {
@@ -499,9 +651,10 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
                              int32_t* comb_rows, int32_t* comb_cnt, int B, int S, int E, int cap,
                              float gate_eps, float gate_scale, cudaStream_t s) {
   const int64_t T = (int64_t)B * S;
-  const int grid = (int)((T + 127) / 128);
-  gate_norm_kernel<<<grid, 128, 0, s>>>(scores_bes, slot_of, gates, comb_rows, comb_cnt, B, S, E,
-                                        cap, gate_eps, gate_scale);
+  const int grid = (int)((T + GN_WARPS - 1) / GN_WARPS);
+  const size_t smem = (size_t)GN_WARPS * E * 8;
+  gate_norm_kernel<<<grid, GN_WARPS * 32, smem, s>>>(scores_bes, slot_of, gates, comb_rows,
+                                                      comb_cnt, B, S, E, cap, gate_eps, gate_scale);
   return cudaGetLastError();
 }
 
@@ -524,23 +677,25 @@ cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t
 template <typename TY, typename TO>
 static void combine_dispatch(const void* yr, const void* ys, const float* gates,
                              const int32_t* rows, const int32_t* cnt, void* out, int64_t T, int d,
-                             cudaStream_t s) {
+                             int E, cudaStream_t s) {
+  const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
+  const size_t smem = (size_t)CB_WARPS * E * 8;
   if (d % 8 == 0)
-    combine_kernel<TY, TO, 8><<<(unsigned)T, 256, 0, s>>>(
-        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d);
+    combine_kernel<TY, TO, 8><<<grid, CB_WARPS * 32, smem, s>>>(
+        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
   else
-    combine_kernel<TY, TO, 1><<<(unsigned)T, 256, 0, s>>>(
-        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d);
+    combine_kernel<TY, TO, 1><<<grid, CB_WARPS * 32, smem, s>>>(
+        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
 }
 
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
-                           void* out, int64_t T, int d, cudaStream_t s) {
+                           void* out, int64_t T, int d, int E, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
-  if (y_bf16 && out_bf16) combine_dispatch<bf16, bf16>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, s);
-  else if (y_bf16) combine_dispatch<bf16, float>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, s);
-  else if (out_bf16) combine_dispatch<float, bf16>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, s);
-  else combine_dispatch<float, float>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, s);
+  if (y_bf16 && out_bf16) combine_dispatch<bf16, bf16>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
+  else if (y_bf16) combine_dispatch<bf16, float>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
+  else if (out_bf16) combine_dispatch<float, bf16>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
+  else combine_dispatch<float, float>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
   return cudaGetLastError();
 }
 

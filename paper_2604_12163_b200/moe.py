@@ -183,3 +183,56 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
         decisions, routing = build_routing(r, B, S, E, cap)
         return out, decisions, routing
     return out
+
+
+class MoEPlan:
+    """Pre-planned MoE layer for a fixed problem shape (serving / benchmark path).
+
+    Owns the workspace, output and routing buffers so a forward is one C-ABI
+    call (`nimg_moe_forward`) with no allocation; `capture()` records that call
+    in a CUDA graph on static input buffers. Same arithmetic as moe_forward.
+    """
+
+    def __init__(self, cfg: RouterConfig, bank: ExpertBank, B: int, S: int,
+                 act: torch.dtype = torch.bfloat16):
+        self.cfg, self.B, self.S, self.act = cfg, B, S, act
+        d, E = cfg.d_model, cfg.n_experts
+        self.bank = bank.on_device(act)
+        _, self.h, self.hs = _check_bank_shapes(self.bank.w1, self.bank.w3, self.bank.w2,
+                                                self.bank.shared_w1, self.bank.shared_w3,
+                                                self.bank.shared_w2, d)
+        self.cap = capacity_for(S, E, cfg.capacity_factor)
+        self.desc = make_desc(B, S, d, E, self.cap, self.h, self.hs, cfg, act)
+        nbytes = C.c_size_t()
+        _lib.check(_lib.lib.nimg_moe_workspace_bytes(C.byref(self.desc), C.byref(nbytes)))
+        self.ws = workspace(nbytes.value)
+        dev = self.ws.device
+        self.out = torch.empty((B, S, d), dtype=act, device=dev)
+        self.r = alloc_route_out(B, S, E, self.cap, dev)
+        self.graph = None
+
+    def _ptrs(self, x_norm, x_mod, t_emb, w_r):
+        w = self.bank
+        return _lib.MoePtrs(ptr(x_norm), ptr(x_mod), ptr(t_emb), ptr(w_r), ptr(w.w1), ptr(w.w3),
+                            ptr(w.w2), ptr(w.shared_w1), ptr(w.shared_w3), ptr(w.shared_w2),
+                            ptr(self.out), route_struct(self.r))
+
+    def forward(self, x_norm, x_mod, t_emb, w_r) -> torch.Tensor:
+        """Inputs must already be contiguous CUDA tensors of the plan's dtypes
+        (x_norm/x_mod act dtype, t_emb/w_r fp32). Returns the plan's out buffer."""
+        p = self._ptrs(x_norm, x_mod, t_emb, w_r)
+        _lib.check(_lib.lib.nimg_moe_forward(C.byref(self.desc), C.byref(p), ptr(self.ws),
+                                             self.ws.numel(), stream_handle()))
+        return self.out
+
+    def capture(self, x_norm, x_mod, t_emb, w_r) -> "torch.cuda.CUDAGraph":
+        """Record forward() on these (static) input buffers into a CUDA graph."""
+        self.forward(x_norm, x_mod, t_emb, w_r)  # warm (attributes, tensor-map fn)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.forward(x_norm, x_mod, t_emb, w_r)
+        self.graph = g
+        return g
+
+    def routing(self, with_decisions: bool = False):
+        return build_routing(self.r, self.B, self.S, self.cfg.n_experts, self.cap, with_decisions)

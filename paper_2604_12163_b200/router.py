@@ -106,7 +106,7 @@ def alloc_route_out(B: int, S: int, E: int, cap: int, dev) -> dict:
         "token_flat": torch.empty(n, dtype=i32, device=dev),
         "gate_raw": torch.empty(n, dtype=f32, device=dev),
         "gates": torch.empty(n, dtype=f32, device=dev),
-        "comb_rows": torch.empty((E, B * S), dtype=i32, device=dev),
+        "comb_rows": torch.empty((B * S, E), dtype=i32, device=dev),
         "comb_cnt": torch.empty(B * S, dtype=i32, device=dev),
     }
 
