@@ -138,23 +138,34 @@ int check_moe_desc(const nimg_moe_desc* d) {
   return NIMG_OK;
 }
 
+// Route scratch. `counters` (B u32) sits right after slot_of so a single
+// 0xFF memset arms both: slot_of = -1 ("not selected"), counters = 0xFFFFFFFF.
 struct RouteWs {
   double* tb;
+  double* part;
   double* wd;
   int16_t* slot_of;
+  unsigned* counters;
 };
+size_t slot_bytes(const nimg_moe_desc* d) { return (size_t)d->E * d->B * d->S * 2; }
 size_t route_ws_bytes(const nimg_moe_desc* d) {
-  return align_up((size_t)d->B * d->E * 8) + align_up(router_wd_bytes((int)d->d, (int)d->E)) +
-         align_up((size_t)d->E * d->B * d->S * 2);
+  return align_up((size_t)d->B * d->E * 8) +
+         align_up(router_part_bytes((int)d->B, (int)d->d, (int)d->E)) +
+         align_up(router_wd_bytes((int)d->d, (int)d->E)) + align_up(slot_bytes(d)) +
+         align_up((size_t)d->B * 4);
 }
 RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
   RouteWs r;
   r.tb = reinterpret_cast<double*>(p);
   p += align_up((size_t)d->B * d->E * 8);
+  r.part = reinterpret_cast<double*>(p);
+  p += align_up(router_part_bytes((int)d->B, (int)d->d, (int)d->E));
   r.wd = reinterpret_cast<double*>(p);
   p += align_up(router_wd_bytes((int)d->d, (int)d->E));
   r.slot_of = reinterpret_cast<int16_t*>(p);
+  p += align_up(slot_bytes(d));
+  r.counters = reinterpret_cast<unsigned*>(p);
   return r;
 }
 
@@ -335,11 +346,14 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
   if (!x_norm || !t_emb || !w_r) return fail(NIMG_ERR_SHAPE, "null input pointer");
   if (!ws || ws_bytes < route_ws_bytes(d)) return fail(NIMG_ERR_CONFIG, "workspace too small");
   const int B = (int)d->B, S = (int)d->S, dd = (int)d->d, E = (int)d->E, cap = (int)d->cap;
-  const int64_t T = d->B * d->S;
   RouteWs w = carve_route(d, ws);
-  CUDA_TRY(launch_router(d->act_dtype == NIMG_BF16, x_norm, t_emb, w_r, w.tb, w.wd, o->logits,
-                         o->scores_bes, B, S, dd, E, st));
-  CUDA_TRY(cudaMemsetAsync(w.slot_of, 0xFF, (size_t)E * T * 2, st));
+  // One memset arms the slot table (-1) and the prep kernel's per-sample
+  // completion counters (0xFFFFFFFF); the workspace is caller-owned.
+  CUDA_TRY(cudaMemsetAsync(w.slot_of, 0xFF,
+                           (size_t)(reinterpret_cast<uint8_t*>(w.counters) -
+                                    reinterpret_cast<uint8_t*>(w.slot_of)) + (size_t)B * 4, st));
+  CUDA_TRY(launch_router(d->act_dtype == NIMG_BF16, x_norm, t_emb, w_r, w.tb, w.part, w.counters,
+                         w.wd, o->logits, o->scores_bes, B, S, dd, E, st));
   CUDA_TRY(launch_ec_select(o->scores_bes, o->token_flat, o->gate_raw, w.slot_of, B, S, E, cap, st));
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
   CUDA_TRY(launch_gate_norm(o->scores_bes, w.slot_of, o->gates, o->comb_rows, o->comb_cnt, B, S,

@@ -70,10 +70,13 @@ cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cud
 
 // routing / data-movement kernels (route_kernels.cu)
 // router prep (t-half bias + f64 copy of W_r[:d]) and FP64 scores kernel
+// counters: B unsigned per-sample completion counters, 0xFFFFFFFF on entry
+// (re-armed by the kernel).
 cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
-                          double* tb, double* wd, float* logits, float* scores_bes, int B, int S,
-                          int d, int E, cudaStream_t s);
+                          double* tb, double* part, unsigned* counter, double* wd, float* logits,
+                          float* scores_bes, int B, int S, int d, int E, cudaStream_t s);
 size_t router_wd_bytes(int d, int E);
+size_t router_part_bytes(int B, int d, int E);
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s);
 cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,

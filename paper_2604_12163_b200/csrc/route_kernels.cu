@@ -13,6 +13,8 @@
 //   gather_rows    x_mod rows into expert-major order (moe.py:152-153).
 //   combine        deterministic expert-ascending weighted sum + shared expert
 //                  (moe.py:156-161, tensor.py:366-378).
+#include <type_traits>
+
 #include "common.cuh"
 #include "nimg_internal.h"
 
@@ -48,42 +50,54 @@ __device__ double np_pairwise_sum(const double* a, int n) {
 // ------------------------------------------------------------------ router prep
 // (a) wd[k, e] = f64(W_r[k, e]) for the x half (k < d), E padded to EP;
 // (b) tb[b, e] = sum_k t_emb[b, k] * W_r[d + k, e] in f64 (the t half of the
-//     concatenated router input, router.py:120-122). Block (b, 32 experts),
-//     8 k-slices per expert folded in a fixed order.
-__global__ void router_prep_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
-                                   double* __restrict__ tb, double* __restrict__ wd, int B, int d,
-                                   int E, int EP) {
-  if (blockIdx.x >= B) {
+//     concatenated router input, router.py:120-122). Block (chunk c, sample b)
+//     folds one 64-row k-chunk into part[b, c, e]; the last of a sample's nkc
+//     blocks (per-sample counter, armed to 0xFFFFFFFF by the caller's memset)
+//     sums its chunks in ascending order -- deterministic -- and re-arms.
+constexpr int RP_KCH = 64;
+constexpr int RP_CONV_BLOCKS = 32;
+__global__ void __launch_bounds__(64)
+router_prep_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
+                   double* __restrict__ tb, double* __restrict__ part, double* __restrict__ wd,
+                   unsigned* __restrict__ counters, int B, int d, int E, int EP) {
+  const int nkc = (d + RP_KCH - 1) / RP_KCH;
+  if ((int)blockIdx.x >= nkc) {  // conversion blocks: grid.x == nkc + RP_CONV_BLOCKS
     const int64_t n = (int64_t)d * EP;
-    for (int64_t i = (int64_t)(blockIdx.x - B) * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)(gridDim.x - B) * blockDim.x) {
+    const int64_t stride = (int64_t)RP_CONV_BLOCKS * gridDim.y * blockDim.x;
+    for (int64_t i = ((int64_t)(blockIdx.x - nkc) * gridDim.y + blockIdx.y) * blockDim.x + threadIdx.x;
+         i < n; i += stride) {
       const int64_t k = i / EP;
       const int e = (int)(i % EP);
       wd[i] = e < E ? (double)w_r[k * E + e] : 0.0;
     }
     return;
   }
-  __shared__ double part[8][32];
-  const int b = blockIdx.x;
-  const int el = threadIdx.x & 31, ks = threadIdx.x >> 5;
-  for (int e0 = 0; e0 < E; e0 += 32) {
-    const int e = e0 + el;
+  const int c = blockIdx.x, b = blockIdx.y;
+  const int k0 = c * RP_KCH, k1 = min(d, k0 + RP_KCH);
+  __shared__ float ts[RP_KCH];
+  for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) ts[k - k0] = t_emb[(int64_t)b * d + k];
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
     double acc = 0.0;
-    if (e < E) {
-      const float* t = t_emb + (int64_t)b * d;
-      const float* w = w_r + (int64_t)d * E + e;
-#pragma unroll 8
-      for (int k = ks; k < d; k += 8) acc = fma((double)t[k], (double)w[(int64_t)k * E], acc);
-    }
-    part[ks][el] = acc;
-    __syncthreads();
-    if (ks == 0 && e < E) {
-      double s = part[0][el];
-      for (int j = 1; j < 8; ++j) s += part[j][el];
-      tb[(int64_t)b * E + e] = s;
-    }
-    __syncthreads();
+    const float* w = w_r + (int64_t)(d + k0) * E + e;
+#pragma unroll 16
+    for (int k = 0; k < k1 - k0; ++k) acc = fma((double)ts[k], (double)w[(int64_t)k * E], acc);
+    part[((int64_t)b * nkc + c) * E + e] = acc;
   }
+  __threadfence();
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(&counters[b], 1u) == (unsigned)(nkc - 2);  // from 0xFFFFFFFF
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    const double* pp = part + (int64_t)b * nkc * E + e;
+    double sacc = 0.0;
+    for (int j = 0; j < nkc; ++j) sacc += __ldcg(pp + (int64_t)j * E);
+    tb[(int64_t)b * E + e] = sacc;
+  }
+  if (threadIdx.x == 0) counters[b] = 0xFFFFFFFFu;
 }
 
 // ------------------------------------------------------------------ router
@@ -314,6 +328,176 @@ router_scores_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
   }
 }
 
+// ------------------------------------------------------------------ router (DMMA, E <= 64)
+// Same contraction on the FP64 tensor pipe: mma.sync m8n8k4 f64 (one
+// instruction = 256 f64 FMAs). CTA = 4 warps x 16 tokens, all 64 (padded)
+// experts; warp tile = 2 x 8 fragments of 8x8, 32 f64 accumulators per lane.
+// Staging strides make every fragment load an optimal 2-wavefront LDS.64:
+// x rows of 36 doubles (288 B == 32 mod 128), W rows of 72 doubles (576 B ==
+// 64 mod 128).
+constexpr int DM_TM = 64, DM_KC = 32, DM_XS = 36, DM_WS = 72, DM_EP = 64;
+__host__ __device__ inline size_t dmma_stage_bytes() {
+  return (size_t)DM_KC * DM_WS * 8 + (size_t)DM_TM * DM_XS * 8;
+}
+__host__ __device__ inline size_t dmma_router_smem(int E) {
+  const size_t stage = 2 * dmma_stage_bytes();
+  const size_t post = (size_t)DM_TM * E * (8 + 4 + 4);
+  return (stage > post ? stage : post) + (size_t)DM_TM * 16;
+}
+
+NIMG_DEV void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <typename TX, bool VEC>
+__global__ void __launch_bounds__(128)
+router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
+                          const double* __restrict__ tb, float* __restrict__ logits,
+                          float* __restrict__ scores_bes, int B, int S, int d, int E) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  constexpr int XV = XVec<TX>::N;
+  constexpr int VPR = DM_KC / XV;
+  constexpr int XR = DM_TM * VPR / 128;      // x vectors per thread per chunk
+  constexpr int WR = DM_KC * DM_EP / 2 / 128;  // 16-B W vectors per thread per chunk
+  const int64_t T = (int64_t)B * S;
+  const int64_t t0 = (int64_t)blockIdx.x * DM_TM;
+  const size_t SB = dmma_stage_bytes();
+  auto wsb = [&](int buf) { return reinterpret_cast<double*>(sm + buf * SB); };
+  auto xsb = [&](int buf) { return reinterpret_cast<double*>(sm + buf * SB + (size_t)DM_KC * DM_WS * 8); };
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nc = (d + DM_KC - 1) / DM_KC;
+
+  uint4 xr[XR];
+  auto load_x = [&](int c) {
+    const int k0 = c * DM_KC;
+#pragma unroll
+    for (int r = 0; r < XR; ++r) {
+      const int i = tid + r * 128;
+      const int tok = i / VPR, kv = i % VPR;
+      const int64_t t = t0 + tok;
+      const int k = k0 + kv * XV;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (t < T) {
+        if (VEC) {
+          if (k < d) v = __ldg(reinterpret_cast<const uint4*>(x + t * d + k));
+        } else {
+          TX tmp[XV];
+#pragma unroll
+          for (int q = 0; q < XV; ++q) tmp[q] = (k + q < d) ? x[t * d + k + q] : from_f32<TX>(0.f);
+          v = *reinterpret_cast<uint4*>(tmp);
+        }
+      }
+      xr[r] = v;
+    }
+  };
+  auto store_x = [&](int buf) {
+    double* xs = xsb(buf);
+#pragma unroll
+    for (int r = 0; r < XR; ++r) {
+      const int i = tid + r * 128;
+      cvt_store_x<TX>(xs + (i / VPR) * DM_XS + (i % VPR) * XV, xr[r]);
+    }
+  };
+  auto load_w = [&](int c, int buf) {
+    const int k0 = c * DM_KC;
+    double* ws = wsb(buf);
+#pragma unroll
+    for (int r = 0; r < WR; ++r) {
+      const int i = tid + r * 128;
+      const int kk = i / (DM_EP / 2), e = (i % (DM_EP / 2)) * 2;
+      if (k0 + kk < d) cp_async16(ws + kk * DM_WS + e, wd + (int64_t)(k0 + kk) * DM_EP + e);
+      else *reinterpret_cast<double2*>(ws + kk * DM_WS + e) = make_double2(0.0, 0.0);
+    }
+  };
+
+  double acc[2][8][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int n = 0; n < 8; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+
+  const int ar = lane >> 2, ac = lane & 3;   // A frag: row, k ; B frag: k = ac, col = ar
+  load_x(0);
+  load_w(0, 0);
+  cp_async_commit();
+  store_x(0);
+  for (int c = 0; c < nc; ++c) {
+    const int buf = c & 1;
+    if (c + 1 < nc) {
+      load_x(c + 1);
+      load_w(c + 1, buf ^ 1);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* xs = xsb(buf) + (warp * 16 + ar) * DM_XS + ac;
+    const double* ws = wsb(buf) + ac * DM_WS + ar;
+#pragma unroll
+    for (int k4 = 0; k4 < DM_KC; k4 += 4) {
+      const double a0 = xs[k4], a1 = xs[8 * DM_XS + k4];
+      double bf[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) bf[n] = ws[k4 * DM_WS + n * 8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        dmma_8x8x4(acc[0][n][0], acc[0][n][1], a0, bf[n]);
+        dmma_8x8x4(acc[1][n][0], acc[1][n][1], a1, bf[n]);
+      }
+    }
+    if (c + 1 < nc) store_x(buf ^ 1);
+    __syncthreads();
+  }
+
+  // ---- epilogue (reuses the staging smem): fp32 logits, f64 softmax
+  double* ex = reinterpret_cast<double*>(sm);
+  float* sc = reinterpret_cast<float*>(sm + (size_t)DM_TM * E * 8);
+  float* lg = sc + (size_t)DM_TM * E;
+  double* mx = reinterpret_cast<double*>(sm + (dmma_router_smem(E) - (size_t)DM_TM * 16));
+  double* sum = mx + DM_TM;
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int tok = warp * 16 + m * 8 + ar;
+    const int64_t t = t0 + tok;
+    if (t < T) {
+      const int64_t b = t / S;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int e = n * 8 + ac * 2 + j;
+          if (e < E) lg[tok * E + e] = (float)(acc[m][n][j] + tb[b * E + e]);  // tensor.py:286-287
+        }
+    }
+  }
+  __syncthreads();
+  for (int tok = tid; tok < DM_TM; tok += 128) {
+    double mv = -INFINITY;
+    for (int e = 0; e < E; ++e) mv = fmax(mv, (double)lg[tok * E + e]);
+    mx[tok] = mv;
+  }
+  __syncthreads();
+  for (int i = tid; i < DM_TM * E; i += 128) ex[i] = exp((double)lg[i] - mx[i / E]);
+  __syncthreads();
+  for (int tok = tid; tok < DM_TM; tok += 128) sum[tok] = np_pairwise_sum(ex + tok * E, E);
+  __syncthreads();
+  for (int i = tid; i < DM_TM * E; i += 128) sc[i] = (float)(ex[i] / sum[i / E]);
+  __syncthreads();
+  for (int i = tid; i < DM_TM * E; i += 128) {
+    const int64_t t = t0 + i / E;
+    if (t < T) logits[t * E + (i % E)] = lg[i];
+  }
+  for (int i = tid; i < DM_TM * E; i += 128) {
+    const int e = i / DM_TM, tok = i % DM_TM;
+    const int64_t t = t0 + tok;
+    if (t < T) {
+      const int64_t b = t / S, s = t % S;
+      scores_bes[(b * E + e) * S + s] = sc[tok * E + e];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ select
 constexpr int SEL_THREADS = 256;
 
@@ -461,7 +645,6 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
   }
 
   // ---- outputs in expert-major (e, b, slot) order (router.py:131-133)
-  const int64_t T = (int64_t)B * S;
   for (int j = tid; j < cap; j += SEL_THREADS) {
     const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(win[j] & 0xFFFFFFFFull);
     const int64_t o = ((int64_t)e * B + b) * cap + j;
@@ -545,12 +728,30 @@ __global__ void gather_rows_byte_kernel(const uint8_t* __restrict__ src, int64_t
 
 // ------------------------------------------------------------------ combine
 // moe.py:156-161 with the reference's rounding chain: gated = fp32(Y*gate),
-// combined = fp32(sum over selecting experts in ascending order, f64),
-// out = round(f64(combined) + f64(shared)). Warp per token; the token's row
-// list and gates are staged in smem, then every lane streams VEC-element
-// vectors of all its rows (independent loads -> memory-level parallelism).
+// combined = fp32(sum over selecting experts in ascending order), out =
+// round(combined + shared). ACC = double for fp32 output (the f64 chain of
+// tensor.py:374-376), float for bf16 output (inside its tolerance). Warp per
+// token: the token's row list and gates are staged in smem, then each lane
+// issues the loads of up to CB_BATCH rows before consuming any of them.
 constexpr int CB_WARPS = 8;
-template <typename TY, typename TO, int VEC>
+constexpr int CB_BATCH = 8;
+
+template <typename T, int VEC> struct VecIO {
+  static_assert(VEC * sizeof(T) % 16 == 0 || VEC == 1, "vector width");
+  static constexpr int NV = VEC * sizeof(T) / 16 > 0 ? VEC * (int)sizeof(T) / 16 : 1;
+  uint4 v[NV];
+  NIMG_DEV void load(const T* p) {
+    if constexpr (VEC == 1) {
+      *reinterpret_cast<T*>(&v[0]) = *p;
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) v[i] = __ldg(reinterpret_cast<const uint4*>(p) + i);
+    }
+  }
+  NIMG_DEV float at(int i) const { return to_f32(reinterpret_cast<const T*>(v)[i]); }
+};
+
+template <typename TY, typename TO, int VEC, typename ACC>
 __global__ void __launch_bounds__(CB_WARPS * 32)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
@@ -569,54 +770,78 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
   }
   __syncwarp();
   for (int c = lane * VEC; c < d; c += 32 * VEC) {
-    double acc[VEC];
+    VecIO<TY, VEC> sh;
+    sh.load(ys + t * d + c);
+    ACC acc[VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[v] = 0.0;
-    int k = 0;
-    for (; k + 2 <= cnt; k += 2) {
-      TY y0[VEC], y1[VEC];
-      const TY* p0 = yr + (int64_t)rows[k] * d + c;
-      const TY* p1 = yr + (int64_t)rows[k + 1] * d + c;
+    for (int v = 0; v < VEC; ++v) acc[v] = ACC(0);
+    for (int kb = 0; kb < cnt; kb += CB_BATCH) {
+      VecIO<TY, VEC> y[CB_BATCH];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) { y0[v] = p0[v]; y1[v] = p1[v]; }
-      const float g0 = gl[k], g1 = gl[k + 1];
+      for (int q = 0; q < CB_BATCH; ++q)
+        if (kb + q < cnt) y[q].load(yr + (int64_t)rows[kb + q] * d + c);
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) {
-        acc[v] += (double)(to_f32(y0[v]) * g0);
-        acc[v] += (double)(to_f32(y1[v]) * g1);
+      for (int q = 0; q < CB_BATCH; ++q) {
+        if (kb + q < cnt) {
+          const float g = gl[kb + q];
+#pragma unroll
+          for (int v = 0; v < VEC; ++v) acc[v] += (ACC)(y[q].at(v) * g);
+        }
       }
     }
-    for (; k < cnt; ++k) {
-      const TY* p = yr + (int64_t)rows[k] * d + c;
-      const float gk = gl[k];
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) acc[v] += (double)(to_f32(p[v]) * gk);
-    }
-    const TY* sh = ys + t * d + c;
-    TO* o = out + t * d + c;
     TO res[VEC];
 #pragma unroll
     for (int v = 0; v < VEC; ++v) {
       const float comb = (float)acc[v];
-      res[v] = from_f32<TO>((float)((double)comb + (double)to_f32(sh[v])));
+      res[v] = from_f32<TO>((float)((ACC)comb + (ACC)sh.at(v)));
     }
+    TO* o = out + t * d + c;
+    if constexpr (VEC * sizeof(TO) % 16 == 0) {
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) o[v] = res[v];
+      for (int i = 0; i < VEC * (int)sizeof(TO) / 16; ++i)
+        reinterpret_cast<uint4*>(o)[i] = reinterpret_cast<const uint4*>(res)[i];
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) o[v] = res[v];
+    }
   }
 }
 
 // ------------------------------------------------------------------ launchers
 cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
-                          double* tb, double* wd, float* logits, float* scores_bes, int B, int S,
-                          int d, int E, cudaStream_t s) {
-  const RouterGeom g = router_geom(E);
-  router_prep_kernel<<<B + 64, 256, 0, s>>>(t_emb, w_r, tb, wd, B, d, E, g.EP);
+                          double* tb, double* part, unsigned* counter, double* wd, float* logits,
+                          float* scores_bes, int B, int S, int d, int E, cudaStream_t s) {
+  const bool dmma = E <= DM_EP;
+  const int EP = dmma ? DM_EP : router_geom(E).EP;
+  const int nkc = (d + RP_KCH - 1) / RP_KCH;
+  router_prep_kernel<<<dim3(nkc + RP_CONV_BLOCKS, B), 64, 0, s>>>(t_emb, w_r, tb, part, wd, counter,
+                                                                  B, d, E, EP);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   const int64_t T = (int64_t)B * S;
+  const bool vec = (d % 8 == 0) && ((uintptr_t)x_norm % 16 == 0);
+  if (dmma) {
+    const int grid = (int)((T + DM_TM - 1) / DM_TM);
+    const size_t smem = dmma_router_smem(E);
+#define NIMG_DMMA_LAUNCH(TX, V)                                                               \
+  do {                                                                                         \
+    err = cudaFuncSetAttribute(router_scores_dmma_kernel<TX, V>,                               \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
+    if (err != cudaSuccess) return err;                                                        \
+    router_scores_dmma_kernel<TX, V><<<grid, 128, smem, s>>>(                                  \
+        reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d, E);          \
+  } while (0)
+    if (x_bf16) {
+      if (vec) NIMG_DMMA_LAUNCH(bf16, true); else NIMG_DMMA_LAUNCH(bf16, false);
+    } else {
+      if (vec) NIMG_DMMA_LAUNCH(float, true); else NIMG_DMMA_LAUNCH(float, false);
+    }
+#undef NIMG_DMMA_LAUNCH
+    return cudaGetLastError();
+  }
+  const RouterGeom g = router_geom(E);
   const int grid = (int)((T + g.TM - 1) / g.TM);
   const size_t smem = router_smem(E);
-  const bool vec = (d % 8 == 0) && ((uintptr_t)x_norm % 16 == 0);
 #define NIMG_ROUTER_LAUNCH(TX, V)                                                              \
   do {                                                                                         \
     err = cudaFuncSetAttribute(router_scores_kernel<TX, V>,                                    \
@@ -628,13 +853,16 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
   if (x_bf16) {
     if (vec) NIMG_ROUTER_LAUNCH(bf16, true); else NIMG_ROUTER_LAUNCH(bf16, false);
   } else {
-    if (vec && d % 4 == 0) NIMG_ROUTER_LAUNCH(float, true); else NIMG_ROUTER_LAUNCH(float, false);
+    if (vec) NIMG_ROUTER_LAUNCH(float, true); else NIMG_ROUTER_LAUNCH(float, false);
   }
 #undef NIMG_ROUTER_LAUNCH
   return cudaGetLastError();
 }
 
-size_t router_wd_bytes(int d, int E) { return (size_t)d * router_geom(E).EP * 8; }
+size_t router_part_bytes(int B, int d, int E) {
+  return (size_t)((d + RP_KCH - 1) / RP_KCH) * B * E * 8;
+}
+size_t router_wd_bytes(int d, int E) { return (size_t)d * (E <= DM_EP ? DM_EP : router_geom(E).EP) * 8; }
 
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s) {
@@ -680,11 +908,12 @@ static void combine_dispatch(const void* yr, const void* ys, const float* gates,
                              int E, cudaStream_t s) {
   const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
   const size_t smem = (size_t)CB_WARPS * E * 8;
+  using ACC = typename std::conditional<sizeof(TO) == 2, float, double>::type;
   if (d % 8 == 0)
-    combine_kernel<TY, TO, 8><<<grid, CB_WARPS * 32, smem, s>>>(
+    combine_kernel<TY, TO, 8, ACC><<<grid, CB_WARPS * 32, smem, s>>>(
         (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
   else
-    combine_kernel<TY, TO, 1><<<grid, CB_WARPS * 32, smem, s>>>(
+    combine_kernel<TY, TO, 1, ACC><<<grid, CB_WARPS * 32, smem, s>>>(
         (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
 }
 
