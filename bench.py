@@ -317,6 +317,132 @@ def run_e2e(args, c, inp, cfg, bank):
             "d2h_bytes_per_step": d2h, "ms_per_step": ms}
 
 
+# ----------------------------------------------------------------- ours, N GPUs (EP)
+def run_ep(args, c, peaks, peak_kind):
+    """Expert parallel over NCCL (torchrun, one rank per GPU): global batch
+    c["B"] split over ranks, E/R experts per rank (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    from paper_2604_12163_b200.ep import EPContext, ep_moe_forward
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    B, S, d, h, E = c["B"], c["S"], c["d"], c["h"], c["E"]
+    if B % world or E % world:
+        raise SystemExit(f"B={B} and E={E} must be divisible by {world}")
+    bl, El = B // world, E // world
+    wc = work_counts(c)
+
+    # same-config single-GPU number, measured here on rank 0 (informational;
+    # the driver computes scaling from the per-N `value`s)
+    same1 = None
+    if rank == 0 and not args.no_same_config_1gpu:
+        inp = make_inputs(c, dev)
+        cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=c["C"])
+        plan = M.MoEPlan(cfg, M.ExpertBank(inp["w1"], inp["w3"], inp["w2"], inp["sw1"],
+                                           inp["sw3"], inp["sw2"]), B, S, torch.bfloat16)
+        f = lambda: plan.forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"])
+        for _ in range(3):
+            f()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(max(3, args.steps // 2)):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        ms1 = e0.elapsed_time(e1) / max(3, args.steps // 2)
+        same1 = {"value": wc["T"] / (ms1 * 1e-3), "ms_per_step": ms1, "n_gpus": 1}
+        del plan, inp
+        torch.cuda.empty_cache()
+    dist.barrier()
+
+    # this rank's samples and expert shard (seeded per rank; shared + router replicated)
+    cl = dict(c, B=bl, seed=c["seed"] * 1000 + rank)
+    inp = make_inputs(cl, dev)
+    g = torch.Generator(device=dev).manual_seed(c["seed"])
+    tn = lambda *s, std: torch.clamp(torch.randn(*s, generator=g, device=dev) * std, -2 * std, 2 * std)
+    w_r = tn(2 * d, E, std=0.006)
+    sw = [tn(*s, std=0.02).to(torch.bfloat16) for s in ((h, d), (h, d), (d, h))]
+    bank = M.ExpertBank(inp["w1"][:El].contiguous(), inp["w3"][:El].contiguous(),
+                        inp["w2"][:El].contiguous(), *sw)
+    del inp["w1"], inp["w3"], inp["w2"]
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=c["C"])
+    ctx = EPContext(overlap=not args.no_overlap)
+    step = lambda: ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = ClockSampler(local) if rank == 0 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = clk.stop() if clk else None
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = wc["T"] / (ms * 1e-3)
+
+    # e2e through the public EP API with host buffers (per rank), max over ranks
+    host = {k: inp[k].cpu().pin_memory() for k in ("x_norm", "x_mod", "t_emb")}
+    out_h = torch.empty(inp["x_mod"].shape, dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        y = ep_moe_forward(dv["x_norm"], dv["x_mod"], dv["t_emb"], cfg, bank, w_r, ctx)
+        out_h.copy_(y, non_blocking=True)
+
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for _ in range(args.steps):
+        e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    t2 = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+    ms2 = float(t2.item())
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+
+    if rank == 0:
+        a2a = wc["R"] // world * (world - 1) * d * 2  # bytes per rank per direction
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded randn, random-init weights)",
+            "config": {"workload": workload_name(c), "capacity": wc["cap"], "tokens": wc["T"],
+                       "parallelism": f"ep{world} (experts {El}/GPU, samples {bl}/GPU), NCCL all-to-all"
+                                      + ("" if args.no_overlap else ", comm/compute overlap"),
+                       "l2": "inputs larger than L2"},
+            "a2a_bytes_per_rank_per_direction": a2a,
+            "same_config_1gpu": same1,
+            "e2e": {"value": wc["T"] / (ms2 * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step":
+                    out_h.numel() * out_h.element_size() * world, "ms_per_step": ms2},
+            "gpu_launches": (8 + 2 * (world - 1)) * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -326,6 +452,8 @@ def main():
     ap.add_argument("--config", default=None, choices=["cfg2", "cfg4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-overlap", action="store_true", help="EP: plain all-to-alls")
+    ap.add_argument("--no-same-config-1gpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per GEMM1 launch, if captured")
     args = ap.parse_args()
@@ -337,8 +465,7 @@ def main():
         return
     peaks, kind = load_peaks()
     if world > 1:
-        from paper_2604_12163_b200 import ep
-        ep.bench_main(args, c, peaks, kind)
+        run_ep(args, c, peaks, kind)
         return
     run_single(args, c, peaks, kind)
 

@@ -1,0 +1,98 @@
+"""Expert parallel on GPUs over NCCL: EP(R) must equal the 1-GPU layer bitwise
+(the returned rows land in the 1-GPU expert-major layout and
+the combine is deterministic). R = 1 (loopback through the EP code path)
+always runs; R = 2 runs when two GPUs are visible."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _inputs(B, S, d, E, h, seed, dev):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    rn = lambda *s, std=1.0: torch.randn(*s, generator=g, device=dev) * std
+    tn = lambda *s, std: torch.clamp(rn(*s, std=std), -2 * std, 2 * std)
+    x = rn(B, S, d)
+    xn = (x * torch.rsqrt((x * x).mean(-1, keepdim=True) + 1e-6) / 4.0).to(torch.bfloat16)
+    xm = (xn.float() * (1 + 0.1 * rn(B, 1, d))).to(torch.bfloat16)
+    bf = torch.bfloat16
+    return dict(x_norm=xn, x_mod=xm, t_emb=rn(B, d), w_r=tn(2 * d, E, std=0.006),
+                w1=tn(E, h, d, std=0.02).to(bf), w3=tn(E, h, d, std=0.02).to(bf),
+                w2=tn(E, d, h, std=0.02).to(bf), sw1=tn(h, d, std=0.02).to(bf),
+                sw3=tn(h, d, std=0.02).to(bf), sw2=tn(d, h, std=0.02).to(bf))
+
+
+def _worker(rank, world, port, q, shape):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        from paper_2604_12163_b200 import moe as M
+        from paper_2604_12163_b200 import router as R
+        from paper_2604_12163_b200.ep import EPContext, ep_moe_forward, shard_bank
+        B, S, d, E, h, C = shape
+        dev = torch.device("cuda", rank)
+        a = _inputs(B, S, d, E, h, 7, dev)
+        cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+        bank = M.ExpertBank(a["w1"], a["w3"], a["w2"], a["sw1"], a["sw3"], a["sw2"])
+        full = M.moe_forward(a["x_mod"], a["x_norm"], a["x_mod"], a["t_emb"], cfg, bank, a["w_r"])
+        bl = B // world
+        sl = slice(rank * bl, (rank + 1) * bl)
+        local = shard_bank(bank, rank, world)
+        res = {}
+        for overlap in (False, True):
+            ctx = EPContext(overlap=overlap)
+            out = ep_moe_forward(a["x_norm"][sl].contiguous(), a["x_mod"][sl].contiguous(),
+                                 a["t_emb"][sl].contiguous(), cfg, local, a["w_r"], ctx)
+            torch.cuda.synchronize()
+            res[overlap] = bool(torch.equal(out, full[sl]))
+        q.put((rank, res))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, shape):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shape)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("shape", [(2, 1024, 2048, 64, 1344, 4.0), (2, 256, 256, 8, 112, 2.0)])
+def test_ep_loopback_bitwise(shape):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    res = _run(1, shape)
+    assert res[0] == {False: True, True: True}
+
+
+def test_ep_two_gpus_bitwise():
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    res = _run(2, (4, 1024, 2048, 64, 1344, 4.0))
+    for r in range(2):
+        assert res[r] == {False: True, True: True}, res
