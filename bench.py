@@ -420,7 +420,7 @@ def run_ep(args, c, peaks, peak_kind):
     h2d = sum(v.numel() * v.element_size() for v in host.values())
 
     if rank == 0:
-        a2a = wc["R"] // world * (world - 1) * d * 2  # bytes per rank per direction
+        a2a = wc["R"] // world * (world - 1) // world * d * 2  # bytes per rank per direction
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
