@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -239,10 +240,13 @@ int check_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex) {
   return NIMG_OK;
 }
 
+// gather_idx != null (tcgen05 path only): routed row r of GEMM1's A operand is
+// row gather_idx[r] of xr, which then has gather_src_rows rows (TMA gather4).
 int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex,
                     const void* xr, const void* w1, const void* w3, const void* w2, void* yr,
                     const void* xs, const void* sw1, const void* sw3, const void* sw2, void* ys,
-                    void* ws, size_t ws_bytes, cudaStream_t st) {
+                    void* ws, size_t ws_bytes, cudaStream_t st,
+                    const int32_t* gather_idx = nullptr, int64_t gather_src_rows = 0) {
   NIMG_TRY(check_ffn(f, off, ex));
   if (ws_bytes < ffn_ws_bytes(f)) return fail(NIMG_ERR_CONFIG, "workspace too small");
   const bool has_r = f->n_rows > 0, has_s = f->n_shared_rows > 0;
@@ -271,7 +275,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       memset(&tm, 0, sizeof(tm));
       const int rb = has_r ? 0 : 1;  // any valid bank to alias an unused one
       if (has_r) {
-        NIMG_TRY(map_2d(&tm.a[0], xr, f->n_rows, d, 128));
+        if (gather_idx) NIMG_TRY(map_2d(&tm.a[0], xr, gather_src_rows, d, 1));
+        else NIMG_TRY(map_2d(&tm.a[0], xr, f->n_rows, d, 128));
         NIMG_TRY(map_3d(&tm.b[0], w1, f->n_experts, h, d, box));
         NIMG_TRY(map_3d(&tm.b3[0], w3, f->n_experts, h, d, box));
       }
@@ -282,8 +287,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       }
       if (!has_r) { tm.a[0] = tm.a[1]; tm.b[0] = tm.b[1]; tm.b3[0] = tm.b3[1]; }
       if (!has_s) { tm.a[1] = tm.a[rb]; tm.b[1] = tm.b[rb]; tm.b3[1] = tm.b3[rb]; }
-      p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0};
-      p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0};
+      p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0, gather_idx};
+      p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, nullptr};
       CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
       mark(3, st);
     }
@@ -307,14 +312,15 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       if (!has_s) { tm.a[1] = tm.a[0]; tm.b[1] = tm.b[0]; }
       tm.b3[0] = tm.b[0];
       tm.b3[1] = tm.b[1];
-      p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0};
-      p.bank[1] = GBank{ys, d, hs, d, (d + bn - 1) / bn, 0};
+      p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0, nullptr};
+      p.bank[1] = GBank{ys, d, hs, d, (d + bn - 1) / bn, 0, nullptr};
       CUDA_TRY(launch_grouped_tc(1, tm, p, sms, st));
     }
     return NIMG_OK;
   }
 
   // SIMT path: fp32 pre / y
+  if (gather_idx) return fail(NIMG_ERR_CONFIG, "internal: fused gather needs the tcgen05 path");
   const bool bf = f->act_dtype == NIMG_BF16;
   const int bm = simt_bm(), bn = simt_bn();
   {
@@ -359,6 +365,18 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
   CUDA_TRY(launch_gate_norm(o->scores_bes, w.slot_of, o->gates, o->comb_rows, o->comb_cnt, B, S,
                             E, cap, d->gate_eps, d->gate_scale, st));
   return NIMG_OK;
+}
+
+// Fusing the routed-row gather into GEMM1 (TMA tile::gather4, one 4-row load
+// per lane) is correct but measured 2.7x slower on B200: gather4 issues at
+// ~45 cycles per 512 B, and a 128x64 A tile needs 32 of them per 448-cycle
+// MMA k-block. Off by default; NIMG_FUSED_GATHER=1 enables it for experiments.
+bool use_fused_gather(int32_t path) {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_FUSED_GATHER");
+    return e && e[0] == '1';
+  }();
+  return on && path == NIMG_PATH_TCGEN05;
 }
 
 nimg_ffn_desc layer_ffn_desc(const nimg_moe_desc* d) {
@@ -458,8 +476,9 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   const nimg_ffn_desc f = layer_ffn_desc(d);
   int32_t path, ydt;
   nimg_ffn_path(&f, &path, &ydt);
-  *bytes = route_ws_bytes(d) + align_up((size_t)f.n_rows * d->d * elt(d->act_dtype)) +
-           ffn_ws_bytes(&f) + align_up((size_t)f.n_rows * d->d * elt(ydt)) +
+  // the gathered-row buffer exists only when the gather is not fused into GEMM1
+  const size_t xg = use_fused_gather(path) ? 0 : align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
+  *bytes = route_ws_bytes(d) + xg + ffn_ws_bytes(&f) + align_up((size_t)f.n_rows * d->d * elt(ydt)) +
            align_up((size_t)f.n_shared_rows * d->d * elt(ydt));
   return NIMG_OK;
 }
@@ -475,9 +494,10 @@ int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, s
   const nimg_ffn_desc f = layer_ffn_desc(d);
   int32_t path, ydt;
   nimg_ffn_path(&f, &path, &ydt);
+  const bool fused_gather = use_fused_gather(path);
   uint8_t* w = static_cast<uint8_t*>(ws);
   void* route_ws = w;                 w += route_ws_bytes(d);
-  void* xg = w;                       w += align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
+  void* xg = w;                       if (!fused_gather) w += align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
   void* ffn_ws = w;                   w += ffn_ws_bytes(&f);
   void* yr = w;                       w += align_up((size_t)f.n_rows * d->d * elt(ydt));
   void* ys = w;
@@ -485,14 +505,17 @@ int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, s
   mark(0, st);
   NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st));
   mark(1, st);
-  CUDA_TRY(launch_gather_rows(p->x_mod, d->d * (int64_t)elt(d->act_dtype), p->route.token_flat,
-                              f.n_rows, xg, st));
+  if (!fused_gather)
+    CUDA_TRY(launch_gather_rows(p->x_mod, d->d * (int64_t)elt(d->act_dtype), p->route.token_flat,
+                                f.n_rows, xg, st));
   mark(2, st);
   int64_t off[kMaxSeg + 1];
   if (f.nseg > kMaxSeg - 8) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
   for (int e = 0; e <= f.nseg; ++e) off[e] = (int64_t)e * d->B * d->cap;  // moe.py:154
-  NIMG_TRY(expert_ffn_impl(&f, off, nullptr, xg, p->w1, p->w3, p->w2, yr, p->x_mod, p->sw1,
-                           p->sw3, p->sw2, ys, ffn_ws, ffn_ws_bytes(&f), st));
+  // fused path: GEMM1 gathers x_mod rows by token_flat itself (TMA gather4)
+  NIMG_TRY(expert_ffn_impl(&f, off, nullptr, fused_gather ? p->x_mod : xg, p->w1, p->w3, p->w2, yr,
+                           p->x_mod, p->sw1, p->sw3, p->sw2, ys, ffn_ws, ffn_ws_bytes(&f), st,
+                           fused_gather ? p->route.token_flat : nullptr, d->B * d->S));
   mark(4, st);
   CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys, p->route.gates,
                           p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,

@@ -74,6 +74,18 @@ NIMG_DEV void tma_load_3d(void* smem_dst, const void* tmap, uint64_t* bar, int c
       : "memory");
 }
 
+// 4 arbitrary rows (r0..r3) x one box of columns from a 2-D map whose box is
+// {cols, 1}; lands as 4 consecutive (swizzled) rows at smem_dst.
+NIMG_DEV void tma_gather4(void* smem_dst, const void* tmap, uint64_t* bar, int col, int r0, int r1,
+                          int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(col), "r"(r0), "r"(r1),
+      "r"(r2), "r"(r3)
+      : "memory");
+}
+
 // ---------------------------------------------------------------- tcgen05
 NIMG_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 NIMG_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }

@@ -108,23 +108,42 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ------------------------------------------------ TMA producer
-      int stage = 0; uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
-        TileInfo ti; decode_tile<MODE>(p, t, ti);
-        for (int kb = 0; kb < ti.nk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * SB;
-          uint8_t* sb = sa + kATileBytes;
-          mbar_arrive_expect_tx(&full[stage], SB);
+    // ------------------------------------------------ TMA producer (whole warp)
+    // Contiguous banks: lane 0 issues one 2-D box per k-block. Gather banks
+    // (a_idx != null, the routed rows of the 1-GPU layer): the A tile is 32
+    // TMA gather4 loads of 4 rows each, one per lane, straight from x_mod by
+    // token_flat -- no gathered copy in HBM (moe.py:152-153 fused).
+    int stage = 0; uint32_t phase = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
+      TileInfo ti; decode_tile<MODE>(p, t, ti);
+      const int32_t* idx = p.bank[ti.bank].a_idx;
+      int r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+      if (idx != nullptr) {
+        const int base = ti.a_row + 4 * lane;
+        const int fallback = __ldg(idx + ti.a_row);
+        r0 = 4 * lane + 0 < ti.rows_valid ? __ldg(idx + base + 0) : fallback;
+        r1 = 4 * lane + 1 < ti.rows_valid ? __ldg(idx + base + 1) : fallback;
+        r2 = 4 * lane + 2 < ti.rows_valid ? __ldg(idx + base + 2) : fallback;
+        r3 = 4 * lane + 3 < ti.rows_valid ? __ldg(idx + base + 3) : fallback;
+      }
+      for (int kb = 0; kb < ti.nk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * SB;
+        uint8_t* sb = sa + kATileBytes;
+        if (lane == 0) mbar_arrive_expect_tx(&full[stage], SB);
+        __syncwarp();
+        if (idx != nullptr) {
+          tma_gather4(sa + lane * 4 * BK * 2, &tm.a[ti.bank], &full[stage], kb * BK, r0, r1, r2, r3);
+        } else if (lane == 0) {
           tma_load_2d(sa, &tm.a[ti.bank], &full[stage], kb * BK, ti.a_row);
+        }
+        if (lane == 0) {
           tma_load_3d(sb, &tm.b[ti.bank], &full[stage], kb * BK, ti.n0, ti.expert);
           if (MODE == 0)
             tma_load_3d(sb + C::B_BOX * BK * 2, &tm.b3[ti.bank], &full[stage], kb * BK, ti.n0,
                         ti.expert);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {

@@ -45,8 +45,14 @@ class ExpertBank:
 
     def on_device(self, dtype: torch.dtype) -> "ExpertBank":
         """Device copies in the kernel dtype (no copy if already there)."""
-        return ExpertBank(*(to_device(w, dtype) for w in (self.w1, self.w3, self.w2, self.shared_w1,
-                                                          self.shared_w3, self.shared_w2)))
+        return bank_on_device(self, dtype)
+
+
+def bank_on_device(bank, dtype: torch.dtype) -> ExpertBank:
+    """Any bank with w1..shared_w2 fields (ours or the reference's moe.ExpertBank,
+    moe.py:73-94) -> device ExpertBank in the kernel dtype."""
+    return ExpertBank(*(to_device(w, dtype) for w in (bank.w1, bank.w3, bank.w2, bank.shared_w1,
+                                                      bank.shared_w3, bank.shared_w2)))
 
 
 @dataclass
@@ -165,7 +171,7 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
     cap = capacity_for(S, E, cfg.capacity_factor)
     if cap < 1:
         raise ConfigError("computed capacity is zero")
-    w = bank.on_device(act)
+    w = bank_on_device(bank, act)
     _, h, hs = _check_bank_shapes(w.w1, w.w3, w.w2, w.shared_w1, w.shared_w3, w.shared_w2, d)
 
     desc = make_desc(B, S, d, E, cap, h, hs, cfg, act)
@@ -197,7 +203,7 @@ class MoEPlan:
                  act: torch.dtype = torch.bfloat16):
         self.cfg, self.B, self.S, self.act = cfg, B, S, act
         d, E = cfg.d_model, cfg.n_experts
-        self.bank = bank.on_device(act)
+        self.bank = bank_on_device(bank, act)
         _, self.h, self.hs = _check_bank_shapes(self.bank.w1, self.bank.w3, self.bank.w2,
                                                 self.bank.shared_w1, self.bank.shared_w3,
                                                 self.bank.shared_w2, d)
