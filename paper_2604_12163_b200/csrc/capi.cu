@@ -240,6 +240,15 @@ int check_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex) {
   return NIMG_OK;
 }
 
+// CTA-pair tcgen05 kernels (default); NIMG_PAIR=0 selects the 1-CTA kernels.
+bool use_pair_kernels() {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_PAIR");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // gather_idx != null (tcgen05 path only): routed row r of GEMM1's A operand is
 // row gather_idx[r] of xr, which then has gather_src_rows rows (TMA gather4).
 int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex,
@@ -265,12 +274,15 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       if (q && !aligned16(q)) return fail(NIMG_ERR_SHAPE, "tensor not 16-byte aligned");
     int sms = 0;
     NIMG_TRY(device_sms(&sms));
+    // CTA-pair (cta_group::2) kernels unless the A rows are gathered in-kernel
+    const bool pair = use_pair_kernels() && gather_idx == nullptr;
+    const int tile_rows = pair ? tc_pair_rows() : 128;
     // GEMM1: pre = SiLU(x W1^T) * (x W3^T)
     {
       GroupedParams p;
       memset(&p, 0, sizeof(p));
       const int bn = tc_bn_out(0), box = tc_b_box(0);
-      NIMG_TRY(fill_segments(p, f, off, ex, 128, (h + bn - 1) / bn, (hs + bn - 1) / bn));
+      NIMG_TRY(fill_segments(p, f, off, ex, tile_rows, (h + bn - 1) / bn, (hs + bn - 1) / bn));
       TmapSet tm;
       memset(&tm, 0, sizeof(tm));
       const int rb = has_r ? 0 : 1;  // any valid bank to alias an unused one
@@ -289,15 +301,16 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       if (!has_s) { tm.a[1] = tm.a[rb]; tm.b[1] = tm.b[rb]; tm.b3[1] = tm.b3[rb]; }
       p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0, gather_idx};
       p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, nullptr};
-      CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
+      if (pair) CUDA_TRY(launch_grouped_tc_pair(0, tm, p, sms, st));
+      else CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
       mark(3, st);
     }
     // GEMM2: y = pre W2^T
     {
       GroupedParams p;
       memset(&p, 0, sizeof(p));
-      const int bn = tc_bn_out(1), box = tc_b_box(1);
-      NIMG_TRY(fill_segments(p, f, off, ex, 128, (d + bn - 1) / bn, (d + bn - 1) / bn));
+      const int bn = tc_bn_out(1), box = pair ? tc_b_box(1) / 2 : tc_b_box(1);
+      NIMG_TRY(fill_segments(p, f, off, ex, tile_rows, (d + bn - 1) / bn, (d + bn - 1) / bn));
       TmapSet tm;
       memset(&tm, 0, sizeof(tm));
       if (has_r) {
@@ -314,7 +327,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       tm.b3[1] = tm.b[1];
       p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0, nullptr};
       p.bank[1] = GBank{ys, d, hs, d, (d + bn - 1) / bn, 0, nullptr};
-      CUDA_TRY(launch_grouped_tc(1, tm, p, sms, st));
+      if (pair) CUDA_TRY(launch_grouped_tc_pair(1, tm, p, sms, st));
+      else CUDA_TRY(launch_grouped_tc(1, tm, p, sms, st));
     }
     return NIMG_OK;
   }

@@ -239,10 +239,226 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
   }
 }
 
+// ============================================================================
+// CTA-pair variant (cta_group::2). A cluster of 2 CTAs owns a 256-row tile:
+// each CTA stages its own 128 A rows and HALF of B (GEMM1: the leader holds
+// the W1 slice, the peer the W3 slice; GEMM2: 128 of the 256 W2 rows each),
+// so per-SM shared-memory traffic per MMA drops by ~1/3 versus the 1-CTA
+// kernel. The leader's single thread issues UMMA M=256; both CTAs' TMA loads
+// complete on the leader's full barrier; MMA commits multicast to both CTAs'
+// empty / tmem_full barriers; both CTAs' epilogues arrive on the leader's
+// tmem_empty barrier. Each CTA's epilogue drains its own TMEM (its 128 rows).
+template <int MODE> struct PairCfg;
+template <> struct PairCfg<0> {
+  static constexpr int BN_OUT = 112, BN_MMA = 224, B_ROWS = 112, STAGES = 6;
+};
+template <> struct PairCfg<1> {
+  static constexpr int BN_OUT = 256, BN_MMA = 256, B_ROWS = 128, STAGES = 6;
+};
+template <int MODE> constexpr int pair_stage_bytes() { return kATileBytes + PairCfg<MODE>::B_ROWS * BK * 2; }
+template <int MODE> constexpr int pair_smem_bytes() { return PairCfg<MODE>::STAGES * pair_stage_bytes<MODE>() + 1024 + 256; }
+
+constexpr int PBM = 256;  // rows per pair tile
+
+template <int MODE>
+NIMG_DEV void decode_pair_tile(const GroupedParams& p, int t, TileInfo& ti) {
+  int lo = 0, hi = p.nseg - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (p.seg_tile0[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  const int bank = lo >= p.nseg0 ? 1 : 0;
+  const int ntn = p.bank[bank].ntn;
+  const int local = t - p.seg_tile0[lo];
+  const int m_blk = local / ntn;
+  const int n_blk = local - m_blk * ntn;
+  ti.bank = bank;
+  ti.expert = p.seg_expert[lo];
+  ti.a_row = p.seg_row0[lo] + m_blk * PBM;            // pair tile start
+  ti.rows_valid = min(PBM, p.seg_rows[lo] - m_blk * PBM);
+  ti.n0 = n_blk * PairCfg<MODE>::BN_OUT;
+  ti.nk = (p.bank[bank].K + BK - 1) / BK;
+}
+
+template <int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constant__ GroupedParams p) {
+  using C = PairCfg<MODE>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int SB = pair_stage_bytes<MODE>();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t crank = cluster_ctarank();
+  const bool leader = crank == 0;
+  const int cluster_id = blockIdx.x >> 1;
+  const int n_clusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 8); }
+    fence_barrier_init();
+    for (int b = 0; b < 2; ++b) {
+      tma_prefetch_desc(&tm.a[b]);
+      tma_prefetch_desc(&tm.b[b]);
+      if (MODE == 0) tma_prefetch_desc(&tm.b3[b]);
+    }
+  }
+  if (warp == 1) tmem_alloc_cg2(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer (both CTAs)
+      int stage = 0; uint32_t phase = 0;
+      for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
+        TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+        const int a_row = ti.a_row + (int)crank * BM;
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * SB;
+          uint8_t* sb = sa + kATileBytes;
+          const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * SB);
+          tma_load_2d_cg2(sa, &tm.a[ti.bank], fb, kb * BK, a_row);
+          if (MODE == 0) {  // leader: W1 slice, peer: W3 slice
+            tma_load_3d_cg2(sb, crank ? (const void*)&tm.b3[ti.bank] : (const void*)&tm.b[ti.bank],
+                            fb, kb * BK, ti.n0, ti.expert);
+          } else {          // W2 rows n0 + 128*crank
+            tma_load_3d_cg2(sb, &tm.b[ti.bank], fb, kb * BK, ti.n0 + (int)crank * C::B_ROWS, ti.expert);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      // ------------------------------------------------ MMA issuer (leader only)
+      constexpr uint32_t idesc = make_idesc_bf16(PBM, C::BN_MMA);
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
+        TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * 256;
+        for (int kb = 0; kb < ti.nk; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + stage * SB);
+          const uint32_t sb = sa + kATileBytes;
+          const uint64_t adesc = make_sdesc_k128(sa);
+          const uint64_t bdesc = make_sdesc_k128(sb);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+          umma_commit_cg2(&empty[stage], 0x3);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_cg2(&tfull[acc], 0x3);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t tempty_leader0 = mapa_shared(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
+      TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+      const GBank& bk = p.bank[ti.bank];
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
+      const int row = (int)crank * BM + r;                 // row within the pair tile
+      const bool rv = row < ti.rows_valid;
+      bf16* orow = reinterpret_cast<bf16*>(bk.out) + (int64_t)(ti.a_row + row) * bk.out_ld + ti.n0;
+#pragma unroll 1
+      for (int c = 0; c < C::BN_OUT / 16; ++c) {
+        uint32_t a[16];
+        tmem_ld16(tb + c * 16, a);
+        uint32_t pk[8];
+        if (MODE == 0) {
+          uint32_t g[16];
+          tmem_ld16(tb + C::B_ROWS + c * 16, g);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            pk[j] = pack_bf16x2(silu_mul(__uint_as_float(a[2 * j]), __uint_as_float(g[2 * j])),
+                                silu_mul(__uint_as_float(a[2 * j + 1]), __uint_as_float(g[2 * j + 1])));
+        } else {
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            pk[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
+        }
+        if (rv && ti.n0 + c * 16 < bk.N) {
+          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_cg2(tmem_base, 512);
+  }
+}
+
 }  // namespace tc
 
 // ------------------------------------------------------------------ host side
 int tc_bn_out(int mode) { return mode == 0 ? tc::Cfg<0>::BN_OUT : tc::Cfg<1>::BN_OUT; }
+int tc_pair_rows() { return tc::PBM; }
+
+cudaError_t launch_grouped_tc_pair(int mode, const TmapSet& tm, const GroupedParams& p, int num_sms,
+                                   cudaStream_t stream) {
+  if (p.total_tiles <= 0) return cudaSuccess;
+  const int clusters = p.total_tiles < num_sms / 2 ? p.total_tiles : num_sms / 2;
+  const int grid = 2 * clusters;
+  if (mode == 0) {
+    constexpr int smem = tc::pair_smem_bytes<0>();
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100_pair<0>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    tc::grouped_gemm_sm100_pair<0><<<grid, tc::kThreads, smem, stream>>>(tm, p);
+  } else {
+    constexpr int smem = tc::pair_smem_bytes<1>();
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100_pair<1>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    tc::grouped_gemm_sm100_pair<1><<<grid, tc::kThreads, smem, stream>>>(tm, p);
+  }
+  return cudaGetLastError();
+}
 int tc_b_box(int mode) { return mode == 0 ? tc::Cfg<0>::B_BOX : tc::Cfg<1>::B_BOX; }
 
 cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& p, int num_sms,

@@ -61,6 +61,10 @@ struct SimtParams {
 };
 
 int tc_bn_out(int mode);
+int tc_pair_rows();
+// CTA-pair (cta_group::2) variant: 256-row tiles, B split across the pair.
+cudaError_t launch_grouped_tc_pair(int mode, const TmapSet& tm, const GroupedParams& p, int num_sms,
+                                   cudaStream_t stream);
 int tc_b_box(int mode);
 cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& p, int num_sms,
                               cudaStream_t stream);
