@@ -355,19 +355,27 @@ template <typename TX, bool VEC>
 __global__ void __launch_bounds__(128)
 router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
                           const double* __restrict__ tb, float* __restrict__ logits,
-                          float* __restrict__ scores_bes, int B, int S, int d, int E) {
+                          float* __restrict__ scores_bes, int B, int S, int d, int E,
+                          int frags_per_cta) {
+  // CTA c owns 8-row fragments [c*fpc, (c+1)*fpc) (fpc <= 8) -- the grid is
+  // sized ~2 CTAs per SM, so per-SM DMMA work is balanced to one fragment.
+  // Warp w computes fragments w and w+4 of the CTA (when present).
   extern __shared__ __align__(16) uint8_t sm[];
   constexpr int XV = XVec<TX>::N;
   constexpr int VPR = DM_KC / XV;
-  constexpr int XR = DM_TM * VPR / 128;      // x vectors per thread per chunk
-  constexpr int WR = DM_KC * DM_EP / 2 / 128;  // 16-B W vectors per thread per chunk
+  constexpr int XR = DM_TM * VPR / 128;
+  constexpr int WR = DM_KC * DM_EP / 2 / 128;
   const int64_t T = (int64_t)B * S;
-  const int64_t t0 = (int64_t)blockIdx.x * DM_TM;
+  const int64_t t0 = (int64_t)blockIdx.x * frags_per_cta * 8;
+  const int64_t rows_left = T - t0;
+  const int rows = (int)(rows_left < (int64_t)frags_per_cta * 8 ? rows_left : (int64_t)frags_per_cta * 8);
   const size_t SB = dmma_stage_bytes();
   auto wsb = [&](int buf) { return reinterpret_cast<double*>(sm + buf * SB); };
   auto xsb = [&](int buf) { return reinterpret_cast<double*>(sm + buf * SB + (size_t)DM_KC * DM_WS * 8); };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nc = (d + DM_KC - 1) / DM_KC;
+  const int nfr = (rows + 7) / 8;
+  const bool has0 = warp < nfr, has1 = warp + 4 < nfr;
 
   uint4 xr[XR];
   auto load_x = [&](int c) {
@@ -376,10 +384,10 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
     for (int r = 0; r < XR; ++r) {
       const int i = tid + r * 128;
       const int tok = i / VPR, kv = i % VPR;
-      const int64_t t = t0 + tok;
       const int k = k0 + kv * XV;
       uint4 v = make_uint4(0, 0, 0, 0);
-      if (t < T) {
+      if (tok < rows) {
+        const int64_t t = t0 + tok;
         if (VEC) {
           if (k < d) v = __ldg(reinterpret_cast<const uint4*>(x + t * d + k));
         } else {
@@ -418,7 +426,7 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
 #pragma unroll
     for (int n = 0; n < 8; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
 
-  const int ar = lane >> 2, ac = lane & 3;   // A frag: row, k ; B frag: k = ac, col = ar
+  const int ar = lane >> 2, ac = lane & 3;   // A frag: (row, k); B frag: (k = ac, col = ar)
   load_x(0);
   load_w(0, 0);
   cp_async_commit();
@@ -432,25 +440,78 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
-    const double* xs = xsb(buf) + (warp * 16 + ar) * DM_XS + ac;
+    const double* xs = xsb(buf) + (warp * 8 + ar) * DM_XS + ac;
     const double* ws = wsb(buf) + ac * DM_WS + ar;
+    if (has0) {
 #pragma unroll
-    for (int k4 = 0; k4 < DM_KC; k4 += 4) {
-      const double a0 = xs[k4], a1 = xs[8 * DM_XS + k4];
-      double bf[8];
+      for (int k4 = 0; k4 < DM_KC; k4 += 4) {
+        const double a0 = xs[k4];
+        const double a1 = has1 ? xs[32 * DM_XS + k4] : 0.0;
+        double bf[8];
 #pragma unroll
-      for (int n = 0; n < 8; ++n) bf[n] = ws[k4 * DM_WS + n * 8];
+        for (int n = 0; n < 8; ++n) bf[n] = ws[k4 * DM_WS + n * 8];
 #pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        dmma_8x8x4(acc[0][n][0], acc[0][n][1], a0, bf[n]);
-        dmma_8x8x4(acc[1][n][0], acc[1][n][1], a1, bf[n]);
+        for (int n = 0; n < 8; ++n) dmma_8x8x4(acc[0][n][0], acc[0][n][1], a0, bf[n]);
+        if (has1) {
+#pragma unroll
+          for (int n = 0; n < 8; ++n) dmma_8x8x4(acc[1][n][0], acc[1][n][1], a1, bf[n]);
+        }
       }
     }
     if (c + 1 < nc) store_x(buf ^ 1);
     __syncthreads();
   }
 
-  // ---- epilogue (reuses the staging smem): fp32 logits, f64 softmax
+  if (E == DM_EP) {
+    // ---- register epilogue (E == 64). Lane (ar, ac) holds, for row ar of each
+    // fragment, columns n*8 + 2*ac + j. numpy's pairwise sum over 64 terms uses
+    // accumulators r[c mod 8] folded ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)); each
+    // r[c mod 8] lives in one lane (summed over n in order), so two xor-shuffles
+    // reproduce the exact order (IEEE add is commutative).
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      if (!(m == 0 ? has0 : has1)) continue;
+      const int tok = (warp + 4 * m) * 8 + ar;
+      const bool tv = tok < rows;
+      const int64_t t = t0 + (tv ? tok : 0);
+      const int64_t b = t / S, srow = t % S;
+      float lg[8][2];
+      double mx = -INFINITY;
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int e = n * 8 + 2 * ac + j;
+          lg[n][j] = (float)(acc[m][n][j] + __ldg(tb + b * E + e));   // tensor.py:286-287
+          mx = fmax(mx, (double)lg[n][j]);
+        }
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      double ex[8][2], r[2] = {0.0, 0.0};
+#pragma unroll
+      for (int n = 0; n < 8; ++n)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          ex[n][j] = exp((double)lg[n][j] - mx);
+          r[j] = n == 0 ? ex[n][j] : r[j] + ex[n][j];
+        }
+      double q = r[0] + r[1];
+      q = q + __shfl_xor_sync(0xffffffffu, q, 1);
+      const double sum = q + __shfl_xor_sync(0xffffffffu, q, 2);
+      if (tv) {
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+          *reinterpret_cast<float2*>(logits + t * E + n * 8 + 2 * ac) = make_float2(lg[n][0], lg[n][1]);
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            scores_bes[(b * E + n * 8 + 2 * ac + j) * S + srow] = (float)(ex[n][j] / sum);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- general epilogue (E < 64) through smem (reuses the staging buffers)
   double* ex = reinterpret_cast<double*>(sm);
   float* sc = reinterpret_cast<float*>(sm + (size_t)DM_TM * E * 8);
   float* lg = sc + (size_t)DM_TM * E;
@@ -458,10 +519,9 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
   double* sum = mx + DM_TM;
 #pragma unroll
   for (int m = 0; m < 2; ++m) {
-    const int tok = warp * 16 + m * 8 + ar;
-    const int64_t t = t0 + tok;
-    if (t < T) {
-      const int64_t b = t / S;
+    const int tok = (warp + 4 * m) * 8 + ar;
+    if (tok < rows) {
+      const int64_t b = (t0 + tok) / S;
 #pragma unroll
       for (int n = 0; n < 8; ++n)
 #pragma unroll
@@ -472,29 +532,24 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
     }
   }
   __syncthreads();
-  for (int tok = tid; tok < DM_TM; tok += 128) {
+  for (int tok = tid; tok < rows; tok += 128) {
     double mv = -INFINITY;
     for (int e = 0; e < E; ++e) mv = fmax(mv, (double)lg[tok * E + e]);
     mx[tok] = mv;
   }
   __syncthreads();
-  for (int i = tid; i < DM_TM * E; i += 128) ex[i] = exp((double)lg[i] - mx[i / E]);
+  for (int i = tid; i < rows * E; i += 128) ex[i] = exp((double)lg[i] - mx[i / E]);
   __syncthreads();
-  for (int tok = tid; tok < DM_TM; tok += 128) sum[tok] = np_pairwise_sum(ex + tok * E, E);
+  for (int tok = tid; tok < rows; tok += 128) sum[tok] = np_pairwise_sum(ex + tok * E, E);
   __syncthreads();
-  for (int i = tid; i < DM_TM * E; i += 128) sc[i] = (float)(ex[i] / sum[i / E]);
+  for (int i = tid; i < rows * E; i += 128) sc[i] = (float)(ex[i] / sum[i / E]);
   __syncthreads();
-  for (int i = tid; i < DM_TM * E; i += 128) {
-    const int64_t t = t0 + i / E;
-    if (t < T) logits[t * E + (i % E)] = lg[i];
-  }
-  for (int i = tid; i < DM_TM * E; i += 128) {
-    const int e = i / DM_TM, tok = i % DM_TM;
+  for (int i = tid; i < rows * E; i += 128) logits[(t0 + i / E) * E + (i % E)] = lg[i];
+  for (int i = tid; i < rows * E; i += 128) {
+    const int e = i / rows, tok = i % rows;
     const int64_t t = t0 + tok;
-    if (t < T) {
-      const int64_t b = t / S, s = t % S;
-      scores_bes[(b * E + e) * S + s] = sc[tok * E + e];
-    }
+    const int64_t b = t / S, sr = t % S;
+    scores_bes[(b * E + e) * S + sr] = sc[tok * E + e];
   }
 }
 
@@ -821,7 +876,18 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
   const int64_t T = (int64_t)B * S;
   const bool vec = (d % 8 == 0) && ((uintptr_t)x_norm % 16 == 0);
   if (dmma) {
-    const int grid = (int)((T + DM_TM - 1) / DM_TM);
+    // 8-row fragments, ~2 CTAs per SM, at most 8 fragments (64 rows) per CTA
+    int sms = 148;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int64_t nfrag = (T + 7) / 8;
+    int64_t fpc = (nfrag + 2 * sms - 1) / (2 * sms);
+    if (fpc < 1) fpc = 1;
+    if (fpc > 8) fpc = 8;
+    const int grid = (int)((nfrag + fpc - 1) / fpc);
     const size_t smem = dmma_router_smem(E);
 #define NIMG_DMMA_LAUNCH(TX, V)                                                               \
   do {                                                                                         \
@@ -829,7 +895,7 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     if (err != cudaSuccess) return err;                                                        \
     router_scores_dmma_kernel<TX, V><<<grid, 128, smem, s>>>(                                  \
-        reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d, E);          \
+        reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d, E, (int)fpc); \
   } while (0)
     if (x_bf16) {
       if (vec) NIMG_DMMA_LAUNCH(bf16, true); else NIMG_DMMA_LAUNCH(bf16, false);

@@ -246,3 +246,25 @@ def test_full_width_layer_vs_oracle_and_properties(B, S, C, seed):
     o_ref = O.moe_forward(xn_np[:1], np_of(xm)[:1], te_np[:1], wr_np, *w_np, capacity_factor=C)
     err = rel_fro(np_of(out[:1]), o_ref)
     assert err <= TOL_BF16, f"rel-err {err:.3e}"
+
+
+def test_host_pipeline_matches_direct_calls():
+    """pipeline.HostPipeline (pinned H2D -> moe_forward -> D2H on three
+    streams) returns exactly what direct moe_forward calls return."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    from paper_2604_12163_b200.pipeline import HostPipeline
+    inp = make_layer_inputs(12, 2, 256, 512, 16, 224, mode="bf16")
+    g = to_gpu(inp, "bf16")
+    cfg = R.RouterConfig(d_model=512, n_experts=16, capacity_factor=2.0)
+    bank = bank_of(g)
+    want = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg, bank, g["w_r"]).cpu()
+    host = [g[k].cpu().pin_memory() for k in ("x_norm", "x_mod", "t_emb")]
+    fn = lambda xn, xm, te: M.moe_forward(xm, xn, xm, te, cfg, bank, g["w_r"])
+    pipe = HostPipeline(fn, host, want.shape, want.dtype)
+    for _ in range(5):
+        pipe.step()
+    pipe.drain()
+    torch.cuda.synchronize()
+    for out in pipe.host_out:
+        assert torch.equal(out, want)
