@@ -329,6 +329,10 @@ def run_ep(args, c, peaks, peak_kind):
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # keep stdout to the single JSON line: NCCL / torch init chatter -> stderr
+    sys.stdout.flush()
+    real_stdout = os.dup(1)
+    os.dup2(2, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
@@ -373,7 +377,7 @@ def run_ep(args, c, peaks, peak_kind):
                         inp["w2"][:El].contiguous(), *sw)
     del inp["w1"], inp["w3"], inp["w2"]
     cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=c["C"])
-    ctx = EPContext(overlap=not args.no_overlap)
+    ctx = EPContext(overlap=not args.no_overlap, transport=args.ep_transport)
     step = lambda: ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx)
 
     for _ in range(args.warmup):
@@ -419,6 +423,14 @@ def run_ep(args, c, peaks, peak_kind):
     ms2 = float(t2.item())
     h2d = sum(v.numel() * v.element_size() for v in host.values())
 
+    # per-stage timeline of one more step (rank 0's compute stream)
+    tl = []
+    ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx, timeline=tl)
+    torch.cuda.synchronize()
+    timeline = {n: round(tl[0][1].elapsed_time(e), 4) for n, e in tl}
+
+    sys.stdout.flush()
+    os.dup2(real_stdout, 1)
     if rank == 0:
         a2a = wc["R"] // world * (world - 1) // world * d * 2  # bytes per rank per direction
         line = {
@@ -427,11 +439,15 @@ def run_ep(args, c, peaks, peak_kind):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded randn, random-init weights)",
             "config": {"workload": workload_name(c), "capacity": wc["cap"], "tokens": wc["T"],
-                       "parallelism": f"ep{world} (experts {El}/GPU, samples {bl}/GPU), NCCL all-to-all"
-                                      + ("" if args.no_overlap else ", comm/compute overlap"),
+                       "parallelism": f"ep{world} (experts {El}/GPU, samples {bl}/GPU), "
+                                      + ("NCCL all-to-all" if args.no_overlap else
+                                         ("copy-engine NVLink exchange (CUDA IPC + stream flags)"
+                                          if args.ep_transport == "ce" else "NCCL")
+                                         + ", comm/compute overlap"),
                        "l2": "inputs larger than L2"},
             "a2a_bytes_per_rank_per_direction": a2a,
             "same_config_1gpu": same1,
+            "timeline_ms_rank0": timeline,
             "e2e": {"value": wc["T"] / (ms2 * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step":
                     out_h.numel() * out_h.element_size() * world, "ms_per_step": ms2},
@@ -450,9 +466,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, choices=["cfg2", "cfg4"])
+    ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-overlap", action="store_true", help="EP: plain all-to-alls")
+    ap.add_argument("--ep-transport", default="ce", choices=["ce", "nccl"],
+                    help="EP exchange: copy engines over NVLink (default) or NCCL")
     ap.add_argument("--no-same-config-1gpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per GEMM1 launch, if captured")
@@ -460,6 +479,8 @@ def main():
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     c = dict(CFG2 if (args.config or ("cfg2" if world == 1 else "cfg4")) == "cfg2" else CFG4)
+    if args.batch:
+        c["B"] = args.batch
     if args.impl == "reference":
         run_reference_arm(args, c)
         return

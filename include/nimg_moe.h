@@ -141,6 +141,21 @@ int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_d
                  const void* y_routed, const void* y_shared, const float* gates,
                  const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream);
 
+/* ------------------------------------------------------------------ expert-parallel transport
+ * Copy-engine exchange over NVLink (no SMs, so transfers overlap the persistent
+ * GEMMs). Setup-time: peer-writable buffers shared between the ranks of one
+ * node through CUDA IPC. Hot path: stream-ordered copies and 32-bit flags. */
+int nimg_ipc_alloc(size_t bytes, void** dev_ptr, void* handle /* 64 B out */);
+int nimg_ipc_open(const void* handle /* 64 B */, void** dev_ptr);
+int nimg_ipc_close(void* dev_ptr);
+int nimg_free(void* dev_ptr);
+/* cudaMemcpyAsync device-to-device (peer pointers allowed: copy engine). */
+int nimg_copy_async(void* dst, const void* src, size_t bytes, void* stream);
+/* Stream-ordered 32-bit store (after a full memory barrier) / wait until
+ * *addr >= value. addr may be a peer-mapped flag. */
+int nimg_stream_write_u32(void* dev_addr, uint32_t value, void* stream);
+int nimg_stream_wait_geq_u32(void* dev_addr, uint32_t value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

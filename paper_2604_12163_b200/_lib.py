@@ -22,7 +22,8 @@ EXPORTS = (
     "nimg_last_error", "nimg_abi_version", "nimg_device_sms", "nimg_capacity_for",
     "nimg_moe_workspace_bytes", "nimg_moe_forward", "nimg_route_workspace_bytes", "nimg_route",
     "nimg_gather_rows", "nimg_ffn_path", "nimg_ffn_workspace_bytes", "nimg_expert_ffn",
-    "nimg_combine", "nimg_profile_events",
+    "nimg_combine", "nimg_profile_events", "nimg_ipc_alloc", "nimg_ipc_open", "nimg_ipc_close",
+    "nimg_free", "nimg_copy_async", "nimg_stream_write_u32", "nimg_stream_wait_geq_u32",
 )
 
 
@@ -75,6 +76,13 @@ def _load():
                             C.c_int),
         "nimg_combine": ([I64, I64, I64, I32, I32, P, P, P, P, P, P, P], C.c_int),
         "nimg_profile_events": ([C.POINTER(C.c_void_p), I32], C.c_int),
+        "nimg_ipc_alloc": ([SZ, C.POINTER(C.c_void_p), P], C.c_int),
+        "nimg_ipc_open": ([P, C.POINTER(C.c_void_p)], C.c_int),
+        "nimg_ipc_close": ([P], C.c_int),
+        "nimg_free": ([P], C.c_int),
+        "nimg_copy_async": ([P, P, SZ, P], C.c_int),
+        "nimg_stream_write_u32": ([P, C.c_uint32, P], C.c_int),
+        "nimg_stream_wait_geq_u32": ([P, C.c_uint32, P], C.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

@@ -105,6 +105,8 @@ int map_3d(CUtensorMap* m, const void* base, uint64_t E, uint64_t N, uint64_t K,
   return NIMG_OK;
 }
 
+// SMs the persistent GEMMs size their grid by. NIMG_GEMM_MAX_SMS caps it
+// (leaves SMs for concurrently running communication kernels).
 int device_sms(int* out) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
@@ -112,6 +114,8 @@ int device_sms(int* out) {
   if (dev < 64 && cache[dev]) { *out = cache[dev]; return NIMG_OK; }
   int n = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  const char* cap = getenv("NIMG_GEMM_MAX_SMS");
+  if (cap && atoi(cap) > 1 && atoi(cap) < n) n = atoi(cap) & ~1;
   if (dev < 64) cache[dev] = n;
   *out = n;
   return NIMG_OK;
@@ -542,6 +546,70 @@ int nimg_profile_events(void* const* events, int32_t n) {
   if (n < 0 || n > 8 || (n > 0 && !events)) return fail(NIMG_ERR_CONFIG, "bad event list");
   for (int i = 0; i < n; ++i) g_events[i] = (cudaEvent_t)events[i];
   g_nevents = n;
+  return NIMG_OK;
+}
+
+// ------------------------------------------------------------------ EP transport
+typedef CUresult (*StreamWriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+static void* driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion(name, &p, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return p;
+}
+
+int nimg_ipc_alloc(size_t bytes, void** dev_ptr, void* handle) {
+  if (!dev_ptr || !handle || bytes == 0) return fail(NIMG_ERR_CONFIG, "bad ipc_alloc arguments");
+  CUDA_TRY(cudaMalloc(dev_ptr, bytes));
+  CUDA_TRY(cudaMemset(*dev_ptr, 0, bytes));
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, *dev_ptr));
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  memcpy(handle, &h, sizeof(h));
+  return NIMG_OK;
+}
+
+int nimg_ipc_open(const void* handle, void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(NIMG_ERR_CONFIG, "bad ipc_open arguments");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return NIMG_OK;
+}
+
+int nimg_ipc_close(void* dev_ptr) {
+  CUDA_TRY(cudaIpcCloseMemHandle(dev_ptr));
+  return NIMG_OK;
+}
+
+int nimg_free(void* dev_ptr) {
+  CUDA_TRY(cudaFree(dev_ptr));
+  return NIMG_OK;
+}
+
+int nimg_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return NIMG_OK;
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+  return NIMG_OK;
+}
+
+int nimg_stream_write_u32(void* dev_addr, uint32_t value, void* stream) {
+  static StreamWriteValue32Fn fn = (StreamWriteValue32Fn)driver_fn("cuStreamWriteValue32");
+  if (!fn) return fail(NIMG_ERR_CUDA, "cuStreamWriteValue32 unavailable");
+  CUresult r = fn((CUstream)stream, (CUdeviceptr)dev_addr, value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(NIMG_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  return NIMG_OK;
+}
+
+int nimg_stream_wait_geq_u32(void* dev_addr, uint32_t value, void* stream) {
+  static StreamWaitValue32Fn fn = (StreamWaitValue32Fn)driver_fn("cuStreamWaitValue32");
+  if (!fn) return fail(NIMG_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+  CUresult r = fn((CUstream)stream, (CUdeviceptr)dev_addr, value, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(NIMG_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
   return NIMG_OK;
 }
 

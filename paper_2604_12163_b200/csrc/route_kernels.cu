@@ -357,9 +357,9 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
                           const double* __restrict__ tb, float* __restrict__ logits,
                           float* __restrict__ scores_bes, int B, int S, int d, int E,
                           int frags_per_cta) {
-  // CTA c owns 8-row fragments [c*fpc, (c+1)*fpc) (fpc <= 8) -- the grid is
-  // sized ~2 CTAs per SM, so per-SM DMMA work is balanced to one fragment.
-  // Warp w computes fragments w and w+4 of the CTA (when present).
+  // CTA c owns 8-row fragments [c*fpc, (c+1)*fpc) (fpc <= 8); the grid is sized
+  // to whole multiples of the SM count (>= 2 CTAs per SM) so per-SM DMMA work
+  // is balanced. Warp w computes fragments w and w+4 of the CTA (when present).
   extern __shared__ __align__(16) uint8_t sm[];
   constexpr int XV = XVec<TX>::N;
   constexpr int VPR = DM_KC / XV;
@@ -446,7 +446,7 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
 #pragma unroll
       for (int k4 = 0; k4 < DM_KC; k4 += 4) {
         const double a0 = xs[k4];
-        const double a1 = has1 ? xs[32 * DM_XS + k4] : 0.0;
+        const double a1 = has1 ? xs[32 * DM_XS + k4] : 0.0;   // fragment w+4
         double bf[8];
 #pragma unroll
         for (int n = 0; n < 8; ++n) bf[n] = ws[k4 * DM_WS + n * 8];
@@ -625,9 +625,15 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = tid; i < 256; i += SEL_THREADS) hist[i] = 0;
     __syncthreads();
-    for (int i = tid; i < S; i += SEL_THREADS) {
-      const uint32_t key = keys[i];
-      if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    // warp-aggregated histogram: near-uniform router scores put most keys in
+    // one bin, so per-element smem atomics would serialise on one address
+    for (int i0 = 0; i0 < S; i0 += SEL_THREADS) {
+      const int i = i0 + tid;
+      const uint32_t key = i < S ? keys[i] : 0u;
+      const bool cand = i < S && (key & pmask) == prefix;
+      const uint32_t dig = (key >> shift) & 255u;
+      const unsigned grp = __match_any_sync(0xffffffffu, cand ? dig : 0xFFFFFFFFu);
+      if (cand && lane == __ffs(grp) - 1) atomicAdd(&hist[dig], (unsigned)__popc(grp));
     }
     __syncthreads();
     if (warp == 0) {
@@ -806,7 +812,7 @@ template <typename T, int VEC> struct VecIO {
   NIMG_DEV float at(int i) const { return to_f32(reinterpret_cast<const T*>(v)[i]); }
 };
 
-template <typename TY, typename TO, int VEC, typename ACC>
+template <typename TY, typename TO, int VEC, typename ACC, int UNR>
 __global__ void __launch_bounds__(CB_WARPS * 32)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
@@ -824,40 +830,54 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
     gl[k] = gates[r];
   }
   __syncwarp();
-  for (int c = lane * VEC; c < d; c += 32 * VEC) {
-    VecIO<TY, VEC> sh;
-    sh.load(ys + t * d + c);
-    ACC acc[VEC];
+  constexpr int STEP = 32 * VEC;
+  for (int c0 = lane * VEC; c0 < d; c0 += STEP * UNR) {
+    VecIO<TY, VEC> sh[UNR];
+    ACC acc[UNR][VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[v] = ACC(0);
-    for (int kb = 0; kb < cnt; kb += CB_BATCH) {
-      VecIO<TY, VEC> y[CB_BATCH];
+    for (int u = 0; u < UNR; ++u) {
+      sh[u].load(ys + t * d + c0 + u * STEP);
 #pragma unroll
-      for (int q = 0; q < CB_BATCH; ++q)
-        if (kb + q < cnt) y[q].load(yr + (int64_t)rows[kb + q] * d + c);
+      for (int v = 0; v < VEC; ++v) acc[u][v] = ACC(0);
+    }
+    constexpr int NB = CB_BATCH / UNR;   // rows in flight per batch (registers: NB*UNR vectors)
+    for (int kb = 0; kb < cnt; kb += NB) {
+      VecIO<TY, VEC> y[NB][UNR];
 #pragma unroll
-      for (int q = 0; q < CB_BATCH; ++q) {
+      for (int q = 0; q < NB; ++q)
+        if (kb + q < cnt) {
+          const TY* src = yr + (int64_t)rows[kb + q] * d + c0;
+#pragma unroll
+          for (int u = 0; u < UNR; ++u) y[q][u].load(src + u * STEP);
+        }
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
         if (kb + q < cnt) {
           const float g = gl[kb + q];
 #pragma unroll
-          for (int v = 0; v < VEC; ++v) acc[v] += (ACC)(y[q].at(v) * g);
+          for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[u][v] += (ACC)(y[q][u].at(v) * g);
         }
       }
     }
-    TO res[VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) {
-      const float comb = (float)acc[v];
-      res[v] = from_f32<TO>((float)((ACC)comb + (ACC)sh.at(v)));
-    }
-    TO* o = out + t * d + c;
-    if constexpr (VEC * sizeof(TO) % 16 == 0) {
+    for (int u = 0; u < UNR; ++u) {
+      TO res[VEC];
 #pragma unroll
-      for (int i = 0; i < VEC * (int)sizeof(TO) / 16; ++i)
-        reinterpret_cast<uint4*>(o)[i] = reinterpret_cast<const uint4*>(res)[i];
-    } else {
+      for (int v = 0; v < VEC; ++v) {
+        const float comb = (float)acc[u][v];
+        res[v] = from_f32<TO>((float)((ACC)comb + (ACC)sh[u].at(v)));
+      }
+      TO* o = out + t * d + c0 + u * STEP;
+      if constexpr (VEC * sizeof(TO) % 16 == 0) {
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) o[v] = res[v];
+        for (int i = 0; i < VEC * (int)sizeof(TO) / 16; ++i)
+          reinterpret_cast<uint4*>(o)[i] = reinterpret_cast<const uint4*>(res)[i];
+      } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) o[v] = res[v];
+      }
     }
   }
 }
@@ -883,8 +903,12 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    // k CTAs per SM (fewest rounds that keep <= 8 fragments per CTA, >= 2),
+    // fragments spread evenly over them
     const int64_t nfrag = (T + 7) / 8;
-    int64_t fpc = (nfrag + 2 * sms - 1) / (2 * sms);
+    int64_t k = (nfrag + 8LL * sms - 1) / (8LL * sms);
+    if (k < 2) k = 2;
+    int64_t fpc = (nfrag + k * sms - 1) / (k * sms);
     if (fpc < 1) fpc = 1;
     if (fpc > 8) fpc = 8;
     const int grid = (int)((nfrag + fpc - 1) / fpc);
@@ -975,11 +999,14 @@ static void combine_dispatch(const void* yr, const void* ys, const float* gates,
   const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
   const size_t smem = (size_t)CB_WARPS * E * 8;
   using ACC = typename std::conditional<sizeof(TO) == 2, float, double>::type;
-  if (d % 8 == 0)
-    combine_kernel<TY, TO, 8, ACC><<<grid, CB_WARPS * 32, smem, s>>>(
+  if (d % 512 == 0)
+    combine_kernel<TY, TO, 8, ACC, 2><<<grid, CB_WARPS * 32, smem, s>>>(
+        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
+  else if (d % 8 == 0)
+    combine_kernel<TY, TO, 8, ACC, 1><<<grid, CB_WARPS * 32, smem, s>>>(
         (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
   else
-    combine_kernel<TY, TO, 1, ACC><<<grid, CB_WARPS * 32, smem, s>>>(
+    combine_kernel<TY, TO, 1, ACC, 1><<<grid, CB_WARPS * 32, smem, s>>>(
         (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
 }
 

@@ -17,10 +17,18 @@ is unnecessary and both exchanges are uniform all-to-alls:
             1-GPU layout -- and the deterministic combine runs unchanged.
             Hence EP(R) == 1-GPU bitwise (tested).
 
-Overlap (default): the dispatch all-to-all runs on a comm stream while the
-compute stream runs the shared expert and the rank's own chunk; remote chunks
-are then computed one source rank at a time and each finished chunk is sent
-back on a second communicator while the next chunk computes.
+Transports.
+  "ce" (default): copy engines over NVLink. Receive and return buffers are
+      CUDA-IPC shared between the ranks; every chunk moves with one
+      cudaMemcpyAsync straight into the peer's buffer on a per-peer stream, and
+      per-step 32-bit flags (cuStreamWriteValue32 into the peer's flag array /
+      cuStreamWaitValue32 locally) order producer and consumer. No SMs are
+      used, so transfers overlap the persistent tensor-core GEMMs, which hold
+      every SM and would otherwise starve NCCL's copy kernels.
+  "nccl": all_to_all for the dispatch on a comm stream (overlapping the shared
+      expert and the rank's own chunk), per-chunk P2P returns on a second
+      communicator. Kept for comparison.
+  overlap=False: two blocking all_to_alls.
 """
 
 from __future__ import annotations
@@ -31,6 +39,10 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
+import ctypes as C
+
+from . import _lib
+from ._tensors import stream_handle
 from .errors import ConfigError
 from .moe import ExpertBank
 from .router import RouterConfig, build_routing, capacity_for
@@ -98,16 +110,98 @@ def shard_bank(bank: ExpertBank, rank: int, world: int) -> ExpertBank:
                       bank.shared_w2)
 
 
-class EPContext:
-    """Process groups and streams for one expert-parallel layer."""
+class _CAI:
+    """__cuda_array_interface__ over a raw device pointer (no ownership)."""
 
-    def __init__(self, group=None, overlap: bool = True):
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1",
+                                         "data": (ptr, False), "version": 3}
+
+
+def _view(ptr: int, shape, dtype: torch.dtype, device) -> torch.Tensor:
+    n = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+    return torch.as_tensor(_CAI(ptr, n), device=device).view(dtype).view(shape)
+
+
+class PeerBuffer:
+    """A device buffer per rank, mapped into every other rank of the group
+    (CUDA IPC; ranks of one node)."""
+
+    def __init__(self, nbytes: int, group, rank: int, world: int):
+        own = C.c_void_p()
+        handle = (C.c_uint8 * 64)()
+        _lib.check(_lib.lib.nimg_ipc_alloc(nbytes, C.byref(own), handle))
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(handle), group=group)
+        self.ptrs, self._opened = [], []
+        for q in range(world):
+            if q == rank:
+                self.ptrs.append(own.value)
+                continue
+            p = C.c_void_p()
+            _lib.check(_lib.lib.nimg_ipc_open((C.c_uint8 * 64).from_buffer_copy(handles[q]),
+                                              C.byref(p)))
+            self.ptrs.append(p.value)
+            self._opened.append(p.value)
+        self.own = own.value
+        self.nbytes = nbytes
+
+    def close(self):
+        for p in self._opened:
+            _lib.lib.nimg_ipc_close(p)
+        _lib.lib.nimg_free(self.own)
+        self._opened, self.ptrs = [], []
+
+
+class CETransport:
+    """Copy-engine exchange state for one (shape, dtype) of the EP layer."""
+
+    def __init__(self, group, rank, world, chunk_rows, d, act, ydt, device):
+        self.rank, self.world, self.chunk_rows, self.d = rank, world, chunk_rows, d
+        self.act_es = torch.empty((), dtype=act).element_size()
+        self.y_es = torch.empty((), dtype=ydt).element_size()
+        rows = world * chunk_rows
+        self.recv = PeerBuffer(rows * d * self.act_es, group, rank, world)
+        self.yback = PeerBuffer(rows * d * self.y_es, group, rank, world)
+        self.flags = PeerBuffer(3 * world * 4, group, rank, world)   # disp | ret | comb
+        self.recv_t = _view(self.recv.own, (world, chunk_rows, d), act, device)
+        self.yback_t = _view(self.yback.own, (world, chunk_rows, d), ydt, device)
+        self.streams = [torch.cuda.Stream(device) for _ in range(world)]
+        self.epoch = 0
+        self.key = (chunk_rows, d, act, ydt)
+        dist.barrier(group=group)   # every buffer zeroed and mapped before first use
+
+    def flag(self, owner: int, kind: int, idx: int) -> int:
+        return self.flags.ptrs[owner] + 4 * (kind * self.world + idx)
+
+    def close(self):
+        for b in (self.recv, self.yback, self.flags):
+            b.close()
+
+
+class EPContext:
+    """Process groups, streams and transport state of one expert-parallel layer."""
+
+    def __init__(self, group=None, overlap: bool = True, transport: str = "ce"):
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.overlap = overlap and self.world > 1
+        if transport not in ("ce", "nccl"):
+            raise ConfigError(f"unknown EP transport {transport!r}")
+        self.transport = transport
+        self._ce = None
         self._ret_group = None
         self._streams = None
+
+    def ce(self, chunk_rows, d, act, ydt, device) -> CETransport:
+        key = (chunk_rows, d, act, ydt)
+        if self._ce is None or self._ce.key != key:
+            if self._ce is not None:
+                torch.cuda.synchronize()
+                self._ce.close()
+            self._ce = CETransport(self.group, self.rank, self.world, chunk_rows, d, act, ydt, device)
+        return self._ce
 
     @property
     def ret_group(self):
@@ -123,8 +217,15 @@ class EPContext:
         return self._streams
 
 
+def _mark(timeline, name):
+    if timeline is not None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        timeline.append((name, ev))
+
+
 def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBank, w_r,
-                   ctx: EPContext, stages=None, return_routing: bool = False):
+                   ctx: EPContext, stages=None, return_routing: bool = False, timeline=None):
     """Expert-parallel moe_forward (moe.py:138-164) for this rank's samples.
 
     x_norm, x_mod: (B_l, S, d) local samples; bank_local: this rank's El
@@ -145,8 +246,11 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
     xm = x_mod.reshape(T, d)
     w = bank_local
 
+    _mark(timeline, "start")
     r = stages.route(x_norm, t_emb, w_r, cfg, cap)
+    _mark(timeline, "routed")
     xg = stages.gather(xm, r["token_flat"])                       # (E*B_l*cap, d)
+    _mark(timeline, "gathered")
 
     if not ctx.overlap:
         recv = torch.empty_like(xg)
@@ -162,17 +266,22 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
             dist.all_to_all_single(y_back, y_recv, group=ctx.group)
         else:
             y_back.copy_(y_recv)
+    elif ctx.transport == "ce":
+        y_back, y_sh = _ce_exchange(plan, ctx, stages, xg, xm, w, timeline)
     else:
-        y_back, y_sh = _overlapped_exchange(plan, ctx, stages, xg, xm, w)
-
+        y_back, y_sh = _overlapped_exchange(plan, ctx, stages, xg, xm, w, timeline)
+    _mark(timeline, "returned")
     out = stages.combine(y_back, y_sh, r, act).view(B_l, S, d)
+    if ctx.overlap and ctx.transport == "ce":
+        ce_after_combine(ctx)
+    _mark(timeline, "combined")
     if return_routing:
         decisions, routing = build_routing(r, B_l, S, E, cap)
         return out, decisions, routing
     return out
 
 
-def _overlapped_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w):
+def _overlapped_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None):
     R, me, n = plan.world, plan.rank, plan.chunk_rows
     comp = torch.cuda.current_stream()
     s_disp, s_ret = ctx.streams()
@@ -196,14 +305,17 @@ def _overlapped_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w):
     y_back = torch.empty((R, n, d), dtype=ydt, device=xg.device)
     _, y_sh = stages.expert_ffn(xg_c[me], coff, cex, w.w1, w.w3, w.w2, xm, w.shared_w1,
                                 w.shared_w3, w.shared_w2, y_routed=y_back[me])
+    _mark(timeline, "own+shared")
 
     comp.wait_event(disp_done)
+    _mark(timeline, "dispatched")
     ret_group = ctx.ret_group
     for s in range(1, R):
         send_to, recv_from = plan.step_peers(s)           # dispatch pairing of step s
         # chunk that arrived from `recv_from` -> compute -> send back to it
         stages.expert_ffn(recv_c[recv_from], coff, cex, w.w1, w.w3, w.w2, None, None, None, None,
                           y_routed=y_recv[recv_from])
+        _mark(timeline, f"chunk{s}")
         s_ret.wait_stream(comp)
         with torch.cuda.stream(s_ret):
             ops = [dist.P2POp(dist.isend, y_recv[recv_from], recv_from, group=ret_group),
@@ -212,3 +324,89 @@ def _overlapped_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w):
                 wk.wait()
     comp.wait_stream(s_ret)
     return y_back.view(R * n, -1), y_sh
+
+
+def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None):
+    """Copy-engine dispatch / return with per-step flags (see module doc).
+
+    Flags in rank r's array: disp[src] (src's chunk for r has landed in r's
+    recv), ret[q] (q's results for r have landed in r's y_back; also: q has
+    consumed r's previous chunk), comb[src] (src combined the previous step, so
+    its y_back slot for r may be overwritten)."""
+    L = _lib.lib
+    R, me, n = plan.world, plan.rank, plan.chunk_rows
+    d = xg.shape[1]
+    dev = xg.device
+    ydt = stages.ffn_y_dtype(xg.dtype, d, w.w1.shape[1], w.shared_w1.shape[0])
+    tp = ctx.ce(n, d, xg.dtype, ydt, dev)
+    tp.epoch += 1
+    k = tp.epoch
+    DISP, RET, COMB = 0, 1, 2
+    comp = torch.cuda.current_stream()
+    xbytes, ybytes = n * d * tp.act_es, n * d * tp.y_es
+    coff, cex = plan.chunk_segments()
+
+    # dispatch: one copy per destination rank, straight into its recv slot
+    x_ready = torch.cuda.Event()
+    x_ready.record(comp)
+    for s in range(1, R):
+        q = (me + s) % R
+        st = tp.streams[q]
+        st.wait_event(x_ready)
+        sh = st.cuda_stream
+        if k > 1:   # q consumed my previous chunk
+            _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, RET, q), k - 1, sh))
+        _lib.check(L.nimg_copy_async(tp.recv.ptrs[q] + me * xbytes, xg[q * n:(q + 1) * n].data_ptr(),
+                                     xbytes, sh))
+        _lib.check(L.nimg_stream_write_u32(tp.flag(q, DISP, me), k, sh))
+        xg.record_stream(st)
+
+    # shared expert first (needs no exchange; covers the dispatch copies)
+    _, y_sh = stages.expert_ffn(None, None, None, None, None, None, xm, w.shared_w1, w.shared_w3,
+                                w.shared_w2)
+    _mark(timeline, "shared")
+
+    y_recv = torch.empty((R, n, d), dtype=ydt, device=dev)
+    for s in range(1, R):
+        src = (me - s) % R
+        _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, DISP, src), k, comp.cuda_stream))
+        stages.expert_ffn(tp.recv_t[src], coff, cex, w.w1, w.w3, w.w2, None, None, None, None,
+                          y_routed=y_recv[src])
+        _mark(timeline, f"chunk{s}")
+        done = torch.cuda.Event()
+        done.record(comp)
+        st = tp.streams[src]
+        st.wait_event(done)
+        sh = st.cuda_stream
+        if k > 1:   # src has combined the previous step: its y_back slot is free
+            _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, COMB, src), k - 1, sh))
+        _lib.check(L.nimg_copy_async(tp.yback.ptrs[src] + me * ybytes, y_recv[src].data_ptr(),
+                                     ybytes, sh))
+        _lib.check(L.nimg_stream_write_u32(tp.flag(src, RET, me), k, sh))
+    for st in tp.streams:
+        y_recv.record_stream(st)
+
+    # own chunk last: its result needs no transfer, so it hides the last return
+    stages.expert_ffn(xg[me * n:(me + 1) * n], coff, cex, w.w1, w.w3, w.w2, None, None, None,
+                      None, y_routed=tp.yback_t[me])
+    _mark(timeline, "own")
+
+    for q in range(R):
+        if q != me:
+            _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, RET, q), k, comp.cuda_stream))
+    return tp.yback_t.view(R * n, d), y_sh
+
+
+def ce_after_combine(ctx: EPContext):
+    """Tell every peer that this rank's y_back slots are free again."""
+    tp = ctx._ce
+    if tp is None:
+        return
+    done = torch.cuda.Event()
+    done.record(torch.cuda.current_stream())
+    for q in range(tp.world):
+        if q == tp.rank:
+            continue
+        st = tp.streams[q]
+        st.wait_event(done)
+        _lib.check(_lib.lib.nimg_stream_write_u32(tp.flag(q, 2, tp.rank), tp.epoch, st.cuda_stream))

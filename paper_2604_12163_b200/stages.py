@@ -77,8 +77,8 @@ class CudaStages:
         nbytes = C.c_size_t()
         _lib.check(_lib.lib.nimg_ffn_workspace_bytes(C.byref(desc), C.byref(nbytes)))
         ws = workspace(nbytes.value)
-        off = np.ascontiguousarray(seg_offsets, dtype=np.int64)
-        ex = np.ascontiguousarray(seg_expert, dtype=np.int32)
+        off = np.ascontiguousarray(seg_offsets if nseg else [0], dtype=np.int64)
+        ex = np.ascontiguousarray(seg_expert if nseg else [0], dtype=np.int32)
         _lib.check(_lib.lib.nimg_expert_ffn(
             C.byref(desc), off.ctypes.data if nseg else None, ex.ctypes.data if nseg else None,
             ptr(x_routed) if nr else None, ptr(w1) if nr else None, ptr(w3) if nr else None,
