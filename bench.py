@@ -46,6 +46,15 @@ def load_peaks():
     return dict(FALLBACK_PEAKS), "fallback"
 
 
+def gemm1_traffic():
+    """DRAM bytes per GEMM1 launch from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "gemm_traffic_r01.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
+    return None
+
+
 def work_counts(c):
     """Algorithmic work per layer step."""
     B, S, d, h, E = c["B"], c["S"], c["d"], c["h"], c["E"]
@@ -274,13 +283,16 @@ def run_single(args, c, peaks, peak_kind):
         "expert_gemm_frac_of_peak": ffn_tf / tf_peak,
         "roofline": {"bound": "tensor", "kernel": "grouped_gemm_sm100<0> (GEMM1 dual-B SwiGLU)",
                      "achieved": g1_tf, "peak": tf_peak, "unit": "TFLOP/s",
-                     "frac": g1_tf / tf_peak, "traffic": args.traffic,
+                     "frac": g1_tf / tf_peak,
+                     "traffic": args.traffic if args.traffic is not None else gemm1_traffic(),
+                     "traffic_unit": "bytes (dram read+write per launch, ncu)",
                      "peak_source": f"{peak_kind} bf16_tflops (burst)",
+                     "kernel_impl": "grouped_gemm_sm100_pair<0>: tcgen05 cta_group::2, UMMA 256x224x16",
                      "algorithmic": f"4*d*h*(R_rows+T) = {wc['flops_g1']:.4g} FLOP per launch"},
         "stages": stage_detail,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": 9 * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)

@@ -206,9 +206,14 @@ def test_decoupling_and_determinism_and_permutation():    # test_moe.py:194-217,
 
 
 # ---------------------------------------------------------------- full size
-@pytest.mark.parametrize("B,S,C,seed", [(16, 1024, 4.0, 2), (4, 4096, 2.0, 4)])
+@pytest.mark.parametrize("B,S,C,seed", [
+    (16, 1024, 4.0, 2),                       # cfg2 (512px, S512 stage)
+    (4, 4096, 2.0, 4),                        # cfg4 shape (1024px, C=2)
+    (2, 4096, 8.0, 31), (2, 4096, 4.0, 32),   # cfg3 capacity sweep: cap 512 / 256
+    (2, 4032, 2.0, 33), (2, 3840, 2.0, 34),   # multi-aspect 1024 buckets: cap 126 / 120
+])
 def test_full_width_layer_vs_oracle_and_properties(B, S, C, seed):
-    """cfg2 / 1024px shapes at full width (d=2048, h=1344, E=64) in bf16.
+    """cfg2 / cfg3 / cfg4 / bucket shapes at full width (d=2048, h=1344, E=64) in bf16.
     Routing for every sample is checked bit-exactly against the oracle's
     router; the layer output of sample 0 against the oracle's full layer;
     plus size-independent properties over the whole batch."""
@@ -268,3 +273,59 @@ def test_host_pipeline_matches_direct_calls():
     torch.cuda.synchronize()
     for out in pipe.host_out:
         assert torch.equal(out, want)
+
+
+def test_full_width_fp32_mode_layer():
+    """fp32 mode (CUDA-core expert GEMMs, no TF32) at full width, one 512px
+    sample: routing bit-exact, layer rel-err <= 1e-4 against the oracle."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    B, S, d, h, E, C = 1, 1024, 2048, 1344, 64, 4.0
+    inp = make_layer_inputs(41, B, S, d, E, h, layer=17, mode="fp32")
+    g = to_gpu(inp, "fp32")
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    out, dec, routing = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg,
+                                      bank_of(g), g["w_r"], return_routing=True)
+    ref_out, ref = O.moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"], inp["w1"],
+                                 inp["w3"], inp["w2"], inp["sw1"], inp["sw3"], inp["sw2"],
+                                 capacity_factor=C, return_routing=True)
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), ref["token_flat"])
+    np.testing.assert_array_equal(np_of(routing["gates"]), ref["gates"])
+    np.testing.assert_array_equal(np_of(routing["logits"]), ref["logits"])
+    err = rel_fro(np_of(out), ref_out)
+    assert err <= TOL_FP32, f"fp32-mode rel-err {err:.3e}"
+
+
+@pytest.mark.parametrize("E,C", [(128, 4.0), (96, 2.0)])
+def test_router_more_than_64_experts(E, C):
+    """E > 64 takes the general FP64 router (DFMA) path: bit-exact vs the oracle."""
+    from oracle.workloads import make_router_inputs
+    from paper_2604_12163_b200 import router as R
+    inp = make_router_inputs(51, 2, 512, 512, E, mode="bf16")
+    g = to_gpu(inp, "bf16")
+    cfg = R.RouterConfig(d_model=512, n_experts=E, capacity_factor=C)
+    dec, routing = R.route_full(g["x_norm"], g["t_emb"], g["w_r"], cfg)
+    ref = O.route_full(inp["x_norm"], inp["t_emb"], inp["w_r"], n_experts=E, capacity_factor=C)
+    np.testing.assert_array_equal(np_of(routing["logits"]), ref["logits"])
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), ref["token_flat"])
+    np.testing.assert_array_equal(np_of(routing["gates"]), ref["gates"])
+
+
+def test_nan_scores_sort_last():
+    """numpy's argsort(-x, stable) puts NaN last (router.py:100): a NaN row of
+    x_norm makes that token's scores NaN, so no expert may pick it before any
+    finite-scored token, and ties among NaNs go to the lower index."""
+    from paper_2604_12163_b200 import router as R
+    rng = np.random.default_rng(3)
+    S, d, E = 64, 16, 4
+    xn = rng.normal(size=(1, S, d)).astype(np.float32)
+    xn[0, [5, 9]] = np.nan
+    te = rng.normal(size=(1, d)).astype(np.float32)
+    wr = rng.normal(size=(2 * d, E)).astype(np.float32)
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=float(E))   # cap = S
+    dec, routing = R.route_full(torch.tensor(xn).cuda(), torch.tensor(te).cuda(),
+                                torch.tensor(wr).cuda(), cfg)
+    ref = O.route_full(xn, te, wr, n_experts=E, capacity_factor=float(E))
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), ref["token_flat"])
+    for e in range(E):
+        assert list(dec[0].top_indices[e][-2:]) == [5, 9]
