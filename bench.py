@@ -292,7 +292,7 @@ def run_single(args, c, peaks, peak_kind):
         "stages": stage_detail,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 9 * args.steps,
+        "gpu_launches": 8 * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
