@@ -278,8 +278,9 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       if (q && !aligned16(q)) return fail(NIMG_ERR_SHAPE, "tensor not 16-byte aligned");
     int sms = 0;
     NIMG_TRY(device_sms(&sms));
-    // CTA-pair (cta_group::2) kernels unless the A rows are gathered in-kernel
-    const bool pair = use_pair_kernels() && gather_idx == nullptr;
+    // CTA-pair (cta_group::2) kernels; they gather A rows with cp.async, the
+    // 1-CTA kernels with TMA gather4
+    const bool pair = use_pair_kernels();
     const int tile_rows = pair ? tc_pair_rows() : 128;
     // GEMM1: pre = SiLU(x W1^T) * (x W3^T)
     {
@@ -303,8 +304,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       }
       if (!has_r) { tm.a[0] = tm.a[1]; tm.b[0] = tm.b[1]; tm.b3[0] = tm.b3[1]; }
       if (!has_s) { tm.a[1] = tm.a[rb]; tm.b[1] = tm.b[rb]; tm.b3[1] = tm.b3[rb]; }
-      p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0, gather_idx};
-      p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, nullptr};
+      p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0, gather_idx, gather_idx ? xr : nullptr};
+      p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, nullptr, nullptr};
       if (pair) CUDA_TRY(launch_grouped_tc_pair(0, tm, p, sms, st));
       else CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
       mark(3, st);
@@ -329,8 +330,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       if (!has_s) { tm.a[1] = tm.a[0]; tm.b[1] = tm.b[0]; }
       tm.b3[0] = tm.b[0];
       tm.b3[1] = tm.b[1];
-      p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0, nullptr};
-      p.bank[1] = GBank{ys, d, hs, d, (d + bn - 1) / bn, 0, nullptr};
+      p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0, nullptr, nullptr};
+      p.bank[1] = GBank{ys, d, hs, d, (d + bn - 1) / bn, 0, nullptr, nullptr};
       if (pair) CUDA_TRY(launch_grouped_tc_pair(1, tm, p, sms, st));
       else CUDA_TRY(launch_grouped_tc(1, tm, p, sms, st));
     }
@@ -385,16 +386,20 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
   return NIMG_OK;
 }
 
-// Fusing the routed-row gather into GEMM1 (TMA tile::gather4, one 4-row load
-// per lane) is correct but measured 2.7x slower on B200: gather4 issues at
-// ~45 cycles per 512 B, and a 128x64 A tile needs 32 of them per 448-cycle
-// MMA k-block. Off by default; NIMG_FUSED_GATHER=1 enables it for experiments.
-bool use_fused_gather(int32_t path) {
+// Routed-row gather (moe.py:152-153): a separate HBM-bound kernel by default.
+// NIMG_FUSED_GATHER=1 fuses it into GEMM1's operand load instead -- the pair
+// kernel copies the token_flat-selected x_mod rows with cp.async (relay-warp
+// signalled), the 1-CTA kernel (NIMG_PAIR=0) with TMA tile::gather4. Both are
+// correct (bitwise equal, tests/test_gpu_parity.py) but slower on B200:
+// LDGSTS sustains ~8 B/cycle/SM and gather4 issues at ~45 cycles per 512 B,
+// against the ~36 B/cycle/SM of A operand the UMMA consumes (GEMM1 1.51 ms /
+// 1.83 ms fused vs 0.63 ms + 0.064 ms separate gather at cfg2).
+bool use_fused_gather(int32_t path, int64_t d) {
   static const bool on = [] {
     const char* e = getenv("NIMG_FUSED_GATHER");
     return e && e[0] == '1';
   }();
-  return on && path == NIMG_PATH_TCGEN05;
+  return on && path == NIMG_PATH_TCGEN05 && d % 64 == 0;
 }
 
 nimg_ffn_desc layer_ffn_desc(const nimg_moe_desc* d) {
@@ -495,7 +500,7 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   int32_t path, ydt;
   nimg_ffn_path(&f, &path, &ydt);
   // the gathered-row buffer exists only when the gather is not fused into GEMM1
-  const size_t xg = use_fused_gather(path) ? 0 : align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
+  const size_t xg = use_fused_gather(path, d->d) ? 0 : align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
   *bytes = route_ws_bytes(d) + xg + ffn_ws_bytes(&f) + align_up((size_t)f.n_rows * d->d * elt(ydt)) +
            align_up((size_t)f.n_shared_rows * d->d * elt(ydt));
   return NIMG_OK;
@@ -512,7 +517,7 @@ int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, s
   const nimg_ffn_desc f = layer_ffn_desc(d);
   int32_t path, ydt;
   nimg_ffn_path(&f, &path, &ydt);
-  const bool fused_gather = use_fused_gather(path);
+  const bool fused_gather = use_fused_gather(path, d->d);
   uint8_t* w = static_cast<uint8_t*>(ws);
   void* route_ws = w;                 w += route_ws_bytes(d);
   void* xg = w;                       if (!fused_gather) w += align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));

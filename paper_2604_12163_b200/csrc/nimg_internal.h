@@ -19,7 +19,8 @@ struct GBank {
   int N;           // output columns (h for GEMM1, d for GEMM2)
   int ntn;         // N tiles
   int pad_;
-  const int32_t* a_idx;  // GEMM1 only: A row r is source row a_idx[r] (TMA gather4); null = contiguous
+  const int32_t* a_idx;  // GEMM1 only: A row r is source row a_idx[r]; null = contiguous
+  const void* a_src;     // gather source rows (bf16, K elements per row) when a_idx != null
 };
 
 // Segments [0, nseg0) use bank 0, [nseg0, nseg) bank 1. Segment i covers rows
