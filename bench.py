@@ -261,6 +261,10 @@ def run_single(args, c, peaks, peak_kind):
         "combine_gbs": wc["bytes_combine"] / (stages["combine"] * 1e-3) / 1e9,
     }
 
+    # ---- the backbone's MoE branch around the layer:
+    # fused prologue + layer + gated residual in the combine epilogue
+    block = run_block(args, c, inp, cfg, bank, ms)
+
     # ---- e2e through the public API with host buffers
     e2e = run_e2e(args, c, inp, cfg, bank)
 
@@ -290,12 +294,42 @@ def run_single(args, c, peaks, peak_kind):
                      "kernel_impl": "grouped_gemm_sm100_pair<0>: tcgen05 cta_group::2, UMMA 256x224x16",
                      "algorithmic": f"4*d*h*(R_rows+T) = {wc['flops_g1']:.4g} FLOP per launch"},
         "stages": stage_detail,
+        "block": block,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": 8 * args.steps,
         "clocks": clocks,
     }
     print(json.dumps(line), flush=True)
+
+
+def run_block(args, c, inp, cfg, bank, layer_ms):
+    """block.moe_block_forward (backbone.py:583-606) on the same shapes."""
+    import torch
+    from paper_2604_12163_b200 import block as BK
+    B, S, d = c["B"], c["S"], c["d"]
+    g = torch.Generator(device="cuda").manual_seed(c["seed"] + 100)
+    x = torch.randn(B, S, d, generator=g, device="cuda").to(torch.bfloat16)
+    ra = (0.5 * torch.randn(B, S, d, generator=g, device="cuda")).to(torch.bfloat16)
+    mods = [0.2 * torch.randn(B, d, generator=g, device="cuda") for _ in range(3)]
+    step = lambda: BK.moe_block_forward(x, mods[0], ra, mods[1], mods[2], inp["t_emb"], c["layer"],
+                                        cfg, bank, inp["w_r"])
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    T = B * S
+    return {"ms_per_step": ms, "tokens_per_s": T / (ms * 1e-3),
+            "overhead_vs_layer_ms": ms - layer_ms,
+            "what": "h = x + tanh(sa_gate) r; x_norm = rmsnorm(h)/sqrt(l+1); x_mod = x_norm (1+ff_scale); "
+                    "layer; out = h + tanh(ff_gate) moe (one prologue kernel + residual in combine)",
+            "prologue_algorithmic_bytes": T * d * 2 * 5}
 
 
 def run_e2e(args, c, inp, cfg, bank):

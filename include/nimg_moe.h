@@ -109,6 +109,30 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
 int nimg_moe_forward(const nimg_moe_desc* desc, const nimg_moe_ptrs* ptrs, void* ws,
                      size_t ws_bytes, void* stream);
 
+/* The backbone's MoE branch around the layer (backbone.py:583-606):
+ *   h = x + tanh(sa_gate) r_attn;  x_norm = rmsnorm(h) / sqrt(layer+1);
+ *   x_mod = x_norm (1 + ff_scale);  moe = moe_forward(h, x_norm, x_mod, t_vec);
+ *   out = h + tanh(ff_gate) moe.
+ * The prologue is one fused pass; the gated residual is the combine's epilogue. */
+typedef struct nimg_block_ptrs {
+  const void* x;         /* (B,S,d) act: residual stream entering the branch */
+  const void* r_attn;    /* (B,S,d) act: attention output */
+  const float* sa_gate;  /* (B,d) fp32 */
+  const float* ff_scale; /* (B,d) fp32 */
+  const float* ff_gate;  /* (B,d) fp32 */
+  const float* t_vec;    /* (B,d) fp32: router timestep input */
+  const float* w_r;      /* (2d,E) fp32 */
+  const void *w1, *w3, *w2, *sw1, *sw3, *sw2;
+  void* h;               /* (B,S,d) act out */
+  void* x_norm;          /* (B,S,d) act out */
+  void* x_mod;           /* (B,S,d) act out */
+  void* out;             /* (B,S,d) act out: h + tanh(ff_gate) * moe */
+  nimg_route_out route;
+} nimg_block_ptrs;
+int nimg_moe_block_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
+int nimg_moe_block_forward(const nimg_moe_desc* desc, const nimg_block_ptrs* ptrs, int32_t layer,
+                           void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------ stages */
 int nimg_route_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
 /* router.py:104-162  route_full (logits, softmax, per-(b,e) top-cap,

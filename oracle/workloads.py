@@ -95,3 +95,30 @@ def digest(arrays: dict) -> str:
         h.update(str(a.shape).encode())
         h.update(a.tobytes())
     return h.hexdigest()
+
+
+def make_block_inputs(seed: int, B: int, S: int, d: int, E: int, h: int, mode: str = "fp32"):
+    """Inputs of the backbone's MoE branch (backbone.py:583-606): residual x,
+    attention output r_attn (act dtype), per-sample modulation vectors
+    sa_gate / ff_scale / ff_gate (fp32, small, as from the zero-init mod_w
+    after training), t_vec (fp32), router and expert weights."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((B, S, d))
+    r_attn = rng.standard_normal((B, S, d)) * 0.5
+    sa_gate = rng.standard_normal((B, d)) * 0.3
+    ff_scale = rng.standard_normal((B, d)) * 0.1
+    ff_gate = rng.standard_normal((B, d)) * 0.3
+    t_vec = rng.standard_normal((B, d))
+    w_r = trunc_normal(rng, (2 * d, E), 0.006)
+    ws = {k: trunc_normal(rng, s, 0.02) for k, s in (("w1", (E, h, d)), ("w3", (E, h, d)),
+                                                     ("w2", (E, d, h)), ("sw1", (h, d)),
+                                                     ("sw3", (h, d)), ("sw2", (d, h)))}
+    out = dict(x=x, r_attn=r_attn, sa_gate=sa_gate, ff_scale=ff_scale, ff_gate=ff_gate,
+               t_vec=t_vec, w_r=w_r, **ws)
+    out = {k: np.ascontiguousarray(v, dtype=np.float32) for k, v in out.items()}
+    if mode == "bf16":
+        for k in ("x", "r_attn", "w1", "w3", "w2", "sw1", "sw3", "sw2"):
+            out[k] = bf16_round(out[k])
+    elif mode != "fp32":
+        raise ValueError(mode)
+    return out

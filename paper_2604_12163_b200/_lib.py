@@ -24,6 +24,7 @@ EXPORTS = (
     "nimg_gather_rows", "nimg_ffn_path", "nimg_ffn_workspace_bytes", "nimg_expert_ffn",
     "nimg_combine", "nimg_profile_events", "nimg_ipc_alloc", "nimg_ipc_open", "nimg_ipc_close",
     "nimg_free", "nimg_copy_async", "nimg_stream_write_u32", "nimg_stream_wait_geq_u32",
+    "nimg_moe_block_workspace_bytes", "nimg_moe_block_forward",
 )
 
 
@@ -45,6 +46,15 @@ class MoePtrs(C.Structure):
                 ("w_r", C.c_void_p), ("w1", C.c_void_p), ("w3", C.c_void_p), ("w2", C.c_void_p),
                 ("sw1", C.c_void_p), ("sw3", C.c_void_p), ("sw2", C.c_void_p),
                 ("out", C.c_void_p), ("route", RouteOut)]
+
+
+class BlockPtrs(C.Structure):
+    _fields_ = [("x", C.c_void_p), ("r_attn", C.c_void_p), ("sa_gate", C.c_void_p),
+                ("ff_scale", C.c_void_p), ("ff_gate", C.c_void_p), ("t_vec", C.c_void_p),
+                ("w_r", C.c_void_p), ("w1", C.c_void_p), ("w3", C.c_void_p), ("w2", C.c_void_p),
+                ("sw1", C.c_void_p), ("sw3", C.c_void_p), ("sw2", C.c_void_p), ("h", C.c_void_p),
+                ("x_norm", C.c_void_p), ("x_mod", C.c_void_p), ("out", C.c_void_p),
+                ("route", RouteOut)]
 
 
 class FfnDesc(C.Structure):
@@ -83,6 +93,9 @@ def _load():
         "nimg_copy_async": ([P, P, SZ, P], C.c_int),
         "nimg_stream_write_u32": ([P, C.c_uint32, P], C.c_int),
         "nimg_stream_wait_geq_u32": ([P, C.c_uint32, P], C.c_int),
+        "nimg_moe_block_workspace_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
+        "nimg_moe_block_forward": ([C.POINTER(MoeDesc), C.POINTER(BlockPtrs), I32, P, SZ, P],
+                                   C.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

@@ -11,6 +11,8 @@
 #include <mutex>
 #include <string>
 
+#include <cuda_bf16.h>
+
 #include "../../include/nimg_moe.h"
 #include "nimg_internal.h"
 
@@ -506,9 +508,9 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   return NIMG_OK;
 }
 
-int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, size_t ws_bytes,
-                     void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+// moe.py:138-164; with resid_h, the combine writes h + th_ff * moe (backbone.py:606)
+static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, size_t ws_bytes,
+                            cudaStream_t st, const void* resid_h, const double* th_ff) {
   NIMG_TRY(check_moe_desc(d));
   if (!p) return fail(NIMG_ERR_SHAPE, "null pointers");
   size_t need = 0;
@@ -542,9 +544,60 @@ int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, s
   mark(4, st);
   CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys, p->route.gates,
                           p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,
-                          (int)d->E, st));
+                          (int)d->E, st, resid_h, th_ff, (int)d->S));
   mark(5, st);
   return NIMG_OK;
+}
+
+int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, size_t ws_bytes,
+                     void* stream) {
+  return moe_forward_impl(d, p, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+static size_t block_extra_bytes(const nimg_moe_desc* d) {
+  return 2 * align_up((size_t)d->B * d->d * 8) + align_up((size_t)d->B * d->d * 4);
+}
+
+int nimg_moe_block_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
+  NIMG_TRY(nimg_moe_workspace_bytes(d, bytes));
+  *bytes += block_extra_bytes(d);
+  return NIMG_OK;
+}
+
+int nimg_moe_block_forward(const nimg_moe_desc* d, const nimg_block_ptrs* b, int32_t layer, void* ws,
+                           size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  NIMG_TRY(check_moe_desc(d));
+  if (!b || !b->x || !b->r_attn || !b->sa_gate || !b->ff_scale || !b->ff_gate || !b->t_vec ||
+      !b->h || !b->x_norm || !b->x_mod || !b->out)
+    return fail(NIMG_ERR_SHAPE, "null block pointer");
+  if (layer < 0) return fail(NIMG_ERR_CONFIG, "layer must be >= 0");
+  size_t need = 0;
+  NIMG_TRY(nimg_moe_block_workspace_bytes(d, &need));
+  if (!ws || ws_bytes < need) return fail(NIMG_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, need);
+  const size_t bd = (size_t)d->B * d->d;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  double* th_sa = reinterpret_cast<double*>(w);          w += align_up(bd * 8);
+  double* th_ff = reinterpret_cast<double*>(w);          w += align_up(bd * 8);
+  float* onep = reinterpret_cast<float*>(w);             w += align_up(bd * 4);
+  const bool bf = d->act_dtype == NIMG_BF16;
+  // as_tensor(1/sqrt(layer+1), like=rmsnorm output): the scalar is stored in the
+  // operand dtype (tensor.py:183-187)
+  float scale_t = (float)(1.0 / std::sqrt((double)layer + 1.0));
+  if (bf) scale_t = __bfloat162float(__float2bfloat16_rn(scale_t));
+  CUDA_TRY(launch_block_modvec(b->sa_gate, b->ff_scale, b->ff_gate, th_sa, th_ff, onep, (int64_t)bd, st));
+  CUDA_TRY(launch_block_prologue(bf, b->x, b->r_attn, th_sa, onep, b->h, b->x_norm, b->x_mod,
+                                 d->B * d->S, (int)d->S, (int)d->d, scale_t, st));
+  nimg_moe_ptrs p;
+  p.x_norm = b->x_norm;
+  p.x_mod = b->x_mod;
+  p.t_emb = b->t_vec;
+  p.w_r = b->w_r;
+  p.w1 = b->w1; p.w3 = b->w3; p.w2 = b->w2;
+  p.sw1 = b->sw1; p.sw3 = b->sw3; p.sw2 = b->sw2;
+  p.out = b->out;
+  p.route = b->route;
+  return moe_forward_impl(d, &p, w, ws_bytes - (size_t)(w - static_cast<uint8_t*>(ws)), st, b->h, th_ff);
 }
 
 int nimg_profile_events(void* const* events, int32_t n) {

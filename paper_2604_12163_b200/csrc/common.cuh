@@ -240,4 +240,32 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);   // M
 }
 
+// ---------------------------------------------------------------- numpy sum
+// Exact restatement of numpy's pairwise summation (float add.reduce over a
+// contiguous axis, e.g. `e.sum(axis=-1)` / `mean` in tensor.py:471, :527):
+// < 8 terms sequential from 0.0; <= 128 terms with eight stride-8
+// accumulators folded ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential
+// tail; larger n split at n/2 rounded down to a multiple of 8.
+static __device__ __noinline__ double np_pairwise_sum(const double* a, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; ++i) res += a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+      r0 += a[i + 0]; r1 += a[i + 1]; r2 += a[i + 2]; r3 += a[i + 3];
+      r4 += a[i + 4]; r5 += a[i + 5]; r6 += a[i + 6]; r7 += a[i + 7];
+    }
+    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
 }  // namespace nimg

@@ -20,33 +20,6 @@
 
 namespace nimg {
 
-// ------------------------------------------------------------------ numpy sum
-// Exact restatement of numpy's pairwise summation (used by `e.sum(axis=-1)`
-// in tensor.py:471): < 8 terms sequential from 0.0; <= 128 terms with eight
-// stride-8 accumulators folded as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a
-// sequential tail; larger n split at n/2 rounded down to a multiple of 8.
-__device__ double np_pairwise_sum(const double* a, int n) {
-  if (n < 8) {
-    double res = 0.0;
-    for (int i = 0; i < n; ++i) res += a[i];
-    return res;
-  }
-  if (n <= 128) {
-    double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8) {
-      r0 += a[i + 0]; r1 += a[i + 1]; r2 += a[i + 2]; r3 += a[i + 3];
-      r4 += a[i + 4]; r5 += a[i + 5]; r6 += a[i + 6]; r7 += a[i + 7];
-    }
-    double res = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
-    for (; i < n; ++i) res += a[i];
-    return res;
-  }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
-}
-
 // ------------------------------------------------------------------ router prep
 // (a) wd[k, e] = f64(W_r[k, e]) for the x half (k < d), E padded to EP;
 // (b) tb[b, e] = sum_k t_emb[b, k] * W_r[d + k, e] in f64 (the t half of the
@@ -812,11 +785,14 @@ template <typename T, int VEC> struct VecIO {
   NIMG_DEV float at(int i) const { return to_f32(reinterpret_cast<const T*>(v)[i]); }
 };
 
-template <typename TY, typename TO, int VEC, typename ACC, int UNR>
+// RESID (the backbone's MoE branch, backbone.py:606): instead of the layer
+// output, write h + tanh(ff_gate) * round(layer output) (f64, rounded).
+template <typename TY, typename TO, int VEC, typename ACC, int UNR, bool RESID>
 __global__ void __launch_bounds__(CB_WARPS * 32)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
-               TO* __restrict__ out, int64_t T, int d, int E) {
+               TO* __restrict__ out, int64_t T, int d, int E, const TO* __restrict__ hres,
+               const double* __restrict__ thg, int S) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* rows = reinterpret_cast<int32_t*>(sm) + (size_t)warp * E;
@@ -868,6 +844,14 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
       for (int v = 0; v < VEC; ++v) {
         const float comb = (float)acc[u][v];
         res[v] = from_f32<TO>((float)((ACC)comb + (ACC)sh[u].at(v)));
+      }
+      if constexpr (RESID) {
+        const int64_t base = t * d + c0 + u * STEP;
+        const double* tg = thg + (t / S) * d + c0 + u * STEP;
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          res[v] = from_f32<TO>((float)__dadd_rn((double)to_f32(hres[base + v]),
+                                                 __dmul_rn(tg[v], (double)to_f32(res[v]))));
       }
       TO* o = out + t * d + c0 + u * STEP;
       if constexpr (VEC * sizeof(TO) % 16 == 0) {
@@ -992,32 +976,38 @@ cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t
   return cudaGetLastError();
 }
 
-template <typename TY, typename TO>
+template <typename TY, typename TO, bool RESID>
 static void combine_dispatch(const void* yr, const void* ys, const float* gates,
                              const int32_t* rows, const int32_t* cnt, void* out, int64_t T, int d,
-                             int E, cudaStream_t s) {
+                             int E, const void* hres, const double* thg, int S, cudaStream_t s) {
   const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
   const size_t smem = (size_t)CB_WARPS * E * 8;
   using ACC = typename std::conditional<sizeof(TO) == 2, float, double>::type;
-  if (d % 512 == 0)
-    combine_kernel<TY, TO, 8, ACC, 2><<<grid, CB_WARPS * 32, smem, s>>>(
-        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
-  else if (d % 8 == 0)
-    combine_kernel<TY, TO, 8, ACC, 1><<<grid, CB_WARPS * 32, smem, s>>>(
-        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
-  else
-    combine_kernel<TY, TO, 1, ACC, 1><<<grid, CB_WARPS * 32, smem, s>>>(
-        (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E);
+#define NIMG_COMBINE(V, U)                                                                      \
+  combine_kernel<TY, TO, V, ACC, U, RESID><<<grid, CB_WARPS * 32, smem, s>>>(                  \
+      (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E, (const TO*)hres, thg, S)
+  if (d % 512 == 0) NIMG_COMBINE(8, 2);
+  else if (d % 8 == 0) NIMG_COMBINE(8, 1);
+  else NIMG_COMBINE(1, 1);
+#undef NIMG_COMBINE
 }
 
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
-                           void* out, int64_t T, int d, int E, cudaStream_t s) {
+                           void* out, int64_t T, int d, int E, cudaStream_t s, const void* hres,
+                           const double* th_gate, int S) {
   if (T <= 0) return cudaSuccess;
-  if (y_bf16 && out_bf16) combine_dispatch<bf16, bf16>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
-  else if (y_bf16) combine_dispatch<bf16, float>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
-  else if (out_bf16) combine_dispatch<float, bf16>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
-  else combine_dispatch<float, float>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, s);
+  const bool r = hres != nullptr;
+#define NIMG_CD(TY, TO)                                                                              \
+  (r ? combine_dispatch<TY, TO, true>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, \
+                                      hres, th_gate, S, s)                                          \
+     : combine_dispatch<TY, TO, false>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, \
+                                       hres, th_gate, S, s))
+  if (y_bf16 && out_bf16) NIMG_CD(bf16, bf16);
+  else if (y_bf16) NIMG_CD(bf16, float);
+  else if (out_bf16) NIMG_CD(float, bf16);
+  else NIMG_CD(float, float);
+#undef NIMG_CD
   return cudaGetLastError();
 }
 

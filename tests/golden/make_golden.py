@@ -22,7 +22,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle.workloads import digest, make_layer_inputs, make_router_inputs  # noqa: E402
+from oracle.workloads import (digest, make_block_inputs, make_layer_inputs,  # noqa: E402
+                              make_router_inputs)
 from tests.refimport import load_reference  # noqa: E402
 
 # name -> (kind, params). kind "moe" = full layer, "route" = router only.
@@ -44,10 +45,17 @@ CASES = {
     # 1024px column length, C=2 (cap 128), one sample
     "s4096_route_bf16": ("route", dict(seed=6, B=1, S=4096, d=2048, E=64, C=2.0, mode="bf16",
                                        layer=17)),
+    # the backbone's MoE branch around the layer (backbone.py:583-606), fp32
+    "block_fp32": ("block", dict(seed=7, B=2, S=128, d=256, E=8, h=112, C=2.0, mode="fp32",
+                                 layer=5)),
+    "block_ragged_fp32": ("block", dict(seed=8, B=2, S=40, d=24, E=4, h=20, C=1.5, mode="fp32",
+                                        layer=3)),
 }
 
 
 def inputs_for(kind, p):
+    if kind == "block":
+        return make_block_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"], mode=p["mode"])
     if kind == "moe":
         return make_layer_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"],
                                  layer=p.get("layer", 3), mode=p["mode"])
@@ -55,7 +63,36 @@ def inputs_for(kind, p):
                               layer=p.get("layer", 3), mode=p["mode"])
 
 
+def run_reference_block(ref, p, inp):
+    """backbone.py:583-606 composed from the reference's own functions."""
+    import math
+    import importlib
+    bb = importlib.import_module("nimg_ref.backbone")
+    nt = ref.tensor
+    T, f32 = nt.Tensor, np.float32
+    B, S, d = inp["x"].shape
+    cfg = ref.router.RouterConfig(d_model=d, n_experts=p["E"], capacity_factor=p["C"])
+    bank = ref.moe.ExpertBank(*(T(inp[k], dtype=f32) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")))
+    x, r_attn = T(inp["x"], dtype=f32), T(inp["r_attn"], dtype=f32)
+    sa_gate, ff_scale, ff_gate = (T(inp[k], dtype=f32) for k in ("sa_gate", "ff_scale", "ff_gate"))
+    t_vec, w_r = T(inp["t_vec"], dtype=f32), T(inp["w_r"], dtype=f32)
+    with nt.no_grad():
+        h = bb.fused_gated_residual(x, sa_gate, r_attn)
+        scale = 1.0 / math.sqrt(p["layer"] + 1)
+        x_norm = nt.mul(nt.rmsnorm(h), scale)
+        x_mod = nt.mul(x_norm, nt.add(nt.broadcast_to(nt.reshape(ff_scale, (B, 1, -1)), h.shape), 1.0))
+        moe_out, decisions, routing = ref.moe.moe_forward(h, x_norm, x_mod, t_vec, cfg, bank, w_r,
+                                                          return_routing=True)
+        out = bb.fused_gated_residual(h, ff_gate, moe_out)
+    return {"out": out.data, "h": h.data, "x_norm": x_norm.data, "x_mod": x_mod.data,
+            "moe": moe_out.data, "logits": routing["logits"].data,
+            "token_flat": np.asarray(routing["token_flat"], dtype=np.int64),
+            "gates": routing["gates"].data, "capacity": np.int64(routing["capacity"])}
+
+
 def run_reference(ref, kind, p, inp):
+    if kind == "block":
+        return run_reference_block(ref, p, inp)
     T = ref.tensor.Tensor
     f32 = np.float32
     cfg = ref.router.RouterConfig(d_model=p["d"], n_experts=p["E"], capacity_factor=p["C"],

@@ -29,6 +29,6 @@ def load_reference():
     sys.modules["nimg_ref"] = mod
     spec.loader.exec_module(mod)
     import importlib as il
-    for sub in ("tensor", "router", "moe"):
+    for sub in ("tensor", "router", "moe", "backbone"):
         setattr(mod, sub, il.import_module(f"nimg_ref.{sub}"))
     return mod

@@ -361,3 +361,68 @@ def test_fused_gather_variants_bitwise_equal():
     np.testing.assert_array_equal(outs["pair"], outs["base"])
     # the 1-CTA kernel accumulates in a different tile order; allow rounding-level differences
     assert rel_fro(outs["g4"], outs["base"]) < 1e-2
+
+
+@pytest.mark.parametrize("name", G.names("block"))
+def test_block_vs_reference_golden(name):
+    """MoE branch of MoEDiT.forward (backbone.py:583-606), fp32: h, x_norm,
+    x_mod and the routing bit-exact with the reference; the updated residual
+    stream within the fp32 bar."""
+    from paper_2604_12163_b200 import block as BK
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    kind, p, inp, exp = G.case(name)
+    T = lambda k: torch.from_numpy(inp[k]).cuda()
+    cfg = R.RouterConfig(d_model=p["d"], n_experts=p["E"], capacity_factor=p["C"])
+    bank = M.ExpertBank(*(T(k) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")))
+    out, dec, routing, mid = BK.moe_block_forward(
+        T("x"), T("sa_gate"), T("r_attn"), T("ff_scale"), T("ff_gate"), T("t_vec"), p["layer"], cfg,
+        bank, T("w_r"), return_routing=True, return_intermediates=True)
+    for k in ("h", "x_norm", "x_mod"):
+        np.testing.assert_array_equal(np_of(mid[k]), exp[k], err_msg=k)
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), exp["token_flat"])
+    np.testing.assert_array_equal(np_of(routing["gates"]), exp["gates"])
+    np.testing.assert_array_equal(np_of(routing["logits"]), exp["logits"])
+    err = rel_fro(np_of(out), exp["out"])
+    assert err <= TOL_FP32, f"{name}: rel-err {err:.3e}"
+
+
+def test_block_full_width_bf16():
+    """bf16 block at full width (d=2048, E=64, h=1344), 512px x 2: the fused
+    prologue equals the same chain in numpy with bf16 rounding; routing of
+    the produced x_norm is bit-exact with the oracle router; the residual
+    output matches h + tanh(ff_gate) * oracle layer(x_norm, x_mod)."""
+    from oracle.workloads import bf16_round, make_block_inputs
+    from paper_2604_12163_b200 import block as BK
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    B, S, d, E, h, C, layer = 2, 1024, 2048, 64, 1344, 4.0, 17
+    inp = make_block_inputs(71, B, S, d, E, h, mode="bf16")
+    bf = torch.bfloat16
+    T = lambda k, dt=None: torch.from_numpy(inp[k]).cuda().to(dt or torch.float32)
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    bank = M.ExpertBank(*(T(k, bf) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")))
+    out, dec, routing, mid = BK.moe_block_forward(
+        T("x", bf), T("sa_gate"), T("r_attn", bf), T("ff_scale"), T("ff_gate"), T("t_vec"), layer,
+        cfg, bank, T("w_r"), return_routing=True, return_intermediates=True)
+    # prologue chain in numpy (f64 ops, bf16 storage rounding)
+    f64 = np.float64
+    hh = bf16_round((inp["x"].astype(f64) + np.tanh(inp["sa_gate"].astype(f64))[:, None, :]
+                     * inp["r_attn"].astype(f64)).astype(np.float32))
+    ms = (hh.astype(f64) ** 2).mean(axis=-1, keepdims=True) + 1e-6
+    xn0 = bf16_round((hh.astype(f64) / np.sqrt(ms)).astype(np.float32))
+    sc = float(bf16_round(np.array([1.0 / np.sqrt(layer + 1)], np.float32))[0])
+    xn = bf16_round((xn0.astype(f64) * sc).astype(np.float32))
+    onep = (inp["ff_scale"].astype(f64) + 1.0).astype(np.float32).astype(f64)[:, None, :]
+    xm = bf16_round((xn.astype(f64) * onep).astype(np.float32))
+    np.testing.assert_array_equal(np_of(mid["h"]), hh)
+    np.testing.assert_array_equal(np_of(mid["x_norm"]), xn)
+    np.testing.assert_array_equal(np_of(mid["x_mod"]), xm)
+    r = O.route_full(xn, inp["t_vec"], inp["w_r"], n_experts=E, capacity_factor=C)
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), r["token_flat"])
+    w = {k: inp[k] for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")}
+    moe = O.moe_forward(xn[:1], xm[:1], inp["t_vec"][:1], inp["w_r"], w["w1"], w["w3"], w["w2"],
+                        w["sw1"], w["sw3"], w["sw2"], capacity_factor=C)
+    want = hh[:1].astype(f64) + np.tanh(inp["ff_gate"][:1].astype(f64))[:, None, :] * moe
+    err = rel_fro(np_of(out[:1]), want)
+    assert err <= TOL_BF16, f"block bf16 rel-err {err:.3e}"

@@ -17,7 +17,22 @@ from tests import golden_cases as G
 from tests.refimport import load_reference, reference_available
 
 
-@pytest.mark.parametrize("name", G.names())
+@pytest.mark.parametrize("name", G.names("block"))
+def test_oracle_block_matches_reference_golden(name):
+    """backbone.py:583-606 (MoE branch around the layer) composed from the
+    reference's own functions vs the oracle restatement: bit-exact."""
+    kind, p, inp, exp = G.case(name)
+    res, r = O.moe_block_forward(inp["x"], inp["sa_gate"], inp["r_attn"], inp["ff_scale"],
+                                 inp["ff_gate"], inp["t_vec"], p["layer"], inp["w_r"], inp["w1"],
+                                 inp["w3"], inp["w2"], inp["sw1"], inp["sw3"], inp["sw2"],
+                                 capacity_factor=p["C"], return_routing=True)
+    for k in ("h", "x_norm", "x_mod", "moe", "out"):
+        np.testing.assert_array_equal(res[k], exp[k], err_msg=k)
+    np.testing.assert_array_equal(r["token_flat"], exp["token_flat"])
+    np.testing.assert_array_equal(r["gates"], exp["gates"])
+
+
+@pytest.mark.parametrize("name", G.names("moe") + G.names("route"))
 def test_oracle_matches_reference_golden(name):
     kind, p, inp, exp = G.case(name)
     kw = dict(capacity_factor=p["C"], gate_scale=p.get("gate_scale", 1.0))
