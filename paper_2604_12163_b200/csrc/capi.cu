@@ -510,7 +510,7 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
 
 // moe.py:138-164; with resid_h, the combine writes h + th_ff * moe (backbone.py:606)
 static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, size_t ws_bytes,
-                            cudaStream_t st, const void* resid_h, const double* th_ff) {
+                            cudaStream_t st, const void* resid_h, const void* th_ff) {
   NIMG_TRY(check_moe_desc(d));
   if (!p) return fail(NIMG_ERR_SHAPE, "null pointers");
   size_t need = 0;
@@ -555,7 +555,7 @@ int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, s
 }
 
 static size_t block_extra_bytes(const nimg_moe_desc* d) {
-  return 2 * align_up((size_t)d->B * d->d * 8) + align_up((size_t)d->B * d->d * 4);
+  return 2 * align_up((size_t)d->B * d->d * 8) + 3 * align_up((size_t)d->B * d->d * 4);
 }
 
 int nimg_moe_block_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
@@ -580,14 +580,17 @@ int nimg_moe_block_forward(const nimg_moe_desc* d, const nimg_block_ptrs* b, int
   double* th_sa = reinterpret_cast<double*>(w);          w += align_up(bd * 8);
   double* th_ff = reinterpret_cast<double*>(w);          w += align_up(bd * 8);
   float* onep = reinterpret_cast<float*>(w);             w += align_up(bd * 4);
+  float* th_sa_f = reinterpret_cast<float*>(w);          w += align_up(bd * 4);
+  float* th_ff_f = reinterpret_cast<float*>(w);          w += align_up(bd * 4);
   const bool bf = d->act_dtype == NIMG_BF16;
   // as_tensor(1/sqrt(layer+1), like=rmsnorm output): the scalar is stored in the
   // operand dtype (tensor.py:183-187)
   float scale_t = (float)(1.0 / std::sqrt((double)layer + 1.0));
   if (bf) scale_t = __bfloat162float(__float2bfloat16_rn(scale_t));
-  CUDA_TRY(launch_block_modvec(b->sa_gate, b->ff_scale, b->ff_gate, th_sa, th_ff, onep, (int64_t)bd, st));
-  CUDA_TRY(launch_block_prologue(bf, b->x, b->r_attn, th_sa, onep, b->h, b->x_norm, b->x_mod,
-                                 d->B * d->S, (int)d->S, (int)d->d, scale_t, st));
+  CUDA_TRY(launch_block_modvec(b->sa_gate, b->ff_scale, b->ff_gate, th_sa, th_ff, onep, th_sa_f,
+                               th_ff_f, (int64_t)bd, st));
+  CUDA_TRY(launch_block_prologue(bf, b->x, b->r_attn, th_sa, th_sa_f, onep, b->h, b->x_norm,
+                                 b->x_mod, d->B * d->S, (int)d->S, (int)d->d, scale_t, st));
   nimg_moe_ptrs p;
   p.x_norm = b->x_norm;
   p.x_mod = b->x_mod;
@@ -597,7 +600,8 @@ int nimg_moe_block_forward(const nimg_moe_desc* d, const nimg_block_ptrs* b, int
   p.sw1 = b->sw1; p.sw3 = b->sw3; p.sw2 = b->sw2;
   p.out = b->out;
   p.route = b->route;
-  return moe_forward_impl(d, &p, w, ws_bytes - (size_t)(w - static_cast<uint8_t*>(ws)), st, b->h, th_ff);
+  return moe_forward_impl(d, &p, w, ws_bytes - (size_t)(w - static_cast<uint8_t*>(ws)), st, b->h,
+                          bf ? (const void*)th_ff_f : (const void*)th_ff);
 }
 
 int nimg_profile_events(void* const* events, int32_t n) {

@@ -91,17 +91,18 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
 cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
                                int64_t n_idx, void* dst, cudaStream_t s);
 // out[t] = fp32(fp32(sum_k fp32(Y[rows[k][t]] * gate)) + shared[t]) -- see combine kernel.
-// hres != null: out[t] = h[t] + th_gate[b] * (that) instead (backbone.py:606).
+// hres != null: out[t] = h[t] + th_gate[b] * (that) instead (backbone.py:606);
+// th_gate is double* for fp32 output (f64 chain), float* for bf16 output.
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
                            void* out, int64_t T, int d, int E, cudaStream_t s,
-                           const void* hres = nullptr, const double* th_gate = nullptr, int S = 1);
+                           const void* hres = nullptr, const void* th_gate = nullptr, int S = 1);
 // backbone MoE branch prologue (block_kernels.cu)
 cudaError_t launch_block_modvec(const float* sa_gate, const float* ff_scale, const float* ff_gate,
-                                double* th_sa, double* th_ff, float* onep, int64_t n,
-                                cudaStream_t s);
+                                double* th_sa, double* th_ff, float* onep, float* th_sa_f,
+                                float* th_ff_f, int64_t n, cudaStream_t s);
 cudaError_t launch_block_prologue(bool bf, const void* x, const void* r_attn, const double* th_sa,
-                                  const float* onep, void* h, void* xn, void* xm, int64_t T, int S,
-                                  int d, float scale_t, cudaStream_t s);
+                                  const float* th_sa_f, const float* onep, void* h, void* xn,
+                                  void* xm, int64_t T, int S, int d, float scale_t, cudaStream_t s);
 
 }  // namespace nimg

@@ -792,7 +792,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
                TO* __restrict__ out, int64_t T, int d, int E, const TO* __restrict__ hres,
-               const double* __restrict__ thg, int S) {
+               const ACC* __restrict__ thg, int S) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* rows = reinterpret_cast<int32_t*>(sm) + (size_t)warp * E;
@@ -847,11 +847,17 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
       }
       if constexpr (RESID) {
         const int64_t base = t * d + c0 + u * STEP;
-        const double* tg = thg + (t / S) * d + c0 + u * STEP;
+        const ACC* tg = thg + (t / S) * d + c0 + u * STEP;
+        VecIO<TO, VEC> hv;
+        hv.load(hres + base);
 #pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          res[v] = from_f32<TO>((float)__dadd_rn((double)to_f32(hres[base + v]),
-                                                 __dmul_rn(tg[v], (double)to_f32(res[v]))));
+        for (int v = 0; v < VEC; ++v) {
+          if constexpr (sizeof(ACC) == 8)   // reference chain: product and sum rounded apart
+            res[v] = from_f32<TO>((float)__dadd_rn((double)hv.at(v),
+                                                   __dmul_rn(__ldg(tg + v), (double)to_f32(res[v]))));
+          else
+            res[v] = from_f32<TO>(__fadd_rn(hv.at(v), __fmul_rn(__ldg(tg + v), to_f32(res[v]))));
+        }
       }
       TO* o = out + t * d + c0 + u * STEP;
       if constexpr (VEC * sizeof(TO) % 16 == 0) {
@@ -979,13 +985,14 @@ cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t
 template <typename TY, typename TO, bool RESID>
 static void combine_dispatch(const void* yr, const void* ys, const float* gates,
                              const int32_t* rows, const int32_t* cnt, void* out, int64_t T, int d,
-                             int E, const void* hres, const double* thg, int S, cudaStream_t s) {
+                             int E, const void* hres, const void* thg, int S, cudaStream_t s) {
   const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
   const size_t smem = (size_t)CB_WARPS * E * 8;
   using ACC = typename std::conditional<sizeof(TO) == 2, float, double>::type;
 #define NIMG_COMBINE(V, U)                                                                      \
   combine_kernel<TY, TO, V, ACC, U, RESID><<<grid, CB_WARPS * 32, smem, s>>>(                  \
-      (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E, (const TO*)hres, thg, S)
+      (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E, (const TO*)hres,   \
+      (const ACC*)thg, S)
   if (d % 512 == 0) NIMG_COMBINE(8, 2);
   else if (d % 8 == 0) NIMG_COMBINE(8, 1);
   else NIMG_COMBINE(1, 1);
@@ -995,7 +1002,7 @@ static void combine_dispatch(const void* yr, const void* ys, const float* gates,
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
                            void* out, int64_t T, int d, int E, cudaStream_t s, const void* hres,
-                           const double* th_gate, int S) {
+                           const void* th_gate, int S) {
   if (T <= 0) return cudaSuccess;
   const bool r = hres != nullptr;
 #define NIMG_CD(TY, TO)                                                                              \
