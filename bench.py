@@ -178,8 +178,8 @@ def run_reference_arm(args, c):
     sample = f"1 sample (S={c['S']} tokens) of {c['name']} per step, fp32 oracle port (f64 compute)"
     line = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "impl": "reference",
+            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": workload_name(c), "l2": "n/a (CPU)"},
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
                              "sample": sample},
