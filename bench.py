@@ -9,8 +9,10 @@ router.py:91-92), bf16 activations/weights, fp32 router. A step = one full
 layer forward (router -> select -> gates -> gather -> grouped SwiGLU GEMMs ->
 combine + shared expert). Synthetic seeded inputs, random-init weights.
 
-N>1 (torchrun): expert parallel over NCCL (see paper_2604_12163_b200/ep.py),
-BASELINE configs[3] shape: S=4096, global batch 32, C=2, 64/N experts per GPU.
+N>1 (torchrun): expert parallel (paper_2604_12163_b200/ep.py), 64/N experts per
+GPU. `value` = the N=1 workload with 16 samples per GPU (weak scaling, so
+value(N)/(N*value(1)) is the EP efficiency); `cfg4_strong` = BASELINE configs[3]
+(S=4096, global batch 32, C=2) split over the N GPUs, with its 1-GPU time.
 
 Prints ONE JSON line on rank 0.
 """
@@ -178,7 +180,7 @@ def run_reference_arm(args, c):
     sample = f"1 sample (S={c['S']} tokens) of {c['name']} per step, fp32 oracle port (f64 compute)"
     line = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong" if args.gpus > 1 else "weak",
+            "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": workload_name(c), "l2": "n/a (CPU)"},
             "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
@@ -364,55 +366,14 @@ def run_e2e(args, c, inp, cfg, bank):
 
 
 # ----------------------------------------------------------------- ours, N GPUs (EP)
-def run_ep(args, c, peaks, peak_kind):
-    """Expert parallel over NCCL (torchrun, one rank per GPU): global batch
-    c["B"] split over ranks, E/R experts per rank (strong scaling)."""
+def _ep_setup(c, world, rank, dev):
+    """This rank's samples (B_l = c["B"] / world) and expert shard; shared
+    expert and router replicated (seeded)."""
     import torch
-    import torch.distributed as dist
     from paper_2604_12163_b200 import moe as M
     from paper_2604_12163_b200 import router as R
-    from paper_2604_12163_b200.ep import EPContext, ep_moe_forward
-
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    # keep stdout to the single JSON line: NCCL / torch init chatter -> stderr
-    sys.stdout.flush()
-    real_stdout = os.dup(1)
-    os.dup2(2, 1)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    B, S, d, h, E = c["B"], c["S"], c["d"], c["h"], c["E"]
-    if B % world or E % world:
-        raise SystemExit(f"B={B} and E={E} must be divisible by {world}")
+    B, d, h, E = c["B"], c["d"], c["h"], c["E"]
     bl, El = B // world, E // world
-    wc = work_counts(c)
-
-    # same-config single-GPU number, measured here on rank 0 (informational;
-    # the driver computes scaling from the per-N `value`s)
-    same1 = None
-    if rank == 0 and not args.no_same_config_1gpu:
-        inp = make_inputs(c, dev)
-        cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=c["C"])
-        plan = M.MoEPlan(cfg, M.ExpertBank(inp["w1"], inp["w3"], inp["w2"], inp["sw1"],
-                                           inp["sw3"], inp["sw2"]), B, S, torch.bfloat16)
-        f = lambda: plan.forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"])
-        for _ in range(3):
-            f()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(max(3, args.steps // 2)):
-            f()
-        e1.record()
-        torch.cuda.synchronize()
-        ms1 = e0.elapsed_time(e1) / max(3, args.steps // 2)
-        same1 = {"value": wc["T"] / (ms1 * 1e-3), "ms_per_step": ms1, "n_gpus": 1}
-        del plan, inp
-        torch.cuda.empty_cache()
-    dist.barrier()
-
-    # this rank's samples and expert shard (seeded per rank; shared + router replicated)
     cl = dict(c, B=bl, seed=c["seed"] * 1000 + rank)
     inp = make_inputs(cl, dev)
     g = torch.Generator(device=dev).manual_seed(c["seed"])
@@ -423,80 +384,162 @@ def run_ep(args, c, peaks, peak_kind):
                         inp["w2"][:El].contiguous(), *sw)
     del inp["w1"], inp["w3"], inp["w2"]
     cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=c["C"])
-    ctx = EPContext(overlap=not args.no_overlap, transport=args.ep_transport)
-    step = lambda: ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx)
+    return inp, bank, cfg, w_r
 
+
+def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
+    """Device time per step of the EP layer on global config c (max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_12163_b200.ep import ep_moe_forward
+    inp, bank, cfg, w_r = _ep_setup(c, world, rank, dev)
+    step = lambda: ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     dist.barrier()
-    clk = ClockSampler(local) if rank == 0 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    dist.barrier()
     e0.record()
     for _ in range(args.steps):
         step()
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
-    clocks = clk.stop() if clk else None
     t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    value = wc["T"] / (ms * 1e-3)
+    out = {"ms": float(t.item())}
+    if timeline:
+        tl = []
+        ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx, timeline=tl)
+        torch.cuda.synchronize()
+        out["timeline"] = {n: round(tl[0][1].elapsed_time(e), 4) for n, e in tl}
+    if want_e2e:
+        # e2e through the public EP API with pinned host buffers per rank,
+        # uploads / layer / downloads overlapped across steps (pipeline.py)
+        from paper_2604_12163_b200.pipeline import HostPipeline
+        host = [inp[k].cpu().pin_memory() for k in ("x_norm", "x_mod", "t_emb")]
+        fn = lambda xn, xm, te: ep_moe_forward(xn, xm, te, cfg, bank, w_r, ctx)
+        pipe = HostPipeline(fn, host, inp["x_mod"].shape, inp["x_mod"].dtype, device=dev)
+        for _ in range(3):
+            pipe.step()
+        pipe.drain()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record()
+        pipe.h2d.wait_stream(torch.cuda.current_stream())
+        for _ in range(args.steps):
+            pipe.step()
+        pipe.drain()
+        e1.record()
+        torch.cuda.synchronize()
+        t2 = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+        dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        out["e2e_ms"] = float(t2.item())
+        out["h2d"] = pipe.bytes_in
+        out["d2h"] = pipe.bytes_out
+    del inp, bank
+    torch.cuda.empty_cache()
+    return out
 
-    # e2e through the public EP API with host buffers (per rank), max over ranks
-    host = {k: inp[k].cpu().pin_memory() for k in ("x_norm", "x_mod", "t_emb")}
-    out_h = torch.empty(inp["x_mod"].shape, dtype=torch.bfloat16).pin_memory()
 
-    def e2e_step():
-        dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
-        y = ep_moe_forward(dv["x_norm"], dv["x_mod"], dv["t_emb"], cfg, bank, w_r, ctx)
-        out_h.copy_(y, non_blocking=True)
-
+def _one_gpu_ms(args, c, dev):
+    import torch
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    inp = make_inputs(c, dev)
+    cfg = R.RouterConfig(d_model=c["d"], n_experts=c["E"], capacity_factor=c["C"])
+    plan = M.MoEPlan(cfg, M.ExpertBank(inp["w1"], inp["w3"], inp["w2"], inp["sw1"], inp["sw3"],
+                                       inp["sw2"]), c["B"], c["S"], torch.bfloat16)
+    f = lambda: plan.forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"])
     for _ in range(3):
-        e2e_step()
+        f()
     torch.cuda.synchronize()
-    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = max(3, args.steps // 2)
     e0.record()
-    for _ in range(args.steps):
-        e2e_step()
+    for _ in range(n):
+        f()
     e1.record()
     torch.cuda.synchronize()
-    t2 = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
-    dist.all_reduce(t2, op=dist.ReduceOp.MAX)
-    ms2 = float(t2.item())
-    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    del plan, inp
+    torch.cuda.empty_cache()
+    return e0.elapsed_time(e1) / n
 
-    # per-stage timeline of one more step (rank 0's compute stream)
-    tl = []
-    ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx, timeline=tl)
-    torch.cuda.synchronize()
-    timeline = {n: round(tl[0][1].elapsed_time(e), 4) for n, e in tl}
+
+def run_ep(args, c, peaks, peak_kind):
+    """Expert parallel (torchrun, one rank per GPU, E/N experts per rank).
+
+    Main line (`value`): the N=1 workload (cfg2 shape, 16 samples of S=1024
+    per GPU, C=4) with the batch grown with N -- weak scaling, so the driver's
+    value(N) / (N * value(1)) is the true EP efficiency against the N=1 line.
+    `cfg4_strong`: BASELINE configs[3] (1024px, global batch 32, C=2) split
+    over the N GPUs, with its own single-GPU time measured in the same run."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_12163_b200.ep import EPContext
+
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    # keep stdout to the single JSON line: NCCL / torch init chatter -> stderr
+    sys.stdout.flush()
+    real_stdout = os.dup(1)
+    os.dup2(2, 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    if CFG2["E"] % world:
+        raise SystemExit(f"E={CFG2['E']} must be divisible by {world}")
+    ctx = EPContext(overlap=not args.no_overlap, transport=args.ep_transport)
+
+    # ---- main: weak scaling of the N=1 workload
+    cw = dict(CFG2, B=CFG2["B"] * world)
+    wcw = work_counts(cw)
+    clk = ClockSampler(local) if rank == 0 else None
+    main = _ep_time(args, cw, world, rank, dev, ctx, want_e2e=True, timeline=True)
+    clocks = clk.stop() if clk else None
+    ms = main["ms"]
+    value = wcw["T"] / (ms * 1e-3)
+
+    # ---- cfg4 strong scaling (north star: >= 75% at 8 GPUs)
+    strong = None
+    if not args.no_strong and CFG4["B"] % world == 0:
+        ms1 = None
+        if rank == 0 and not args.no_same_config_1gpu:
+            ms1 = _one_gpu_ms(args, CFG4, dev)
+        dist.barrier()
+        st = _ep_time(args, CFG4, world, rank, dev, ctx, timeline=True)
+        wc4 = work_counts(CFG4)
+        strong = {"workload": workload_name(CFG4), "ms_per_step": st["ms"],
+                  "value": wc4["T"] / (st["ms"] * 1e-3), "unit": "tokens/s",
+                  "timeline_ms_rank0": st["timeline"]}
+        if ms1 is not None:
+            strong["same_config_1gpu"] = {"ms_per_step": ms1, "value": wc4["T"] / (ms1 * 1e-3)}
+            strong["efficiency"] = ms1 / (world * st["ms"])
 
     sys.stdout.flush()
     os.dup2(real_stdout, 1)
     if rank == 0:
-        a2a = wc["R"] // world * (world - 1) // world * d * 2  # bytes per rank per direction
+        d = cw["d"]
+        a2a = wcw["R"] // world * (world - 1) // world * d * 2
+        transport = ("NCCL all-to-all" if args.no_overlap else
+                     ("copy-engine NVLink exchange (CUDA IPC + stream flags)"
+                      if args.ep_transport == "ce" else "NCCL") + ", comm/compute overlap")
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded randn, random-init weights)",
-            "config": {"workload": workload_name(c), "capacity": wc["cap"], "tokens": wc["T"],
-                       "parallelism": f"ep{world} (experts {El}/GPU, samples {bl}/GPU), "
-                                      + ("NCCL all-to-all" if args.no_overlap else
-                                         ("copy-engine NVLink exchange (CUDA IPC + stream flags)"
-                                          if args.ep_transport == "ce" else "NCCL")
-                                         + ", comm/compute overlap"),
+            "config": {"workload": workload_name(cw) + f" ({CFG2['B']} samples per GPU)",
+                       "capacity": wcw["cap"], "tokens": wcw["T"],
+                       "parallelism": f"ep{world}: {CFG2['E'] // world} experts/GPU, "
+                                      f"{CFG2['B']} samples/GPU, {transport}",
                        "l2": "inputs larger than L2"},
             "a2a_bytes_per_rank_per_direction": a2a,
-            "same_config_1gpu": same1,
-            "timeline_ms_rank0": timeline,
-            "e2e": {"value": wc["T"] / (ms2 * 1e-3), "unit": "tokens/s",
-                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step":
-                    out_h.numel() * out_h.element_size() * world, "ms_per_step": ms2},
+            "timeline_ms_rank0": main["timeline"],
+            "cfg4_strong": strong,
+            "e2e": {"value": wcw["T"] / (main["e2e_ms"] * 1e-3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": main["h2d"] * world,
+                    "d2h_bytes_per_step": main["d2h"] * world, "ms_per_step": main["e2e_ms"]},
             "gpu_launches": (8 + 2 * (world - 1)) * args.steps,
             "clocks": clocks,
         }
@@ -519,12 +562,13 @@ def main():
     ap.add_argument("--ep-transport", default="ce", choices=["ce", "nccl"],
                     help="EP exchange: copy engines over NVLink (default) or NCCL")
     ap.add_argument("--no-same-config-1gpu", action="store_true")
+    ap.add_argument("--no-strong", action="store_true", help="EP: skip the cfg4 strong-scaling leg")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per GEMM1 launch, if captured")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    c = dict(CFG2 if (args.config or ("cfg2" if world == 1 else "cfg4")) == "cfg2" else CFG4)
+    c = dict(CFG2 if (args.config or "cfg2") == "cfg2" else CFG4)
     if args.batch:
         c["B"] = args.batch
     if args.impl == "reference":

@@ -16,6 +16,8 @@
 // Pipelines: STAGES-deep smem ring (full/empty mbarriers) and a 2-deep TMEM
 // accumulator ring (tmem_full/tmem_empty), so the epilogue of tile i overlaps
 // the MMAs of tile i+1.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "nimg_internal.h"
 
@@ -256,7 +258,8 @@ template <> struct PairCfg<1> {
   static constexpr int BN_OUT = 256, BN_MMA = 256, B_ROWS = 128, STAGES = 6;
 };
 template <int MODE> constexpr int pair_stage_bytes() { return kATileBytes + PairCfg<MODE>::B_ROWS * BK * 2; }
-template <int MODE> constexpr int pair_smem_bytes() { return PairCfg<MODE>::STAGES * pair_stage_bytes<MODE>() + 1024 + 256; }
+template <int MODE, int STAGES = PairCfg<MODE>::STAGES>
+constexpr int pair_smem_bytes() { return STAGES * pair_stage_bytes<MODE>() + 1024 + 256; }
 
 constexpr int PBM = 256;  // rows per pair tile
 
@@ -292,11 +295,10 @@ NIMG_DEV void decode_pair_tile(const GroupedParams& p, int t, TileInfo& ti) {
 // tiles the gather threads arrive without copying.
 constexpr int kGatherWarps = 2;
 
-template <int MODE, bool GATHER>
+template <int MODE, bool GATHER, int STAGES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (GATHER ? 32 * (kGatherWarps + 1) : 0), 1)
 grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constant__ GroupedParams p) {
   using C = PairCfg<MODE>;
-  constexpr int STAGES = C::STAGES;
   constexpr int SB = pair_stage_bytes<MODE>();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -500,19 +502,29 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
 int tc_bn_out(int mode) { return mode == 0 ? tc::Cfg<0>::BN_OUT : tc::Cfg<1>::BN_OUT; }
 int tc_pair_rows() { return tc::PBM; }
 
-template <int MODE, bool GATHER>
+template <int MODE, bool GATHER, int STAGES>
 static cudaError_t launch_pair(const TmapSet& tm, const GroupedParams& p, int grid, cudaStream_t stream) {
-  constexpr int smem = tc::pair_smem_bytes<MODE>();
+  constexpr int smem = tc::pair_smem_bytes<MODE, STAGES>();
   constexpr int threads = tc::kThreads + (GATHER ? 32 * (tc::kGatherWarps + 1) : 0);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100_pair<MODE, GATHER>,
+    cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tc::grouped_gemm_sm100_pair<MODE, GATHER><<<grid, threads, smem, stream>>>(tm, p);
+  tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES><<<grid, threads, smem, stream>>>(tm, p);
   return cudaGetLastError();
+}
+
+// Shallow-pipeline variant (4 stages, ~122-130 KB smem) leaves room on each
+// SM for a co-resident router CTA; NIMG_GEMM_STAGES=4 selects it globally.
+static int pair_stages() {
+  static const int st = [] {
+    const char* e = getenv("NIMG_GEMM_STAGES");
+    return (e && atoi(e) == 4) ? 4 : 6;
+  }();
+  return st;
 }
 
 cudaError_t launch_grouped_tc_pair(int mode, const TmapSet& tm, const GroupedParams& p, int num_sms,
@@ -521,8 +533,12 @@ cudaError_t launch_grouped_tc_pair(int mode, const TmapSet& tm, const GroupedPar
   const int clusters = p.total_tiles < num_sms / 2 ? p.total_tiles : num_sms / 2;
   const int grid = 2 * clusters;
   const bool gather = p.bank[0].a_idx != nullptr || p.bank[1].a_idx != nullptr;
-  if (mode == 0) return gather ? launch_pair<0, true>(tm, p, grid, stream) : launch_pair<0, false>(tm, p, grid, stream);
-  return launch_pair<1, false>(tm, p, grid, stream);
+  const bool shallow = pair_stages() == 4;
+  if (mode == 0) {
+    if (gather) return launch_pair<0, true, 6>(tm, p, grid, stream);
+    return shallow ? launch_pair<0, false, 4>(tm, p, grid, stream) : launch_pair<0, false, 6>(tm, p, grid, stream);
+  }
+  return shallow ? launch_pair<1, false, 4>(tm, p, grid, stream) : launch_pair<1, false, 6>(tm, p, grid, stream);
 }
 int tc_b_box(int mode) { return mode == 0 ? tc::Cfg<0>::B_BOX : tc::Cfg<1>::B_BOX; }
 

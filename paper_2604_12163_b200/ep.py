@@ -361,10 +361,27 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
         _lib.check(L.nimg_stream_write_u32(tp.flag(q, DISP, me), k, sh))
         xg.record_stream(st)
 
-    # shared expert first (needs no exchange; covers the dispatch copies)
+    # The rank's own chunk needs no exchange: its first half of experts runs
+    # right after the shared expert (together they cover the dispatch copies),
+    # its second half last (covers the final return copy).
+    El = plan.experts_per_rank
+    half = El // 2 if R > 1 else El
+    blk = plan.block_rows
+    own_x = xg[me * n:(me + 1) * n]
+
+    def own_part(e0, e1):
+        if e1 <= e0:
+            return
+        off = (np.arange(e0, e1 + 1, dtype=np.int64) - e0) * blk
+        stages.expert_ffn(own_x[e0 * blk:e1 * blk], off, np.arange(e0, e1, dtype=np.int32), w.w1,
+                          w.w3, w.w2, None, None, None, None,
+                          y_routed=tp.yback_t[me, e0 * blk:e1 * blk])
+
     _, y_sh = stages.expert_ffn(None, None, None, None, None, None, xm, w.shared_w1, w.shared_w3,
                                 w.shared_w2)
     _mark(timeline, "shared")
+    own_part(0, half)
+    _mark(timeline, "own_a")
 
     y_recv = torch.empty((R, n, d), dtype=ydt, device=dev)
     for s in range(1, R):
@@ -386,10 +403,8 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
     for st in tp.streams:
         y_recv.record_stream(st)
 
-    # own chunk last: its result needs no transfer, so it hides the last return
-    stages.expert_ffn(xg[me * n:(me + 1) * n], coff, cex, w.w1, w.w3, w.w2, None, None, None,
-                      None, y_routed=tp.yback_t[me])
-    _mark(timeline, "own")
+    own_part(half, El)
+    _mark(timeline, "own_b")
 
     for q in range(R):
         if q != me:
