@@ -412,7 +412,19 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
         tl = []
         ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx, timeline=tl)
         torch.cuda.synchronize()
-        out["timeline"] = {n: round(tl[0][1].elapsed_time(e), 4) for n, e in tl}
+        full = {n: round(tl[0][1].elapsed_time(e), 4) for n, e in tl}
+        out["timeline"] = {n: v for n, v in full.items() if not n.startswith("copy_")}
+        starts = [v for n, v in full.items() if n.startswith("copy_start")]
+        ends = [v for n, v in full.items() if n.startswith("copy_end")]
+        if starts:
+            # dispatch copies (copy engines over NVLink): bytes this rank sent / wall span
+            from paper_2604_12163_b200.router import capacity_for
+            cap = capacity_for(c["S"], c["E"], c["C"])
+            chunk = c["E"] // world * (c["B"] // world) * cap * c["d"] * 2
+            span = max(ends) - min(starts)
+            out["dispatch"] = {"bytes": chunk * (world - 1), "ms": round(span, 4),
+                               "gbs": chunk * (world - 1) / (span * 1e-3) / 1e9,
+                               "per_copy_ms": sorted(round(e - s_, 4) for s_, e in zip(starts, ends))}
     if want_e2e:
         # e2e through the public EP API with pinned host buffers per rank,
         # uploads / layer / downloads overlapped across steps (pipeline.py)
@@ -511,7 +523,7 @@ def run_ep(args, c, peaks, peak_kind):
         wc4 = work_counts(CFG4)
         strong = {"workload": workload_name(CFG4), "ms_per_step": st["ms"],
                   "value": wc4["T"] / (st["ms"] * 1e-3), "unit": "tokens/s",
-                  "timeline_ms_rank0": st["timeline"]}
+                  "timeline_ms_rank0": st["timeline"], "nvlink_dispatch_rank0": st.get("dispatch")}
         if ms1 is not None:
             strong["same_config_1gpu"] = {"ms_per_step": ms1, "value": wc4["T"] / (ms1 * 1e-3)}
             strong["efficiency"] = ms1 / (world * st["ms"])
@@ -536,6 +548,7 @@ def run_ep(args, c, peaks, peak_kind):
                        "l2": "inputs larger than L2"},
             "a2a_bytes_per_rank_per_direction": a2a,
             "timeline_ms_rank0": main["timeline"],
+            "nvlink_dispatch_rank0": main.get("dispatch"),
             "cfg4_strong": strong,
             "e2e": {"value": wcw["T"] / (main["e2e_ms"] * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": main["h2d"] * world,

@@ -48,6 +48,11 @@ from .moe import ExpertBank
 from .router import RouterConfig, build_routing, capacity_for
 
 
+import os as _os
+
+_DISPATCH_SERIAL = _os.environ.get("NIMG_EP_DISPATCH", "parallel") == "serial"
+
+
 @dataclass(frozen=True)
 class EPPlan:
     """Static exchange plan for one rank (pure host arithmetic)."""
@@ -166,7 +171,8 @@ class CETransport:
         self.flags = PeerBuffer(3 * world * 4, group, rank, world)   # disp | ret | comb
         self.recv_t = _view(self.recv.own, (world, chunk_rows, d), act, device)
         self.yback_t = _view(self.yback.own, (world, chunk_rows, d), ydt, device)
-        self.streams = [torch.cuda.Stream(device) for _ in range(world)]
+        self.streams = [torch.cuda.Stream(device) for _ in range(world)]   # returns, per peer
+        self.disp_stream = torch.cuda.Stream(device)
         self.epoch = 0
         self.key = (chunk_rows, d, act, ydt)
         dist.barrier(group=group)   # every buffer zeroed and mapped before first use
@@ -346,18 +352,31 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
     xbytes, ybytes = n * d * tp.act_es, n * d * tp.y_es
     coff, cex = plan.chunk_segments()
 
-    # dispatch: one copy per destination rank, straight into its recv slot
+    # dispatch: one copy per destination rank, straight into its recv slot.
+    # "parallel" (default): one stream per destination; "serial"
+    # (NIMG_EP_DISPATCH=serial): one stream, in the order destinations consume
+    # the chunks (destination me+s uses it at its step s).
     x_ready = torch.cuda.Event()
     x_ready.record(comp)
+    serial = _DISPATCH_SERIAL
     for s in range(1, R):
         q = (me + s) % R
-        st = tp.streams[q]
-        st.wait_event(x_ready)
+        st = tp.disp_stream if serial else tp.streams[q]
+        if not serial or s == 1:
+            st.wait_event(x_ready)
         sh = st.cuda_stream
         if k > 1:   # q consumed my previous chunk
             _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, RET, q), k - 1, sh))
+        if timeline is not None:
+            ev0 = torch.cuda.Event(enable_timing=True)
+            ev0.record(st)
         _lib.check(L.nimg_copy_async(tp.recv.ptrs[q] + me * xbytes, xg[q * n:(q + 1) * n].data_ptr(),
                                      xbytes, sh))
+        if timeline is not None:
+            ev1 = torch.cuda.Event(enable_timing=True)
+            ev1.record(st)
+            timeline.append((f"copy_start_q{q}", ev0))
+            timeline.append((f"copy_end_q{q}", ev1))
         _lib.check(L.nimg_stream_write_u32(tp.flag(q, DISP, me), k, sh))
         xg.record_stream(st)
 
