@@ -36,18 +36,25 @@ def _inputs(B, S, d, E, h, seed, dev):
                 sw3=tn(h, d, std=0.02).to(bf), sw2=tn(d, h, std=0.02).to(bf))
 
 
-def _worker(rank, world, port, q, shape):
+def _worker(rank, world, port, q, shape, modes=("plain", "nccl", "ce")):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device("cuda", rank))
+    ngpu = torch.cuda.device_count()
+    dev_idx = rank % ngpu
+    torch.cuda.set_device(dev_idx)
+    if world > ngpu:
+        # oversubscribed (several ranks per GPU): NCCL refuses duplicate
+        # devices, the copy-engine transport only needs a CPU control plane
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", dev_idx))
     try:
         from paper_2604_12163_b200 import moe as M
         from paper_2604_12163_b200 import router as R
         from paper_2604_12163_b200.ep import EPContext, ep_moe_forward, shard_bank
         B, S, d, E, h, C = shape
-        dev = torch.device("cuda", rank)
+        dev = torch.device("cuda", dev_idx)
         a = _inputs(B, S, d, E, h, 7, dev)
         cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
         bank = M.ExpertBank(a["w1"], a["w3"], a["w2"], a["sw1"], a["sw3"], a["sw2"])
@@ -56,7 +63,7 @@ def _worker(rank, world, port, q, shape):
         sl = slice(rank * bl, (rank + 1) * bl)
         local = shard_bank(bank, rank, world)
         res = {}
-        for mode in ("plain", "nccl", "ce"):
+        for mode in modes:
             ctx = EPContext(overlap=mode != "plain", transport="nccl" if mode == "nccl" else "ce")
             ok = True
             for _ in range(3):   # several steps: exercises the per-step flag epochs
@@ -71,11 +78,12 @@ def _worker(rank, world, port, q, shape):
         dist.destroy_process_group()
 
 
-def _run(world, shape):
+def _run(world, shape, modes=("plain", "nccl", "ce")):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shape)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shape, modes))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -112,3 +120,17 @@ def test_ep_two_gpus_bitwise():
     res = _run(2, (4, 1024, 2048, 64, 1344, 4.0))
     for r in range(2):
         assert res[r] == {"plain": True, "nccl": True, "ce": True}, res
+
+
+@pytest.mark.parametrize("world", [4, 8])
+def test_ep_oversubscribed_ce_bitwise(world):
+    """R ranks on fewer GPUs (rank % n_gpus): exercises the R-peer copy-engine
+    schedule, segment tables and flag epochs at R = 4 and 8 on any box
+    (an 8-GPU node is not available to the test runner)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    if torch.cuda.device_count() >= world:
+        pytest.skip("covered by the one-rank-per-GPU runs")
+    res = _run(world, (world, 512, 2048, 64, 1344, 4.0), modes=("ce",))
+    for r in range(world):
+        assert res[r] == {"ce": True}, res
