@@ -400,16 +400,22 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    h0 = time.perf_counter()
     for _ in range(args.steps):
         step()
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # issue time per step
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
     t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    out = {"ms": float(t.item())}
+    out = {"ms": float(t.item()), "host_issue_ms": round(host_ms, 4)}
     if timeline:
         tl = []
+        # two steps ahead of the recorded one keep the host ahead of the GPU,
+        # as in the timed loop (an idle GPU would show host issue latency)
+        step()
+        step()
         ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx, timeline=tl)
         torch.cuda.synchronize()
         full = {n: round(tl[0][1].elapsed_time(e), 4) for n, e in tl}
@@ -549,6 +555,7 @@ def run_ep(args, c, peaks, peak_kind):
             "a2a_bytes_per_rank_per_direction": a2a,
             "timeline_ms_rank0": main["timeline"],
             "nvlink_dispatch_rank0": main.get("dispatch"),
+            "host_issue_ms_rank0": main.get("host_issue_ms"),
             "cfg4_strong": strong,
             "e2e": {"value": wcw["T"] / (main["e2e_ms"] * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": main["h2d"] * world,

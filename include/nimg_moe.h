@@ -151,7 +151,10 @@ int nimg_ffn_workspace_bytes(const nimg_ffn_desc* desc, size_t* bytes);
 /* moe.py:115-135 grouped_forward / moe.py:31-51 swiglu: for each segment i,
  * rows [seg_offsets[i], seg_offsets[i+1]) of x_routed go through expert
  * seg_expert[i] (host arrays). If n_shared_rows > 0, x_shared goes through
- * the shared expert. y dtype: see nimg_ffn_path. */
+ * the shared expert. y dtype: see nimg_ffn_path.
+ * seg_expert[i] == -1 marks a skip segment: its rows are neither read nor
+ * written (the expert-parallel path runs a subset of the received chunks in
+ * one grouped launch over the whole receive buffer). */
 int nimg_expert_ffn(const nimg_ffn_desc* desc, const int64_t* seg_offsets,
                     const int32_t* seg_expert, const void* x_routed, const void* w1,
                     const void* w3, const void* w2, void* y_routed, const void* x_shared,

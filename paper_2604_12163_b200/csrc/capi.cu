@@ -192,13 +192,15 @@ int fill_segments(P& p, const nimg_ffn_desc* f, const int64_t* off, const int32_
                   int ntn0, int ntn1) {
   int64_t tiles = 0;
   int n = 0;
-  for (int i = 0; i < f->nseg; ++i, ++n) {
+  for (int i = 0; i < f->nseg; ++i) {
     const int64_t rows = off[i + 1] - off[i];
+    if (ex && ex[i] < 0) continue;   // skip segment: rows not computed, output untouched
     p.seg_row0[n] = (int)off[i];
     p.seg_rows[n] = (int)rows;
     p.seg_expert[n] = ex ? ex[i] : i;
     p.seg_tile0[n] = (int)tiles;
     tiles += (rows + bm - 1) / bm * ntn0;
+    ++n;
   }
   p.nseg0 = n;
   if (f->n_shared_rows > 0) {
@@ -238,7 +240,7 @@ int check_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex) {
                   (long long)f->n_rows);
     for (int i = 0; i < f->nseg; ++i) {
       const int e = ex ? ex[i] : i;
-      if (e < 0 || e >= f->n_experts) return fail(NIMG_ERR_SHAPE, "segment %d expert %d out of range", i, e);
+      if (e < -1 || e >= f->n_experts) return fail(NIMG_ERR_SHAPE, "segment %d expert %d out of range", i, e);
     }
   } else if (f->n_rows != 0) {
     return fail(NIMG_ERR_SHAPE, "rows without segments");

@@ -51,6 +51,8 @@ from .router import RouterConfig, build_routing, capacity_for
 import os as _os
 
 _DISPATCH_SERIAL = _os.environ.get("NIMG_EP_DISPATCH", "parallel") == "serial"
+# remote chunks are computed in groups of at least this many rows per launch
+_GROUP_ROWS = int(_os.environ.get("NIMG_EP_GROUP_ROWS", "12288"))
 
 
 @dataclass(frozen=True)
@@ -97,6 +99,45 @@ class EPPlan:
         El = self.experts_per_rank
         return (np.arange(El + 1, dtype=np.int64) * self.block_rows,
                 np.arange(El, dtype=np.int32))
+
+    def chunk_groups(self, min_rows: int):
+        """Remote source ranks in arrival order (src = rank-1, rank-2, ...: the
+        sender at distance s dispatches to this rank at its step s), split
+        into consecutive groups of ~min_rows rows each, one grouped launch per
+        group: small chunks alone would run partial waves on every launch.
+        Group sizes are non-increasing, so the last group's return (which
+        the rank's own second half must hide) is the smallest."""
+        srcs = [(self.rank - s) % self.world for s in range(1, self.world)]
+        if not srcs:
+            return []
+        g = max(1, -(-min_rows // max(1, self.chunk_rows)))
+        ng = -(-len(srcs) // g)
+        base, extra = divmod(len(srcs), ng)
+        out, i = [], 0
+        for j in range(ng):
+            k = base + (1 if j < extra else 0)
+            out.append(srcs[i:i + k])
+            i += k
+        return out
+
+    def group_segments(self, srcs):
+        """(offsets, expert ids) over the whole receive buffer computing only
+        the chunks of `srcs`; other chunks are skip segments (expert -1, one
+        per run of skipped chunks)."""
+        El, blk, n = self.experts_per_rank, self.block_rows, self.chunk_rows
+        want = set(srcs)
+        off, ex = [0], []
+        for src in range(self.world):
+            if src in want:
+                for el in range(El):
+                    off.append(src * n + (el + 1) * blk)
+                    ex.append(el)
+            elif ex and ex[-1] == -1:
+                off[-1] = (src + 1) * n
+            else:
+                off.append((src + 1) * n)
+                ex.append(-1)
+        return np.asarray(off, dtype=np.int64), np.asarray(ex, dtype=np.int32)
 
     def step_peers(self, s: int):
         """Pairwise step s (1..R-1): (send-to, receive-from) for the dispatch;
@@ -388,37 +429,44 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
     blk = plan.block_rows
     own_x = xg[me * n:(me + 1) * n]
 
-    def own_part(e0, e1):
+    def own_part(e0, e1, shared=False):
+        xs = (xm, w.shared_w1, w.shared_w3, w.shared_w2) if shared else (None,) * 4
         if e1 <= e0:
-            return
+            return stages.expert_ffn(None, None, None, None, None, None, *xs) if shared else None
         off = (np.arange(e0, e1 + 1, dtype=np.int64) - e0) * blk
-        stages.expert_ffn(own_x[e0 * blk:e1 * blk], off, np.arange(e0, e1, dtype=np.int32), w.w1,
-                          w.w3, w.w2, None, None, None, None,
-                          y_routed=tp.yback_t[me, e0 * blk:e1 * blk])
+        return stages.expert_ffn(own_x[e0 * blk:e1 * blk], off, np.arange(e0, e1, dtype=np.int32),
+                                 w.w1, w.w3, w.w2, *xs, y_routed=tp.yback_t[me, e0 * blk:e1 * blk])
 
-    _, y_sh = stages.expert_ffn(None, None, None, None, None, None, xm, w.shared_w1, w.shared_w3,
-                                w.shared_w2)
-    _mark(timeline, "shared")
-    own_part(0, half)
-    _mark(timeline, "own_a")
+    # shared expert + first half of the own chunk in one grouped launch
+    _, y_sh = own_part(0, half, shared=True)
+    _mark(timeline, "shared+own_a")
 
     y_recv = torch.empty((R, n, d), dtype=ydt, device=dev)
-    for s in range(1, R):
-        src = (me - s) % R
-        _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, DISP, src), k, comp.cuda_stream))
-        stages.expert_ffn(tp.recv_t[src], coff, cex, w.w1, w.w3, w.w2, None, None, None, None,
-                          y_routed=y_recv[src])
-        _mark(timeline, f"chunk{s}")
+    recv_all = tp.recv_t.view(R * n, d)
+    y_all = y_recv.view(R * n, d)
+    for gi, grp in enumerate(plan.chunk_groups(_GROUP_ROWS)):
+        for src in grp:
+            _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, DISP, src), k, comp.cuda_stream))
+        if len(grp) == 1:
+            src = grp[0]
+            stages.expert_ffn(tp.recv_t[src], coff, cex, w.w1, w.w3, w.w2, None, None, None, None,
+                              y_routed=y_recv[src])
+        else:
+            goff, gex = plan.group_segments(grp)
+            stages.expert_ffn(recv_all, goff, gex, w.w1, w.w3, w.w2, None, None, None, None,
+                              y_routed=y_all)
+        _mark(timeline, f"group{gi + 1}")
         done = torch.cuda.Event()
         done.record(comp)
-        st = tp.streams[src]
-        st.wait_event(done)
-        sh = st.cuda_stream
-        if k > 1:   # src has combined the previous step: its y_back slot is free
-            _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, COMB, src), k - 1, sh))
-        _lib.check(L.nimg_copy_async(tp.yback.ptrs[src] + me * ybytes, y_recv[src].data_ptr(),
-                                     ybytes, sh))
-        _lib.check(L.nimg_stream_write_u32(tp.flag(src, RET, me), k, sh))
+        for src in grp:
+            st = tp.streams[src]
+            st.wait_event(done)
+            sh = st.cuda_stream
+            if k > 1:   # src has combined the previous step: its y_back slot is free
+                _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, COMB, src), k - 1, sh))
+            _lib.check(L.nimg_copy_async(tp.yback.ptrs[src] + me * ybytes, y_recv[src].data_ptr(),
+                                         ybytes, sh))
+            _lib.check(L.nimg_stream_write_u32(tp.flag(src, RET, me), k, sh))
     for st in tp.streams:
         y_recv.record_stream(st)
 

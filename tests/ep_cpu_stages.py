@@ -43,15 +43,13 @@ class OracleStages:
                    y_routed=None, y_shared=None):
         if x_routed is not None:
             xr = x_routed.numpy()
-            y = np.zeros((xr.shape[0], xr.shape[1]), np.float32)
+            if y_routed is None:
+                y_routed = torch.zeros((xr.shape[0], xr.shape[1]), dtype=torch.float32)
             for i, e in enumerate(seg_expert):
                 lo, hi = int(seg_offsets[i]), int(seg_offsets[i + 1])
-                if hi > lo:
-                    y[lo:hi] = O.swiglu_arrays(xr[lo:hi], w1[e].numpy(), w3[e].numpy(), w2[e].numpy())
-            if y_routed is None:
-                y_routed = torch.from_numpy(y)
-            else:
-                y_routed.copy_(torch.from_numpy(y))
+                if hi > lo and e >= 0:      # e == -1: skip segment, rows untouched
+                    y_routed[lo:hi] = torch.from_numpy(
+                        O.swiglu_arrays(xr[lo:hi], w1[e].numpy(), w3[e].numpy(), w2[e].numpy()))
         if x_shared is not None:
             ys = torch.from_numpy(O.swiglu_arrays(x_shared.numpy(), sw1.numpy(), sw3.numpy(), sw2.numpy()))
             if y_shared is None:

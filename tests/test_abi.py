@@ -75,6 +75,23 @@ def test_ffn_path_selection():
     assert p.value == L.NIMG_PATH_SIMT
 
 
+def test_ffn_segment_validation():
+    """Host-side checks run before any device work: expert ids must lie in
+    [-1, E) (-1 = skip segment), offsets start at 0, end at n_rows."""
+    L = _lib()
+    f = L.FfnDesc(n_rows=64, n_shared_rows=0, d=32, h=32, h_shared=32, n_experts=4,
+                  act_dtype=L.NIMG_BF16, nseg=2)
+    off = (C.c_int64 * 3)(0, 32, 64)
+    call = lambda ex: L.lib.nimg_expert_ffn(C.byref(f), off, (C.c_int32 * 2)(*ex), None, None, None,
+                                            None, None, None, None, None, None, None, None, 0, None)
+    assert call((0, 4)) == L.NIMG_ERR_SHAPE
+    assert b"expert 4 out of range" in L.lib.nimg_last_error()
+    assert call((-2, 0)) == L.NIMG_ERR_SHAPE
+    off[2] = 63
+    assert call((0, -1)) == L.NIMG_ERR_SHAPE
+    assert b"offsets end" in L.lib.nimg_last_error()
+
+
 def test_python_api_mirrors_reference_host_functions():
     from paper_2604_12163_b200 import router as R
     assert R.capacity_for(1024, 64, 4.0) == 64

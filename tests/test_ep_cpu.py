@@ -34,6 +34,36 @@ def test_plan_layout():
         EPPlan(world=3, rank=0, n_experts=64, b_local=1, seq=8, cap=1)
 
 
+def test_chunk_groups_and_skip_segments():
+    from paper_2604_12163_b200.ep import EPPlan
+    # cfg2 weak-scaled at 8 ranks: chunks of 8192 rows run in pairs
+    p = EPPlan(world=8, rank=1, n_experts=64, b_local=16, seq=1024, cap=64)
+    assert p.chunk_rows == 8192
+    groups = p.chunk_groups(12288)
+    assert groups == [[0, 7], [6, 5], [4, 3], [2]]           # arrival order, sizes 2,2,2,1
+    assert sorted(sum(groups, [])) == [0, 2, 3, 4, 5, 6, 7]
+    off, ex = p.group_segments([0, 7])                      # wraps around the buffer
+    n, blk = p.chunk_rows, p.block_rows
+    assert off[0] == 0 and off[-1] == 8 * n and np.all(np.diff(off) >= 0)
+    assert list(ex) == list(range(8)) + [-1] + list(range(8))
+    assert off[8] == n and off[9] == 7 * n and off[10] == 7 * n + blk
+    # 4 ranks: chunks already >= the threshold, one per launch
+    q = EPPlan(world=4, rank=2, n_experts=64, b_local=16, seq=1024, cap=64)
+    assert q.chunk_groups(12288) == [[1], [0], [3]]
+    # cfg4 strong at 8 ranks (4096-row chunks): groups of 3,2,2
+    r = EPPlan(world=8, rank=0, n_experts=64, b_local=4, seq=4096, cap=128)
+    assert [len(g) for g in r.chunk_groups(12288)] == [3, 2, 2]
+    assert EPPlan(world=1, rank=0, n_experts=8, b_local=2, seq=16, cap=4).chunk_groups(12288) == []
+    # every computed row is covered exactly once, skipped chunks not at all
+    off, ex = r.group_segments([7, 6, 5])
+    cover = np.zeros(8 * r.chunk_rows, np.int32)
+    for i, e in enumerate(ex):
+        if e >= 0:
+            cover[off[i]:off[i + 1]] += 1
+    assert cover.reshape(8, -1).all(axis=1).tolist() == [False] * 5 + [True] * 3
+    assert cover.max() == 1
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))

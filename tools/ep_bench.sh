@@ -6,7 +6,7 @@ echo "== N=$N rc=$?"
 python - <<PY
 import json
 j = json.loads(open("gpurun_out/ep${N}.json").read().strip().splitlines()[-1])
-print("weak: ms %.3f value %.4g" % (j["ms_per_step"], j["value"]), j["timeline_ms_rank0"])
+print("weak: ms %.3f value %.4g host %s" % (j["ms_per_step"], j["value"], j.get("host_issue_ms_rank0")), j["timeline_ms_rank0"])
 s = j.get("cfg4_strong")
 if s:
     print("cfg4 strong: ms %.3f eff %s" % (s["ms_per_step"], s.get("efficiency")), s["timeline_ms_rank0"])
