@@ -37,6 +37,11 @@ FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 
 CFG2 = dict(name="cfg2", B=16, S=1024, d=2048, h=1344, E=64, C=4.0, layer=17, seed=2)
 CFG4 = dict(name="cfg4", B=32, S=4096, d=2048, h=1344, E=64, C=2.0, layer=17, seed=4)
+# the capacity-factor sweep (C in {8, 4, 2}) at 1024px, 1 GPU
+CFG3 = dict(name="cfg3", B=16, S=4096, d=2048, h=1344, E=64, C=4.0, layer=17, seed=3)
+CONFIGS = {"cfg2": CFG2, "cfg3": CFG3, "cfg4": CFG4}
+# FP64 (DMMA/DFMA) throughput measured on the B200 boxes with tools/microbench_fp64.cu
+FP64_PEAK_TFLOPS = 37.0
 
 
 def load_peaks():
@@ -231,22 +236,24 @@ def run_single(args, c, peaks, peak_kind):
     value = wc["T"] / (ms * 1e-3)
 
     # ---- per-stage times (stage events recorded by the library on the stream)
-    n_ev = 6
+    n_ev = 7   # marks 0..5 = stage boundaries, 6 = router scores done
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
     for row in evs:
         for e in row:
             e.record()  # torch creates the underlying cudaEvent_t lazily
     torch.cuda.synchronize()
-    stage_ms = [0.0] * (n_ev - 1)
+    stage_ms = [0.0] * 5
     for k in range(args.steps):
         arr = (C.c_void_p * n_ev)(*[e.cuda_event for e in evs[k]])
         _lib.check(_lib.lib.nimg_profile_events(arr, n_ev))
         fwd()
     _lib.check(_lib.lib.nimg_profile_events(None, 0))
     torch.cuda.synchronize()
+    router_ms = 0.0
     for k in range(args.steps):
-        for i in range(n_ev - 1):
+        for i in range(5):
             stage_ms[i] += evs[k][i].elapsed_time(evs[k][i + 1]) / args.steps
+        router_ms += evs[k][0].elapsed_time(evs[k][6]) / args.steps
     names = ["route", "gather", "gemm1_swiglu", "gemm2", "combine"]
     stages = dict(zip(names, stage_ms))
     hbm = peaks["hbm_gbs"]
@@ -259,6 +266,12 @@ def run_single(args, c, peaks, peak_kind):
         "gemm1_ms": stages["gemm1_swiglu"], "gemm2_ms": stages["gemm2"],
         "combine_ms": stages["combine"],
         "gemm1_tflops": g1_tf, "gemm2_tflops": g2_tf,
+        # router scores kernel (f64-accumulated [x_norm|t_emb] W_r + softmax) vs
+        # the measured FP64 pipe; the rest of route_ms is select + gates
+        "router_scores_ms": router_ms,
+        "router_f64_tflops": wc["flops_router"] / (router_ms * 1e-3) / 1e12,
+        "router_frac_of_fp64_peak": wc["flops_router"] / (router_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+        "select_gates_ms": stages["route"] - router_ms,
         "gather_gbs": wc["bytes_gather"] / (stages["gather"] * 1e-3) / 1e9,
         "combine_gbs": wc["bytes_combine"] / (stages["combine"] * 1e-3) / 1e9,
     }
@@ -284,13 +297,17 @@ def run_single(args, c, peaks, peak_kind):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded randn, random-init weights)",
         "config": {"workload": workload_name(c), "capacity": wc["cap"], "routed_rows": wc["R"],
                    "tokens": wc["T"], "parallelism": "single GPU",
-                   "l2": "inputs larger than L2 (1.07 GB expert weights + 134 MB activations per step)"},
+                   "l2": f"inputs larger than L2 (1.07 GB expert weights + "
+                         f"{2 * wc['T'] * c['d'] * 2 / 1e6:.0f} MB activations per step)"},
         "expert_gemm_tflops": ffn_tf,
         "expert_gemm_frac_of_peak": ffn_tf / tf_peak,
+        "expert_gemm_frac_of_datasheet": ffn_tf / 2250.0,
         "roofline": {"bound": "tensor", "kernel": "grouped_gemm_sm100<0> (GEMM1 dual-B SwiGLU)",
                      "achieved": g1_tf, "peak": tf_peak, "unit": "TFLOP/s",
                      "frac": g1_tf / tf_peak,
-                     "traffic": args.traffic if args.traffic is not None else gemm1_traffic(),
+                     # the committed ncu capture is of the default cfg2 workload
+                     "traffic": args.traffic if args.traffic is not None else (
+                         gemm1_traffic() if c == CFG2 else None),
                      "traffic_unit": "bytes (dram read+write per launch, ncu)",
                      "peak_source": f"{peak_kind} bf16_tflops (burst)",
                      "kernel_impl": "grouped_gemm_sm100_pair<0>: tcgen05 cta_group::2, UMMA 256x224x16",
@@ -574,7 +591,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, choices=["cfg2", "cfg4"])
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--capacity", type=float, default=None,
+                    help="override the config's capacity factor C (cfg3 sweep: 8, 4, 2)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -588,9 +607,11 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    c = dict(CFG2 if (args.config or "cfg2") == "cfg2" else CFG4)
+    c = dict(CONFIGS[args.config or "cfg2"])
     if args.batch:
         c["B"] = args.batch
+    if args.capacity:
+        c["C"] = args.capacity
     if args.impl == "reference":
         run_reference_arm(args, c)
         return

@@ -24,6 +24,7 @@ __global__ void block_modvec_kernel(const float* __restrict__ sa_gate,
                                     double* __restrict__ th_ff, float* __restrict__ onep,
                                     float* __restrict__ th_sa_f, float* __restrict__ th_ff_f,
                                     int64_t n) {
+  pdl_trigger();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const double a = tanh((double)sa_gate[i]), g = tanh((double)ff_gate[i]);
@@ -42,6 +43,8 @@ block_prologue_bf16_kernel(const bf16* __restrict__ x, const bf16* __restrict__ 
                            const float* __restrict__ th_sa, const float* __restrict__ onep,
                            bf16* __restrict__ h_out, bf16* __restrict__ xn_out,
                            bf16* __restrict__ xm_out, int64_t T_tok, int S, int d, float scale_t) {
+  pdl_trigger();
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t = (int64_t)blockIdx.x * BPF_WARPS + warp;
   if (t >= T_tok) return;
@@ -102,6 +105,8 @@ block_prologue_kernel(const T* __restrict__ x, const T* __restrict__ r_attn,
                       const double* __restrict__ th_sa, const float* __restrict__ onep,
                       T* __restrict__ h_out, T* __restrict__ xn_out, T* __restrict__ xm_out,
                       int64_t T_tok, int S, int d, float scale_t, int balanced) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nleaf = (d + 127) / 128;
@@ -206,10 +211,9 @@ cudaError_t launch_block_prologue(bool bf, const void* x, const void* r_attn, co
                                   void* xm, int64_t T, int S, int d, float scale_t, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
   if (bf && d % 256 == 0 && d <= 2048) {
-    block_prologue_bf16_kernel<<<(unsigned)((T + BPF_WARPS - 1) / BPF_WARPS), BPF_WARPS * 32, 0, s>>>(
-        (const bf16*)x, (const bf16*)r_attn, th_sa_f, onep, (bf16*)h, (bf16*)xn, (bf16*)xm, T, S, d,
-        scale_t);
-    return cudaGetLastError();
+    return launch_pdl(block_prologue_bf16_kernel, dim3((unsigned)((T + BPF_WARPS - 1) / BPF_WARPS)),
+                      dim3(BPF_WARPS * 32), 0, s, (const bf16*)x, (const bf16*)r_attn, th_sa_f, onep,
+                      (bf16*)h, (bf16*)xn, (bf16*)xm, T, S, d, scale_t);
   }
   const int nleaf = (d + 127) / 128;
   const int balanced = (d % 128 == 0) && nleaf <= 32 && (nleaf & (nleaf - 1)) == 0;
@@ -219,17 +223,17 @@ cudaError_t launch_block_prologue(bool bf, const void* x, const void* r_attn, co
   if (bf) {
     e = cudaFuncSetAttribute(block_prologue_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    block_prologue_kernel<bf16><<<grid, BP_WARPS * 32, smem, s>>>(
-        (const bf16*)x, (const bf16*)r_attn, th_sa, onep, (bf16*)h, (bf16*)xn, (bf16*)xm, T, S, d,
-        scale_t, balanced);
+    e = launch_pdl(block_prologue_kernel<bf16>, dim3(grid), dim3(BP_WARPS * 32), smem, s,
+                   (const bf16*)x, (const bf16*)r_attn, th_sa, onep, (bf16*)h, (bf16*)xn, (bf16*)xm,
+                   T, S, d, scale_t, balanced);
   } else {
     e = cudaFuncSetAttribute(block_prologue_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    block_prologue_kernel<float><<<grid, BP_WARPS * 32, smem, s>>>(
-        (const float*)x, (const float*)r_attn, th_sa, onep, (float*)h, (float*)xn, (float*)xm, T,
-        S, d, scale_t, balanced);
+    e = launch_pdl(block_prologue_kernel<float>, dim3(grid), dim3(BP_WARPS * 32), smem, s,
+                   (const float*)x, (const float*)r_attn, th_sa, onep, (float*)h, (float*)xn,
+                   (float*)xm, T, S, d, scale_t, balanced);
   }
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace nimg

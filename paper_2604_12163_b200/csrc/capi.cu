@@ -22,7 +22,8 @@ namespace {
 
 thread_local std::string g_err;
 // Optional stage events (nimg_profile_events): recorded on the launch stream
-// at the stage boundaries of nimg_moe_forward. Null = off.
+// at the stage boundaries of nimg_moe_forward (0 start, 1 routed, 2 gathered,
+// 3 GEMM1 done, 4 GEMM2 done, 5 combined; 6 router scores done). Null = off.
 thread_local cudaEvent_t g_events[8];
 thread_local int g_nevents = 0;
 inline void mark(int i, cudaStream_t st) {
@@ -145,8 +146,9 @@ int check_moe_desc(const nimg_moe_desc* d) {
   return NIMG_OK;
 }
 
-// Route scratch. `counters` (B u32) sits right after slot_of so a single
-// 0xFF memset arms both: slot_of = -1 ("not selected"), counters = 0xFFFFFFFF.
+// Route scratch: t-bias, DFMA-router partials / f64 W_r / counters, and the
+// slot table slot_of (B, E, S) int16 (slot in the expert's column, -1 = not
+// selected), written in full by ec_select.
 struct RouteWs {
   double* tb;
   double* part;
@@ -376,13 +378,14 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
   if (!ws || ws_bytes < route_ws_bytes(d)) return fail(NIMG_ERR_CONFIG, "workspace too small");
   const int B = (int)d->B, S = (int)d->S, dd = (int)d->d, E = (int)d->E, cap = (int)d->cap;
   RouteWs w = carve_route(d, ws);
-  // One memset arms the slot table (-1) and the prep kernel's per-sample
-  // completion counters (0xFFFFFFFF); the workspace is caller-owned.
-  CUDA_TRY(cudaMemsetAsync(w.slot_of, 0xFF,
-                           (size_t)(reinterpret_cast<uint8_t*>(w.counters) -
-                                    reinterpret_cast<uint8_t*>(w.slot_of)) + (size_t)B * 4, st));
+  // ec_select writes the whole slot table; only the DFMA router (E > 64) needs
+  // its per-sample completion counters armed (0xFFFFFFFF; the workspace is
+  // caller-owned).
+  if (!router_uses_dmma(E))
+    CUDA_TRY(cudaMemsetAsync(w.counters, 0xFF, (size_t)B * 4, st));
   CUDA_TRY(launch_router(d->act_dtype == NIMG_BF16, x_norm, t_emb, w_r, w.tb, w.part, w.counters,
                          w.wd, o->logits, o->scores_bes, B, S, dd, E, st));
+  mark(6, st);   // router scores done (inside stage 0 -> 1)
   CUDA_TRY(launch_ec_select(o->scores_bes, o->token_flat, o->gate_raw, w.slot_of, B, S, E, cap, st));
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
   CUDA_TRY(launch_gate_norm(o->scores_bes, w.slot_of, o->gates, o->comb_rows, o->comb_cnt, B, S,

@@ -14,6 +14,14 @@ namespace nimg {
 typedef __nv_bfloat16 bf16;
 
 // ---------------------------------------------------------------- basics
+// Programmatic dependent launch. Every kernel of the layer triggers its
+// dependents on entry and waits for its predecessor before its first global
+// access, so a kernel's launch and prologue overlap the previous kernel's tail
+// while all memory effects stay in stream order (each wait covers the whole
+// chain transitively). Both are no-ops for a launch without the attribute.
+NIMG_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+NIMG_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 NIMG_DEV uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

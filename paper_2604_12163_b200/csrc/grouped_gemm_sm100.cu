@@ -92,6 +92,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
@@ -108,6 +109,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();   // setup above overlapped the previous kernel; inputs are ready now
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer (whole warp)
@@ -315,6 +317,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
   const bool leader = crank == 0;
   const int cluster_id = blockIdx.x >> 1;
   const int n_clusters = gridDim.x >> 1;
+  pdl_trigger();
 
   if (threadIdx.x == 0) {
     const uint32_t full_count = 1 + (GATHER ? 2 : 0);   // producer + one relay per CTA
@@ -336,6 +339,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();   // setup above overlapped the previous kernel; inputs are ready now
 
   if (warp == 0) {
     if (lane == 0) {
@@ -513,8 +517,8 @@ static cudaError_t launch_pair(const TmapSet& tm, const GroupedParams& p, int gr
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES><<<grid, threads, smem, stream>>>(tm, p);
-  return cudaGetLastError();
+  return launch_pdl(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES>, dim3(grid), dim3(threads),
+                    (size_t)smem, stream, tm, p);
 }
 
 // Shallow-pipeline variant (4 stages, ~122-130 KB smem) leaves room on each
@@ -555,7 +559,8 @@ cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& 
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    tc::grouped_gemm_sm100<0><<<grid, tc::kThreads, smem, stream>>>(tm, p);
+    return launch_pdl(tc::grouped_gemm_sm100<0>, dim3(grid), dim3(tc::kThreads), (size_t)smem,
+                      stream, tm, p);
   } else {
     constexpr int smem = tc::smem_bytes<1>();
     static bool attr = false;
@@ -565,9 +570,9 @@ cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& 
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    tc::grouped_gemm_sm100<1><<<grid, tc::kThreads, smem, stream>>>(tm, p);
+    return launch_pdl(tc::grouped_gemm_sm100<1>, dim3(grid), dim3(tc::kThreads), (size_t)smem,
+                      stream, tm, p);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace nimg

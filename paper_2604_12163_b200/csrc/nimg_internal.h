@@ -61,6 +61,25 @@ struct SimtParams {
   int seg_expert[kMaxSeg];
 };
 
+// Launch with programmatic stream serialization (PDL) unless NIMG_PDL=0. The
+// kernel must call pdl_wait() before touching global memory (common.cuh).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 int tc_bn_out(int mode);
 int tc_pair_rows();
 // CTA-pair (cta_group::2) variant: 256-row tiles, B split across the pair.
@@ -75,9 +94,12 @@ int simt_bn();
 cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream);
 
 // routing / data-movement kernels (route_kernels.cu)
-// router prep (t-half bias + f64 copy of W_r[:d]) and FP64 scores kernel
-// counters: B unsigned per-sample completion counters, 0xFFFFFFFF on entry
-// (re-armed by the kernel).
+// router prep (t-half bias + f64 copy of W_r[:d]) and FP64 scores kernel.
+// E <= 64 (DMMA): one prep kernel writes tb and wd (no counters / part, may
+// be null); the scores kernel is its PDL secondary.
+// E > 64 (DFMA): counters = B unsigned per-sample completion counters,
+// 0xFFFFFFFF on entry (re-armed by the kernel).
+bool router_uses_dmma(int E);
 cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
                           double* tb, double* part, unsigned* counter, double* wd, float* logits,
                           float* scores_bes, int B, int S, int d, int E, cudaStream_t s);

@@ -13,6 +13,7 @@
 //   gather_rows    x_mod rows into expert-major order (moe.py:152-153).
 //   combine        deterministic expert-ascending weighted sum + shared expert
 //                  (moe.py:156-161, tensor.py:366-378).
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -139,6 +140,8 @@ __global__ void __launch_bounds__(RT_THREADS)
 router_scores_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
                      const double* __restrict__ tb, float* __restrict__ logits,
                      float* __restrict__ scores_bes, int B, int S, int d, int E) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   const RouterGeom g = router_geom(E);
   constexpr int XV = XVec<TX>::N;            // elements per 16-B vector
@@ -309,13 +312,58 @@ router_scores_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
 // x rows of 36 doubles (288 B == 32 mod 128), W rows of 72 doubles (576 B ==
 // 64 mod 128).
 constexpr int DM_TM = 64, DM_KC = 32, DM_XS = 36, DM_WS = 72, DM_EP = 64;
+// Router prep for the DMMA router (E <= 64), one short kernel with no
+// counters: blocks [0, B) compute tb[b, e] = sum_k t_emb[b, k] * W_r[d + k, e]
+// in f64 (router.py:120-122; thread (e, slice q) sums 1/16 of k, slices folded
+// in a fixed order, deterministic); blocks [B, B + RP2_CONV) write
+// wd[k, e] = f64(W_r[k, e]) for the x half, E padded to 64.
+constexpr int RP2_CONV = 64;
+__global__ void __launch_bounds__(1024)
+router_prep_dmma_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
+                        double* __restrict__ tb, double* __restrict__ wd, int B, int d, int E) {
+  pdl_trigger();
+  if ((int)blockIdx.x >= B) {
+    const int64_t n = (int64_t)d * DM_EP;
+    const int64_t stride = (int64_t)RP2_CONV * blockDim.x;
+    for (int64_t i = (int64_t)(blockIdx.x - B) * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const int64_t k = i / DM_EP;
+      const int e = (int)(i % DM_EP);
+      wd[i] = e < E ? (double)__ldg(w_r + k * E + e) : 0.0;
+    }
+    return;
+  }
+  __shared__ double part[16][64];
+  const int b = blockIdx.x, e = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int kq = (d + 15) / 16, k0 = q * kq, k1 = min(d, k0 + kq);
+  double acc = 0.0;
+  if (e < E) {
+    const float* t = t_emb + (int64_t)b * d;
+    const float* w = w_r + (int64_t)d * E + e;
+#pragma unroll 8
+    for (int k = k0; k < k1; ++k) acc = fma((double)__ldg(t + k), (double)__ldg(w + (int64_t)k * E), acc);
+  }
+  part[q][e] = acc;
+  __syncthreads();
+  if (q == 0 && e < E) {
+    double r = part[0][e];
+#pragma unroll
+    for (int j = 1; j < 16; ++j) r += part[j][e];
+    tb[(int64_t)b * E + e] = r;
+  }
+}
+
 __host__ __device__ inline size_t dmma_stage_bytes() {
   return (size_t)DM_KC * DM_WS * 8 + (size_t)DM_TM * DM_XS * 8;
 }
 __host__ __device__ inline size_t dmma_router_smem(int E) {
   const size_t stage = 2 * dmma_stage_bytes();
   const size_t post = (size_t)DM_TM * E * (8 + 4 + 4);
-  return (stage > post ? stage : post) + (size_t)DM_TM * 16;
+  const size_t need = (stage > post ? stage : post) + (size_t)DM_TM * 16;
+  // The grid is sized for exactly 2 CTAs per SM; registers and 74 KB would
+  // admit 3, and a CTA placed early (PDL) on a half-busy GPU would then stack
+  // 3 on some SMs and 1 on others. >= 76 KB caps residency at 2 per SM.
+  constexpr size_t kTwoPerSm = 76 * 1024;
+  return need > kTwoPerSm ? need : kTwoPerSm;
 }
 
 NIMG_DEV void dmma_8x8x4(double& d0, double& d1, double a, double b) {
@@ -330,6 +378,9 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
                           const double* __restrict__ tb, float* __restrict__ logits,
                           float* __restrict__ scores_bes, int B, int S, int d, int E,
                           int frags_per_cta) {
+  // PDL secondary of router_prep_dmma_kernel: only the layer input x_norm is
+  // read before pdl_wait(); wd and tb come from the prep kernel.
+  pdl_trigger();
   // CTA c owns 8-row fragments [c*fpc, (c+1)*fpc) (fpc <= 8); the grid is sized
   // to whole multiples of the SM count (>= 2 CTAs per SM) so per-SM DMMA work
   // is balanced. Warp w computes fragments w and w+4 of the CTA (when present).
@@ -401,6 +452,7 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
 
   const int ar = lane >> 2, ac = lane & 3;   // A frag: (row, k); B frag: (k = ac, col = ar)
   load_x(0);
+  pdl_wait();   // prep kernel complete: wd and tb are ready
   load_w(0, 0);
   cp_async_commit();
   store_x(0);
@@ -587,6 +639,8 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
   __shared__ uint32_t s_digit;
   __shared__ int s_k;
 
+  pdl_trigger();
+  pdl_wait();
   const int b = blockIdx.x, e = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const float* col = scores_bes + ((int64_t)b * E + e) * S;
@@ -663,6 +717,8 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
   }
   for (int i = cap + tid; i < P; i += SEL_THREADS) win[i] = 0ull;
   __syncthreads();
+  // keys[] is free from here on: it becomes this column's slot table
+  for (int i = tid; i < S; i += SEL_THREADS) keys[i] = 0xFFFFFFFFu;
 
   // ---- bitonic sort, descending composite key (score desc, index asc)
   for (int size = 2; size <= P; size <<= 1) {
@@ -684,8 +740,13 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
     const int64_t o = ((int64_t)e * B + b) * cap + j;
     token_flat[o] = (int32_t)((int64_t)b * S + idx);
     gate_raw[o] = col[idx];
-    slot_of[((int64_t)b * S + idx) * E + e] = (int16_t)j;
+    keys[idx] = (uint32_t)j;
   }
+  __syncthreads();
+  // the whole (b, e) column of the slot table, -1 where not selected: no
+  // separate arming pass over the workspace
+  int16_t* scol = slot_of + ((int64_t)b * E + e) * S;
+  for (int i = tid; i < S; i += SEL_THREADS) scol[i] = (int16_t)(int32_t)keys[i];
 }
 
 // ------------------------------------------------------------------ gates
@@ -704,6 +765,8 @@ gate_norm_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* raw_l = reinterpret_cast<float*>(sm) + (size_t)warp * E;
   int32_t* row_l = reinterpret_cast<int32_t*>(sm + (size_t)GN_WARPS * E * 4) + (size_t)warp * E;
+  pdl_trigger();
+  pdl_wait();
   const int64_t T = (int64_t)B * S;
   const int64_t t = (int64_t)blockIdx.x * GN_WARPS + warp;
   if (t >= T) return;
@@ -711,7 +774,7 @@ gate_norm_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict
   int cnt = 0;
   for (int e0 = 0; e0 < E; e0 += 32) {
     const int e = e0 + lane;
-    const int j = e < E ? (int)slot_of[t * E + e] : -1;
+    const int j = e < E ? (int)slot_of[(b * E + e) * S + s] : -1;   // slot table (B, E, S)
     const unsigned m = __ballot_sync(0xffffffffu, j >= 0);
     if (j >= 0) {
       const int pos = cnt + __popc(m & ((1u << lane) - 1u));
@@ -739,6 +802,8 @@ gate_norm_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict
 __global__ void gather_rows_vec_kernel(const int4* __restrict__ src, int64_t row_vecs,
                                        const int32_t* __restrict__ idx, int64_t n_idx,
                                        int4* __restrict__ dst) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= n_idx) return;
   const int lane = threadIdx.x & 31;
@@ -754,6 +819,8 @@ __global__ void gather_rows_vec_kernel(const int4* __restrict__ src, int64_t row
 __global__ void gather_rows_byte_kernel(const uint8_t* __restrict__ src, int64_t row_bytes,
                                         const int32_t* __restrict__ idx, int64_t n_idx,
                                         uint8_t* __restrict__ dst) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t row = blockIdx.x;
   if (row >= n_idx) return;
   const uint8_t* s = src + (int64_t)idx[row] * row_bytes;
@@ -793,6 +860,8 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
                TO* __restrict__ out, int64_t T, int d, int E, const TO* __restrict__ hres,
                const ACC* __restrict__ thg, int S) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int32_t* rows = reinterpret_cast<int32_t*>(sm) + (size_t)warp * E;
@@ -876,11 +945,14 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
 cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
                           double* tb, double* part, unsigned* counter, double* wd, float* logits,
                           float* scores_bes, int B, int S, int d, int E, cudaStream_t s) {
-  const bool dmma = E <= DM_EP;
+  const bool dmma = router_uses_dmma(E);
   const int EP = dmma ? DM_EP : router_geom(E).EP;
   const int nkc = (d + RP_KCH - 1) / RP_KCH;
-  router_prep_kernel<<<dim3(nkc + RP_CONV_BLOCKS, B), 64, 0, s>>>(t_emb, w_r, tb, part, wd, counter,
-                                                                  B, d, E, EP);
+  // the first kernel of the chain: an ordinary launch (full stream order)
+  if (dmma) router_prep_dmma_kernel<<<B + RP2_CONV, 1024, 0, s>>>(t_emb, w_r, tb, wd, B, d, E);
+  // (conversion blocks: RP2_CONV x 1024 threads, 2 elements each at d = 2048)
+  else router_prep_kernel<<<dim3(nkc + RP_CONV_BLOCKS, B), 64, 0, s>>>(t_emb, w_r, tb, part, wd,
+                                                                       counter, B, d, E, EP);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   const int64_t T = (int64_t)B * S;
@@ -908,8 +980,10 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
     err = cudaFuncSetAttribute(router_scores_dmma_kernel<TX, V>,                               \
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     if (err != cudaSuccess) return err;                                                        \
-    router_scores_dmma_kernel<TX, V><<<grid, 128, smem, s>>>(                                  \
-        reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d, E, (int)fpc); \
+    err = launch_pdl(router_scores_dmma_kernel<TX, V>, dim3(grid), dim3(128), smem, s,        \
+                     reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d,   \
+                     E, (int)fpc);                                                              \
+    if (err != cudaSuccess) return err;                                                        \
   } while (0)
     if (x_bf16) {
       if (vec) NIMG_DMMA_LAUNCH(bf16, true); else NIMG_DMMA_LAUNCH(bf16, false);
@@ -927,8 +1001,9 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
     err = cudaFuncSetAttribute(router_scores_kernel<TX, V>,                                    \
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     if (err != cudaSuccess) return err;                                                        \
-    router_scores_kernel<TX, V><<<grid, RT_THREADS, smem, s>>>(                                \
-        reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d, E);          \
+    err = launch_pdl(router_scores_kernel<TX, V>, dim3(grid), dim3(RT_THREADS), smem, s,       \
+                     reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d, E); \
+    if (err != cudaSuccess) return err;                                                        \
   } while (0)
   if (x_bf16) {
     if (vec) NIMG_ROUTER_LAUNCH(bf16, true); else NIMG_ROUTER_LAUNCH(bf16, false);
@@ -937,6 +1012,15 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
   }
 #undef NIMG_ROUTER_LAUNCH
   return cudaGetLastError();
+}
+
+bool router_uses_dmma(int E) { return E <= DM_EP; }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 size_t router_part_bytes(int B, int d, int E) {
@@ -950,9 +1034,8 @@ cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float
   cudaError_t err = cudaFuncSetAttribute(ec_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   dim3 grid(B, E);
-  ec_select_kernel<<<grid, SEL_THREADS, smem, s>>>(scores_bes, token_flat, gate_raw, slot_of, B,
-                                                   S, E, cap);
-  return cudaGetLastError();
+  return launch_pdl(ec_select_kernel, grid, dim3(SEL_THREADS), smem, s, scores_bes, token_flat,
+                    gate_raw, slot_of, B, S, E, cap);
 }
 
 cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,
@@ -961,9 +1044,8 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
   const int64_t T = (int64_t)B * S;
   const int grid = (int)((T + GN_WARPS - 1) / GN_WARPS);
   const size_t smem = (size_t)GN_WARPS * E * 8;
-  gate_norm_kernel<<<grid, GN_WARPS * 32, smem, s>>>(scores_bes, slot_of, gates, comb_rows,
-                                                      comb_cnt, B, S, E, cap, gate_eps, gate_scale);
-  return cudaGetLastError();
+  return launch_pdl(gate_norm_kernel, dim3(grid), dim3(GN_WARPS * 32), smem, s, scores_bes, slot_of,
+                    gates, comb_rows, comb_cnt, B, S, E, cap, gate_eps, gate_scale);
 }
 
 cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
@@ -973,29 +1055,29 @@ cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t
   if (vec) {
     const int rows_per_cta = 8;
     const int64_t grid = (n_idx + rows_per_cta - 1) / rows_per_cta;
-    gather_rows_vec_kernel<<<(unsigned)grid, 32 * rows_per_cta, 0, s>>>(
-        reinterpret_cast<const int4*>(src), row_bytes / 16, idx, n_idx, reinterpret_cast<int4*>(dst));
-  } else {
-    gather_rows_byte_kernel<<<(unsigned)n_idx, 128, 0, s>>>(
-        reinterpret_cast<const uint8_t*>(src), row_bytes, idx, n_idx, reinterpret_cast<uint8_t*>(dst));
+    return launch_pdl(gather_rows_vec_kernel, dim3((unsigned)grid), dim3(32 * rows_per_cta), 0, s,
+                      reinterpret_cast<const int4*>(src), row_bytes / 16, idx, n_idx,
+                      reinterpret_cast<int4*>(dst));
   }
-  return cudaGetLastError();
+  return launch_pdl(gather_rows_byte_kernel, dim3((unsigned)n_idx), dim3(128), 0, s,
+                    reinterpret_cast<const uint8_t*>(src), row_bytes, idx, n_idx,
+                    reinterpret_cast<uint8_t*>(dst));
 }
 
 template <typename TY, typename TO, bool RESID>
-static void combine_dispatch(const void* yr, const void* ys, const float* gates,
+static cudaError_t combine_dispatch(const void* yr, const void* ys, const float* gates,
                              const int32_t* rows, const int32_t* cnt, void* out, int64_t T, int d,
                              int E, const void* hres, const void* thg, int S, cudaStream_t s) {
   const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
   const size_t smem = (size_t)CB_WARPS * E * 8;
   using ACC = typename std::conditional<sizeof(TO) == 2, float, double>::type;
 #define NIMG_COMBINE(V, U)                                                                      \
-  combine_kernel<TY, TO, V, ACC, U, RESID><<<grid, CB_WARPS * 32, smem, s>>>(                  \
-      (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E, (const TO*)hres,   \
-      (const ACC*)thg, S)
-  if (d % 512 == 0) NIMG_COMBINE(8, 2);
-  else if (d % 8 == 0) NIMG_COMBINE(8, 1);
-  else NIMG_COMBINE(1, 1);
+  launch_pdl(combine_kernel<TY, TO, V, ACC, U, RESID>, dim3(grid), dim3(CB_WARPS * 32), smem, s, \
+             (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E, (const TO*)hres, \
+             (const ACC*)thg, S)
+  if (d % 512 == 0) return NIMG_COMBINE(8, 2);
+  if (d % 8 == 0) return NIMG_COMBINE(8, 1);
+  return NIMG_COMBINE(1, 1);
 #undef NIMG_COMBINE
 }
 
@@ -1010,12 +1092,13 @@ cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, con
                                       hres, th_gate, S, s)                                          \
      : combine_dispatch<TY, TO, false>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, \
                                        hres, th_gate, S, s))
-  if (y_bf16 && out_bf16) NIMG_CD(bf16, bf16);
-  else if (y_bf16) NIMG_CD(bf16, float);
-  else if (out_bf16) NIMG_CD(float, bf16);
-  else NIMG_CD(float, float);
+  cudaError_t err;
+  if (y_bf16 && out_bf16) err = NIMG_CD(bf16, bf16);
+  else if (y_bf16) err = NIMG_CD(bf16, float);
+  else if (out_bf16) err = NIMG_CD(float, bf16);
+  else err = NIMG_CD(float, float);
 #undef NIMG_CD
-  return cudaGetLastError();
+  return err;
 }
 
 }  // namespace nimg
