@@ -122,3 +122,31 @@ def make_block_inputs(seed: int, B: int, S: int, d: int, E: int, h: int, mode: s
     elif mode != "fp32":
         raise ValueError(mode)
     return out
+
+
+def perturb_modulation(params: dict, seed: int, w_std: float = 0.2, b_std: float = 0.1):
+    """Zero-initialised modulation makes every block an exact identity
+    (backbone.py:1-6); for parity fixtures, overwrite the modulation weights
+    and biases IN PLACE (same arrays the model holds) with seeded values, in
+    sorted-name order so both sides draw identically."""
+    rng = np.random.default_rng(seed)
+    names = sorted(k for k in params if k.endswith(("img_mod.weight", "img_mod.bias",
+                                                     "final_mod.weight", "final_mod.bias")))
+    for k in names:
+        a = params[k]
+        std = w_std if k.endswith("weight") else b_std
+        a[...] = (trunc_normal(rng, a.shape, std) if k.endswith("weight")
+                  else rng.standard_normal(a.shape) * std).astype(a.dtype)
+    return params
+
+
+def make_latent(seed: int, B: int, C: int, H: int, W: int):
+    """Noisy latent z_t ~ N(0, 1) (B, C, H, W) fp32 and per-sample timesteps
+    spread over [0.2, 0.8]."""
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((B, C, H, W)).astype(np.float32)
+    return z, np.linspace(0.2, 0.8, B)
+
+
+DIT_PROMPTS = ("a red fox in fresh snow at dawn", "two cups of coffee on a wooden table",
+               "mountain lake")

@@ -7,3 +7,7 @@ class ShapeError(ValueError):
 
 class ConfigError(ValueError):
     """Invalid routing configuration (router.py:22-23)."""
+
+
+class DomainError(ValueError):
+    """Scalar argument outside its documented domain (tensor.py:31-32)."""

@@ -22,8 +22,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
-from oracle.workloads import (digest, make_block_inputs, make_layer_inputs,  # noqa: E402
-                              make_router_inputs)
+from oracle.workloads import (DIT_PROMPTS, digest, make_block_inputs,  # noqa: E402
+                              make_latent, make_layer_inputs, make_router_inputs,
+                              perturb_modulation)
 from tests.refimport import load_reference  # noqa: E402
 
 # name -> (kind, params). kind "moe" = full layer, "route" = router only.
@@ -50,10 +51,26 @@ CASES = {
                                  layer=5)),
     "block_ragged_fp32": ("block", dict(seed=8, B=2, S=40, d=24, E=4, h=20, C=1.5, mode="fp32",
                                         layer=3)),
+    # the denoising-step stack (MoEDiT.forward, backbone.py:548-619), SURVEY 8(d)
+    # cfg1 block variant: 3 dense + 1 MoE layer, d=256, GQA 4:1, text context
+    "dit_cfg1": ("dit", dict(seed=9, B=2, H=32, W=32, stage="S256", mod_seed=11,
+                             model=dict(n_layers=4, d_model=256, n_q_heads=4, n_kv_heads=1,
+                                        head_dim=64, n_experts=8, expert_hidden=168,
+                                        dense_layers=3, latent_channels=16, patch=2,
+                                        capacity_override=2.0, dtype="float32", seed=0))),
+    # 2 MoE layers on the stage schedule (S256: C=8), GQA 2:1, ragged prompts
+    "dit_small": ("dit", dict(seed=10, B=3, H=16, W=16, stage="S256", mod_seed=12,
+                              model=dict(n_layers=5, d_model=128, n_q_heads=4, n_kv_heads=2,
+                                         head_dim=32, n_experts=4, expert_hidden=64,
+                                         dense_layers=3, latent_channels=4, patch=2,
+                                         dtype="float32", seed=3))),
 }
 
 
 def inputs_for(kind, p):
+    if kind == "dit":
+        z, t = dit_inputs(p)
+        return {"z": z, "t": t}
     if kind == "block":
         return make_block_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"], mode=p["mode"])
     if kind == "moe":
@@ -90,7 +107,35 @@ def run_reference_block(ref, p, inp):
             "gates": routing["gates"].data, "capacity": np.int64(routing["capacity"])}
 
 
+def dit_inputs(p):
+    return make_latent(p["seed"], p["B"], p["model"]["latent_channels"], p["H"], p["W"])
+
+
+def run_reference_dit(p):
+    """MoEDiT.forward (backbone.py:548-619) of the reference, modulation
+    perturbed so the blocks are not identities."""
+    import importlib
+    bb = importlib.import_module("nimg_ref.backbone")
+    rt = importlib.import_module("nimg_ref.router")
+    nt = importlib.import_module("nimg_ref.tensor")
+    cfg = bb.ModelConfig(**p["model"])
+    model = bb.MoEDiT(cfg)
+    params = {k: v.data for k, v in model.named_parameters().items()}
+    perturb_modulation(params, p["mod_seed"])
+    z, t = dit_inputs(p)
+    ctx = model.precompute_text_kv(list(DIT_PROMPTS[:p["B"]]))
+    with nt.no_grad():
+        vel, aux = model.forward(nt.Tensor(z, dtype=np.float32), t, ctx, rt.StageId[p["stage"]])
+    res = {"vel": vel.data, "param_digest": np.array(digest(params))}
+    for j, (layer, decs) in enumerate(aux["decisions"]):
+        res[f"logits_{layer}"] = aux["router_logits"][j].data
+        res[f"top_{layer}"] = np.stack([dd.top_indices for dd in decs])
+    return res
+
+
 def run_reference(ref, kind, p, inp):
+    if kind == "dit":
+        return run_reference_dit(p)
     if kind == "block":
         return run_reference_block(ref, p, inp)
     T = ref.tensor.Tensor
@@ -127,8 +172,12 @@ def run_reference(ref, kind, p, inp):
 
 def main():
     ref = load_reference()
-    manifest = {}
+    only = set(sys.argv[1:])
+    mpath = os.path.join(HERE, "manifest.json")
+    manifest = json.load(open(mpath)) if only and os.path.exists(mpath) else {}
     for name, (kind, p) in CASES.items():
+        if only and name not in only:
+            continue
         inp = inputs_for(kind, p)
         res = run_reference(ref, kind, p, inp)
         res["input_digest"] = np.array(digest(inp))

@@ -8,7 +8,8 @@ import os
 
 import numpy as np
 
-from oracle.workloads import digest, make_block_inputs, make_layer_inputs, make_router_inputs
+from oracle.workloads import (digest, make_block_inputs, make_latent, make_layer_inputs,
+                              make_router_inputs)
 
 GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
@@ -22,7 +23,10 @@ def case(name: str):
     """Returns (kind, params, inputs, expected) for a golden case."""
     m = manifest()[name]
     kind, p = m["kind"], m["params"]
-    if kind == "block":
+    if kind == "dit":
+        z, t = make_latent(p["seed"], p["B"], p["model"]["latent_channels"], p["H"], p["W"])
+        inp = {"z": z, "t": t}
+    elif kind == "block":
         inp = make_block_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"], mode=p["mode"])
     elif kind == "moe":
         inp = make_layer_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"],
