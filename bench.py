@@ -322,6 +322,79 @@ def run_single(args, c, peaks, peak_kind):
     print(json.dumps(line), flush=True)
 
 
+def run_stack(args, peaks, peak_kind):
+    """one denoising step of the full
+    Nucleus-Image stack (dit.MoEDiT: 3 dense + 29 MoE blocks, d=2048, GQA
+    16/4) at the 1024px stage (S=4096 image tokens per sample, per-layer C:
+    4 for layers 3-4, 2 for 5-31), bf16, random weights, 256-token text
+    context precomputed once (as the reference does per prompt set)."""
+    import torch
+    from paper_2604_12163_b200 import dit as D
+    from paper_2604_12163_b200.router import StageId
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    B = args.batch or 4
+    cfg = D.ModelConfig(**D.NUCLEUS_IMAGE)
+    model = D.MoEDiT(cfg, D.random_parameters(cfg, dev), compute_dtype=torch.bfloat16)
+    prompt = " ".join(f"tok{i}" for i in range(256))
+    ctx = model.precompute_text_kv([prompt] * B)
+    lat = 1024 // 8
+    g = torch.Generator(device=dev).manual_seed(5)
+    z = torch.randn(B, cfg.latent_channels, lat, lat, generator=g, device=dev)
+    t = __import__("numpy").linspace(0.2, 0.8, B)
+    step = lambda: model.forward(z, t, ctx, StageId.S1024, return_aux=False)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    clk = ClockSampler(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    # phase split: events around the library calls (one extra step)
+    spans = {"moe_blocks": [], "dense_ffn": []}
+    be = model.backend
+    orig = {"moe_blocks": be.moe_block, "dense_ffn": be.dense_ffn}
+
+    def wrap(kind):
+        def f(*a, **k):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+            ev[0].record()
+            r = orig[kind](*a, **k)
+            ev[1].record()
+            spans[kind].append(ev)
+            return r
+        return f
+    be.moe_block, be.dense_ffn = wrap("moe_blocks"), wrap("dense_ffn")
+    step()
+    torch.cuda.synchronize()
+    be.moe_block, be.dense_ffn = orig["moe_blocks"], orig["dense_ffn"]
+    split = {k: sum(a.elapsed_time(b) for a, b in v) for k, v in spans.items()}
+    split["attention_and_rest"] = ms - split["moe_blocks"] - split["dense_ffn"]
+    T = B * 4096
+    moe_flops = sum(6.0 * cfg.d_model * cfg.expert_hidden * (
+        cfg.n_experts * B * min(math.ceil(model.capacity_factor_for(i, StageId.S1024) * 4096 /
+                                          cfg.n_experts), 4096) + T)
+        for i in range(cfg.dense_layers, cfg.n_layers))
+    line = {
+        "metric": "Denoising-step stack tokens/s (Nucleus-Image, 1024px stage)",
+        "value": T / (ms * 1e-3), "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random latent, random weights)",
+        "config": {"workload": f"cfg5: MoEDiT 32 layers (3 dense + 29 MoE) d=2048 GQA 16/4 "
+                               f"E=64 h=1344 S=4096 B={B} text 256 tokens, C 4/2 per layer",
+                   "parallelism": "single GPU", "l2": "inputs larger than L2 (31 GB weights)"},
+        "phase_ms": split,
+        "moe_expert_gemm_tflops_in_blocks": moe_flops / (split["moe_blocks"] * 1e-3) / 1e12,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def run_block(args, c, inp, cfg, bank, layer_ms):
     """block.moe_block_forward (backbone.py:583-606) on the same shapes."""
     import torch
@@ -591,7 +664,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=None, choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS) + ["cfg5"])
     ap.add_argument("--capacity", type=float, default=None,
                     help="override the config's capacity factor C (cfg3 sweep: 8, 4, 2)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
@@ -607,6 +680,13 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.config == "cfg5":
+        if args.impl == "reference" or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+            print(json.dumps({"impl": args.impl, "unavailable": "cfg5 stack: 1 GPU, ours only"}))
+            return
+        peaks, kind = load_peaks()
+        run_stack(args, peaks, kind)
+        return
     c = dict(CONFIGS[args.config or "cfg2"])
     if args.batch:
         c["B"] = args.batch

@@ -168,6 +168,30 @@ int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_d
                  const void* y_routed, const void* y_shared, const float* gates,
                  const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream);
 
+/* ------------------------------------------------------------------ denoising-step stack
+ * Fused element-wise chains around attention and the dense FFN of the
+ * backbone (backbone.py:42-121, :128-182, tensor.py:518-531), used by the
+ * stack (dit.py) in fp32 / bf16. Rows are (B*S) tokens of width d; per-sample
+ * vectors are (B, d) fp32; th = tanh(gate). d * elt must be a multiple of 16 B,
+ * pointers 16-B aligned. */
+/* out = LayerNorm(x) * (1 + scale[b]) (+ shift[b] if shift != NULL) */
+int nimg_ln_modulate(int64_t rows, int64_t S, int64_t d, int32_t dtype, const void* x,
+                     const float* scale, const float* shift, void* out, float eps, void* stream);
+/* h = x + th[b] * r; m = LayerNorm(h) * (1 + scale[b]) */
+int nimg_gate_res_ln_modulate(int64_t rows, int64_t S, int64_t d, int32_t dtype, const void* x,
+                              const void* r, const float* th, const float* scale, void* h_out,
+                              void* m_out, float eps, void* stream);
+/* out = x + th[b] * r */
+int nimg_gated_residual(int64_t rows, int64_t S, int64_t d, int32_t dtype, const void* x,
+                        const void* r, const float* th, void* out, void* stream);
+/* per (token, head) row of dh: RMSNorm then the 2-axis rotary rotation with
+ * per-position tables cos_t / sin_t (S, dh) fp32; rows = B*S*H. Token t's
+ * heads start at x + t * x_token_stride elements (a slice of a fused QKV
+ * projection); out is contiguous (rows, dh). */
+int nimg_qk_norm_rope(int64_t rows, int64_t S, int64_t H, int64_t dh, int32_t dtype, const void* x,
+                      int64_t x_token_stride, const float* cos_t, const float* sin_t, void* out,
+                      float eps, void* stream);
+
 /* ------------------------------------------------------------------ expert-parallel transport
  * Copy-engine exchange over NVLink (no SMs, so transfers overlap the persistent
  * GEMMs). Setup-time: peer-writable buffers shared between the ranks of one

@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnimg_moe.so")
 SOURCES = ["capi.cu", "route_kernels.cu", "grouped_gemm_sm100.cu", "grouped_gemm_simt.cu",
-           "block_kernels.cu"]
+           "block_kernels.cu", "stack_kernels.cu"]
 HEADERS = ["common.cuh", "nimg_internal.h", os.path.join("..", "..", "include", "nimg_moe.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -25,6 +25,7 @@ EXPORTS = (
     "nimg_combine", "nimg_profile_events", "nimg_ipc_alloc", "nimg_ipc_open", "nimg_ipc_close",
     "nimg_free", "nimg_copy_async", "nimg_stream_write_u32", "nimg_stream_wait_geq_u32",
     "nimg_moe_block_workspace_bytes", "nimg_moe_block_forward",
+    "nimg_ln_modulate", "nimg_gate_res_ln_modulate", "nimg_gated_residual", "nimg_qk_norm_rope",
 )
 
 
@@ -96,6 +97,11 @@ def _load():
         "nimg_moe_block_workspace_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
         "nimg_moe_block_forward": ([C.POINTER(MoeDesc), C.POINTER(BlockPtrs), I32, P, SZ, P],
                                    C.c_int),
+        "nimg_ln_modulate": ([I64, I64, I64, I32, P, P, P, P, C.c_float, P], C.c_int),
+        "nimg_gate_res_ln_modulate": ([I64, I64, I64, I32, P, P, P, P, P, P, C.c_float, P],
+                                      C.c_int),
+        "nimg_gated_residual": ([I64, I64, I64, I32, P, P, P, P, P], C.c_int),
+        "nimg_qk_norm_rope": ([I64, I64, I64, I64, I32, P, I64, P, P, P, C.c_float, P], C.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

@@ -500,6 +500,56 @@ int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_d
   return NIMG_OK;
 }
 
+// ---------------------------------------------------------------- stack helpers
+static int check_rows(int64_t rows, int64_t S, int64_t d, int32_t dt, const void* const* ptrs, int n) {
+  if (rows < 0 || S < 1 || d < 1 || rows % S) return fail(NIMG_ERR_SHAPE, "bad row geometry");
+  if (dt != NIMG_BF16 && dt != NIMG_F32) return fail(NIMG_ERR_CONFIG, "unsupported dtype %d", dt);
+  if (d % (dt == NIMG_BF16 ? 8 : 4)) return fail(NIMG_ERR_SHAPE, "d %lld not a multiple of 16 bytes", (long long)d);
+  for (int i = 0; i < n; ++i)
+    if (!ptrs[i] || !aligned16(ptrs[i])) return fail(NIMG_ERR_SHAPE, "null or misaligned pointer");
+  return NIMG_OK;
+}
+
+int nimg_ln_modulate(int64_t rows, int64_t S, int64_t d, int32_t dtype, const void* x,
+                     const float* scale, const float* shift, void* out, float eps, void* stream) {
+  const void* p[] = {x, scale, out};
+  NIMG_TRY(check_rows(rows, S, d, dtype, p, 3));
+  CUDA_TRY(launch_row_modulate(0, dtype == NIMG_BF16, x, nullptr, nullptr, scale, shift, nullptr,
+                               out, rows, (int)S, (int)d, eps, (cudaStream_t)stream));
+  return NIMG_OK;
+}
+
+int nimg_gate_res_ln_modulate(int64_t rows, int64_t S, int64_t d, int32_t dtype, const void* x,
+                              const void* r, const float* th, const float* scale, void* h_out,
+                              void* m_out, float eps, void* stream) {
+  const void* p[] = {x, r, th, scale, h_out, m_out};
+  NIMG_TRY(check_rows(rows, S, d, dtype, p, 6));
+  CUDA_TRY(launch_row_modulate(1, dtype == NIMG_BF16, x, r, th, scale, nullptr, h_out, m_out, rows,
+                               (int)S, (int)d, eps, (cudaStream_t)stream));
+  return NIMG_OK;
+}
+
+int nimg_gated_residual(int64_t rows, int64_t S, int64_t d, int32_t dtype, const void* x,
+                        const void* r, const float* th, void* out, void* stream) {
+  const void* p[] = {x, r, th, out};
+  NIMG_TRY(check_rows(rows, S, d, dtype, p, 4));
+  CUDA_TRY(launch_row_modulate(2, dtype == NIMG_BF16, x, r, th, nullptr, nullptr, out, nullptr, rows,
+                               (int)S, (int)d, 0.f, (cudaStream_t)stream));
+  return NIMG_OK;
+}
+
+int nimg_qk_norm_rope(int64_t rows, int64_t S, int64_t H, int64_t dh, int32_t dtype, const void* x,
+                      int64_t x_token_stride, const float* cos_t, const float* sin_t, void* out,
+                      float eps, void* stream) {
+  if (rows < 0 || S < 1 || H < 1 || dh < 2 || dh % 2 || rows % (S * H) || x_token_stride < H * dh)
+    return fail(NIMG_ERR_SHAPE, "bad head geometry");
+  if (dtype != NIMG_BF16 && dtype != NIMG_F32) return fail(NIMG_ERR_CONFIG, "unsupported dtype %d", dtype);
+  if (!x || !cos_t || !sin_t || !out) return fail(NIMG_ERR_SHAPE, "null pointer");
+  CUDA_TRY(launch_qk_norm_rope(dtype == NIMG_BF16, x, x_token_stride, cos_t, sin_t, out, rows, (int)S,
+                               (int)H, (int)dh, eps, (cudaStream_t)stream));
+  return NIMG_OK;
+}
+
 int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   NIMG_TRY(check_moe_desc(d));
   if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");

@@ -127,4 +127,13 @@ cudaError_t launch_block_prologue(bool bf, const void* x, const void* r_attn, co
                                   const float* th_sa_f, const float* onep, void* h, void* xn,
                                   void* xm, int64_t T, int S, int d, float scale_t, cudaStream_t s);
 
+// denoising-step stack helpers (stack_kernels.cu). mode 0: m = LN(x)(1+scale)
+// (+ shift); 1: h = x + th*r, m = LN(h)(1+scale); 2: h = x + th*r.
+cudaError_t launch_row_modulate(int mode, bool bf, const void* x, const void* r, const float* th,
+                                const float* scale, const float* shift, void* h, void* m,
+                                int64_t rows, int S, int d, float eps, cudaStream_t s);
+cudaError_t launch_qk_norm_rope(bool bf, const void* x, int64_t xs, const float* cs, const float* sn,
+                                void* out, int64_t rows, int S, int H, int dh, float eps,
+                                cudaStream_t s);
+
 }  // namespace nimg

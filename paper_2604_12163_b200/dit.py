@@ -45,7 +45,8 @@ from .moe import ExpertBank, bank_on_device
 from .router import DENSE, RouterConfig, StageId, capacity_schedule
 
 __all__ = ["ModelConfig", "NUCLEUS_IMAGE", "MoEDiT", "TextContext", "CudaBackend",
-           "init_parameters", "encode_prompt", "hash_token_embedding", "trunc_normal"]
+           "init_parameters", "random_parameters", "encode_prompt", "hash_token_embedding",
+           "trunc_normal"]
 
 
 @dataclass
@@ -146,6 +147,46 @@ def init_parameters(cfg: ModelConfig) -> dict[str, np.ndarray]:
     return p
 
 
+def random_parameters(cfg: ModelConfig, device, expert_dtype=torch.bfloat16, seed: int = 0):
+    """Device-side random init with the reference's distributions (trunc
+    normal 0.02, router 0.006, zero biases; modulation N(0, 0.02) instead of
+    zero so the blocks are not identities) for full-size benchmarking, where
+    the numpy draw of init_parameters would take minutes. Expert and dense
+    FFN matrices are created in `expert_dtype`."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    dt = torch.float64 if cfg.dtype == "float64" else torch.float32
+
+    def tn(shape, std=0.02, dtype=dt):
+        out = torch.empty(shape, device=device, dtype=torch.float32)
+        out.normal_(0.0, std, generator=g).clamp_(-2 * std, 2 * std)
+        return out.to(dtype)
+    shapes = {k: v.shape for k, v in init_parameters(
+        ModelConfig(**{**cfg.__dict__, "n_layers": 0})).items()}
+    p = {k: (tn(s) if k.endswith(("weight",)) and not k.startswith("final_mod")
+             else torch.zeros(s, device=device, dtype=dt)) for k, s in shapes.items()}
+    d, kv = cfg.d_model, cfg.n_kv_heads * cfg.head_dim
+    p["final_mod.weight"] = tn((d, 2 * d))
+    for i in range(cfg.n_layers):
+        pre = f"blocks.{i}"
+        for name, shape in (("wq", (d, d)), ("wk", (d, kv)), ("wv", (d, kv)), ("wo", (d, d)),
+                            ("wk_txt", (d, kv)), ("wv_txt", (d, kv))):
+            p[f"{pre}.attn.{name}"] = tn(shape)
+        p[f"{pre}.img_mod.weight"] = tn((d, 5 * d))
+        p[f"{pre}.img_mod.bias"] = torch.zeros(5 * d, device=device, dtype=dt)
+        if i < cfg.dense_layers:
+            h = cfg.dense_hidden
+            for name, shape in (("w1", (h, d)), ("w3", (h, d)), ("w2", (d, h))):
+                p[f"{pre}.ffn.{name}"] = tn(shape, dtype=expert_dtype)
+        else:
+            E, h, hs = cfg.n_experts, cfg.expert_hidden, cfg.shared_hidden
+            p[f"{pre}.router.gate"] = tn((2 * d, E), 0.006)
+            for name, shape in (("w1", (E, h, d)), ("w3", (E, h, d)), ("w2", (E, d, h)),
+                                ("shared_w1", (hs, d)), ("shared_w3", (hs, d)),
+                                ("shared_w2", (d, hs))):
+                p[f"{pre}.moe.{name}"] = tn(shape, dtype=expert_dtype)
+    return p
+
+
 # ---------------------------------------------------------------- text encoder
 def hash_token_embedding(token: str, dim: int) -> np.ndarray:
     """backbone.py:299-303: deterministic per-token embedding from sha256."""
@@ -170,6 +211,7 @@ class TextContext:
     mask: torch.Tensor            # (B, S_t) bool, True = valid token
     s_t: int
     prompts: tuple = ()
+    all_valid: bool = True        # no padding: attention needs no mask
 
 
 # ---------------------------------------------------------------- backends
@@ -206,6 +248,51 @@ class CudaBackend:
         return moe_block_forward(x.to(self.act).contiguous(), sa_gate.to(f32), r_attn.to(self.act),
                                  ff_scale.to(f32), ff_gate.to(f32), t_vec.to(f32), layer, rcfg,
                                  bank, w_r, return_routing=return_routing)
+
+
+class _StackKernels:
+    """The fused element-wise chains (csrc/stack_kernels.cu) for fp32 / bf16."""
+
+    def __init__(self, act: torch.dtype):
+        from . import _lib
+        from ._tensors import nimg_dtype
+        self.L, self.dt, self.act = _lib, nimg_dtype(act), act
+
+    def _s(self):
+        return torch.cuda.current_stream().cuda_stream
+
+    def ln_mod(self, x, scale, shift=None, eps=1e-6):
+        B, S, d = x.shape
+        out = torch.empty_like(x)
+        self.L.check(self.L.lib.nimg_ln_modulate(B * S, S, d, self.dt, x.data_ptr(),
+                                                 scale.data_ptr(),
+                                                 None if shift is None else shift.data_ptr(),
+                                                 out.data_ptr(), eps, self._s()))
+        return out
+
+    def gate_res_ln(self, x, th, r, scale, eps=1e-6):
+        B, S, d = x.shape
+        h, m = torch.empty_like(x), torch.empty_like(x)
+        self.L.check(self.L.lib.nimg_gate_res_ln_modulate(B * S, S, d, self.dt, x.data_ptr(),
+                                                          r.data_ptr(), th.data_ptr(),
+                                                          scale.data_ptr(), h.data_ptr(),
+                                                          m.data_ptr(), eps, self._s()))
+        return h, m
+
+    def gated_res(self, x, th, r):
+        B, S, d = x.shape
+        out = torch.empty_like(x)
+        self.L.check(self.L.lib.nimg_gated_residual(B * S, S, d, self.dt, x.data_ptr(),
+                                                    r.data_ptr(), th.data_ptr(), out.data_ptr(),
+                                                    self._s()))
+        return out
+
+    def qk_norm_rope(self, x, token_stride, B, S, H, dh, cos, sin, eps=1e-6):
+        out = torch.empty((B, S, H, dh), dtype=self.act, device=x.device)
+        self.L.check(self.L.lib.nimg_qk_norm_rope(B * S * H, S, H, dh, self.dt, x.data_ptr(),
+                                                  token_stride, cos.data_ptr(), sin.data_ptr(),
+                                                  out.data_ptr(), eps, self._s()))
+        return out
 
 
 # ---------------------------------------------------------------- model
@@ -256,13 +343,28 @@ class MoEDiT:
         params = init_parameters(cfg) if params is None else params
         t = lambda a, dt: torch.as_tensor(np.asarray(a) if not isinstance(a, torch.Tensor) else a
                                           ).to(self.dev, dt).contiguous()
-        self.params = {k: t(v, self.store) for k, v in params.items()}
+        # expert / dense-FFN matrices stay in the dtype given (a bf16 bank is
+        # used in place); everything else is held in the storage dtype
+        big = lambda k: ".moe." in k or ".ffn." in k
+        self.params = {k: (t(v, v.dtype) if big(k) and isinstance(v, torch.Tensor) else
+                           t(v, self.store)) for k, v in params.items()}
         P, cd = self.params, compute_dtype
         # working copies: attention / embeddings in compute dtype, modulation in f64
         self.w = {k: v.to(cd) for k, v in P.items()
                   if ".attn." in k or k.startswith(("patch_embed", "final_proj"))}
-        self.f64 = {k: v.double() for k, v in P.items()
-                    if k.startswith("time_embed") or "mod." in k}
+        self.f64 = {k: v.double() for k, v in P.items() if k.startswith("time_embed")}
+        # modulation in f64 only for the f64 pin; fp32 otherwise (B x d x 5d)
+        self.mdt = torch.float64 if compute_dtype == torch.float64 else torch.float32
+        self.modw = {k: v.to(self.mdt) for k, v in P.items() if "mod." in k}
+        # fused element-wise kernels for fp32 / bf16 on CUDA, one QKV GEMM
+        self.fast = (compute_dtype in (torch.float32, torch.bfloat16) and self.dev.type == "cuda"
+                     and cfg.d_model % 8 == 0)
+        self.K = _StackKernels(compute_dtype) if self.fast else None
+        if self.fast:
+            for i in range(cfg.n_layers):
+                pre = f"blocks.{i}.attn"
+                self.w[f"{pre}.wqkv"] = torch.cat([self.w[f"{pre}.wq"], self.w[f"{pre}.wk"],
+                                                   self.w[f"{pre}.wv"]], dim=1).contiguous()
         self.banks, self.dense = {}, {}
         for i in range(cfg.n_layers):
             pre = f"blocks.{i}"
@@ -283,12 +385,13 @@ class MoEDiT:
         return {i: self.params[f"blocks.{i}.router.gate"] for i in self.banks}
 
     # ---- helpers
-    def _rope(self, pos_h, pos_w, d_h: int):
-        key = (tuple(np.asarray(pos_h).tolist()), tuple(np.asarray(pos_w).tolist()), d_h)
+    def _rope(self, pos_h, pos_w, d_h: int, dtype=None):
+        dtype = self.cd if dtype is None else dtype
+        key = (tuple(np.asarray(pos_h).tolist()), tuple(np.asarray(pos_w).tolist()), d_h, dtype)
         if key not in self._rope_cache:
             c, s = _rope_tables(pos_h, pos_w, d_h)
-            self._rope_cache[key] = (torch.from_numpy(c).to(self.dev, self.cd),
-                                     torch.from_numpy(s).to(self.dev, self.cd))
+            self._rope_cache[key] = (torch.from_numpy(c).to(self.dev, dtype).contiguous(),
+                                     torch.from_numpy(s).to(self.dev, dtype).contiguous())
         return self._rope_cache[key]
 
     def _apply_rope(self, x: torch.Tensor, pos_h, pos_w) -> torch.Tensor:
@@ -317,7 +420,7 @@ class MoEDiT:
             cmat[b, :e.shape[0]] = e
         mask_t = torch.from_numpy(mask).to(self.dev)
         if s_t == 0:
-            return TextContext([], [], mask_t, 0, tuple(prompts))
+            return TextContext([], [], mask_t, 0, tuple(prompts), True)
         c = torch.from_numpy(cmat).to(self.dev, self.store).to(self.cd)
         # projections and the K RMSNorm of storage-dtype operands round to the
         # storage dtype; RoPE's f64 tables promote K (backbone.py:505-512)
@@ -331,7 +434,7 @@ class MoEDiT:
             ks.append(self._apply_rope(rd(_rmsnorm(k)), pos_h, pos_w))
             vs.append(rd(self._linear(c, self.w[f"{pre}.wv_txt"])).view(B, s_t, cfg.n_kv_heads,
                                                                          cfg.head_dim))
-        return TextContext(ks, vs, mask_t, s_t, tuple(prompts))
+        return TextContext(ks, vs, mask_t, s_t, tuple(prompts), bool(mask.all()))
 
     # ---- layout
     def patchify(self, z: torch.Tensor):
@@ -383,6 +486,8 @@ class MoEDiT:
         cfg = self.cfg
         B, S, _ = a_in.shape
         pre = f"blocks.{i}.attn"
+        if self.fast:
+            return self._attention_fast(i, a_in, ctx, pos_h, pos_w)
         q = self._linear(a_in, self.w[f"{pre}.wq"]).view(B, S, cfg.n_q_heads, cfg.head_dim)
         k = self._linear(a_in, self.w[f"{pre}.wk"]).view(B, S, cfg.n_kv_heads, cfg.head_dim)
         v = self._linear(a_in, self.w[f"{pre}.wv"]).view(B, S, cfg.n_kv_heads, cfg.head_dim)
@@ -402,6 +507,33 @@ class MoEDiT:
                                              scale=1.0 / math.sqrt(cfg.head_dim))
         return self._linear(out.transpose(1, 2).reshape(B, S, cfg.d_model), self.w[f"{pre}.wo"])
 
+    def _attention_fast(self, i, a_in, ctx, pos_h, pos_w):
+        """One QKV GEMM, fused QK-RMSNorm + RoPE kernel, cuDNN SDPA with native
+        GQA (no mask unless the text context has padding)."""
+        cfg = self.cfg
+        B, S, d = a_in.shape
+        Hq, Hkv, dh = cfg.n_q_heads, cfg.n_kv_heads, cfg.head_dim
+        kv = Hkv * dh
+        pre = f"blocks.{i}.attn"
+        qkv = a_in @ self.w[f"{pre}.wqkv"]                       # (B, S, d + 2 kv)
+        cos, sin = self._rope(pos_h, pos_w, dh, torch.float32)
+        ld = d + 2 * kv
+        q = self.K.qk_norm_rope(qkv, ld, B, S, Hq, dh, cos, sin)
+        k = self.K.qk_norm_rope(qkv[..., d:], ld, B, S, Hkv, dh, cos, sin)
+        v = qkv[..., d + kv:].view(B, S, Hkv, dh)
+        mask = None
+        if ctx is not None and ctx.s_t > 0:
+            k = torch.cat([k, ctx.k_txt[i].to(k.dtype)], dim=1)
+            v = torch.cat([v, ctx.v_txt[i].to(v.dtype)], dim=1)
+            if not ctx.all_valid:
+                valid = torch.cat([torch.ones((B, S), dtype=torch.bool, device=self.dev),
+                                   ctx.mask], 1)
+                mask = valid[:, None, None, :]
+        out = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2),
+                                             v.transpose(1, 2), attn_mask=mask,
+                                             scale=1.0 / math.sqrt(dh), enable_gqa=True)
+        return out.transpose(1, 2).reshape(B, S, d) @ self.w[f"{pre}.wo"]
+
     def forward(self, z_t, t, ctx: TextContext | None, stage: StageId,
                 capture_step: int | None = None, return_aux: bool = True):
         """backbone.py:548-619. Returns (velocity, aux); aux has the per-MoE-
@@ -419,14 +551,25 @@ class MoEDiT:
         pos_w = np.tile(np.arange(gw), gh)
         d = cfg.d_model
         aux = {"router_logits": [], "decisions": [], "records": []}
+        K = self.K
+        t_m = t_vec.to(self.mdt)
         for i in range(cfg.n_layers):
             pre = f"blocks.{i}"
-            mod = t_vec @ self.f64[f"{pre}.img_mod.weight"] + self.f64[f"{pre}.img_mod.bias"]
+            mod = t_m @ self.modw[f"{pre}.img_mod.weight"] + self.modw[f"{pre}.img_mod.bias"]
             sa_shift, sa_scale, sa_gate, ff_scale, ff_gate = (mod[:, j * d:(j + 1) * d]
                                                               for j in range(5))
-            a_in = (_ln_scale(x, sa_scale).to(cd) + sa_shift.to(cd)[:, None, :])
+            if self.fast:
+                a_in = K.ln_mod(x, sa_scale.float().contiguous(), sa_shift.float().contiguous())
+            else:
+                a_in = (_ln_scale(x, sa_scale).to(cd) + sa_shift.to(cd)[:, None, :])
             r_attn = self._attention(i, a_in, ctx, pos_h, pos_w)
-            if i in self.dense:
+            if i in self.dense and self.fast:
+                h, f_in = K.gate_res_ln(x, torch.tanh(sa_gate).float().contiguous(), r_attn,
+                                        ff_scale.float().contiguous())
+                f_out = self.backend.dense_ffn(f_in.reshape(B * gh * gw, d), *self.dense[i])
+                x = K.gated_res(h, torch.tanh(ff_gate).float().contiguous(),
+                                f_out.to(cd).view(B, gh * gw, d))
+            elif i in self.dense:
                 # fused_gate_res_ln_scale (backbone.py:91-121, :577-580)
                 h = x + torch.tanh(sa_gate).to(cd)[:, None, :] * r_attn
                 f_in = _ln_scale(h, ff_scale)
@@ -452,9 +595,12 @@ class MoEDiT:
                 else:
                     out = res
                 x = out.to(cd)
-        fmod = t_vec @ self.f64["final_mod.weight"] + self.f64["final_mod.bias"]
+        fmod = t_m @ self.modw["final_mod.weight"] + self.modw["final_mod.bias"]
         f_shift, f_scale = fmod[:, :d], fmod[:, d:]
-        y = _ln_scale(x, f_scale).to(cd) + f_shift.to(cd)[:, None, :]
+        if self.fast:
+            y = K.ln_mod(x, f_scale.float().contiguous(), f_shift.float().contiguous())
+        else:
+            y = _ln_scale(x, f_scale).to(cd) + f_shift.to(cd)[:, None, :]
         out = y @ self.w["final_proj.weight"] + self.w["final_proj.bias"]
         vel = self.unpatchify(out, (gh, gw), tuple(z.shape))
         return vel, aux
