@@ -168,6 +168,22 @@ int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_d
                  const void* y_routed, const void* y_shared, const float* gates,
                  const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream);
 
+/* backbone.py:584-589 alone (the expert-parallel block runs the layer between
+ * this and nimg_combine_residual): h, x_norm, x_mod exactly as
+ * nimg_moe_block_forward computes them, and th_ff = tanh(ff_gate) (B, d) in
+ * the combine epilogue's precision (double for an fp32 layer, float for bf16). */
+int nimg_moe_block_prologue_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
+int nimg_moe_block_prologue(const nimg_moe_desc* desc, const void* x, const void* r_attn,
+                            const float* sa_gate, const float* ff_scale, const float* ff_gate,
+                            int32_t layer, void* h, void* x_norm, void* x_mod, void* th_ff, void* ws,
+                            size_t ws_bytes, void* stream);
+/* nimg_combine with backbone.py:606 in its epilogue:
+ * out[t] = h[t] + th_ff[t / S] * combined[t] (th_ff from nimg_moe_block_prologue). */
+int nimg_combine_residual(int64_t T, int64_t d, int64_t E, int64_t S, int32_t y_dtype,
+                          int32_t out_dtype, const void* y_routed, const void* y_shared,
+                          const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
+                          const void* hres, const void* th_ff, void* out, void* stream);
+
 /* ------------------------------------------------------------------ denoising-step stack
  * Fused element-wise chains around attention and the dense FFN of the
  * backbone (backbone.py:42-121, :128-182, tensor.py:518-531), used by the

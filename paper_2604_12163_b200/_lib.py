@@ -26,6 +26,7 @@ EXPORTS = (
     "nimg_free", "nimg_copy_async", "nimg_stream_write_u32", "nimg_stream_wait_geq_u32",
     "nimg_moe_block_workspace_bytes", "nimg_moe_block_forward",
     "nimg_ln_modulate", "nimg_gate_res_ln_modulate", "nimg_gated_residual", "nimg_qk_norm_rope",
+    "nimg_moe_block_prologue_workspace_bytes", "nimg_moe_block_prologue", "nimg_combine_residual",
 )
 
 
@@ -98,6 +99,11 @@ def _load():
         "nimg_moe_block_forward": ([C.POINTER(MoeDesc), C.POINTER(BlockPtrs), I32, P, SZ, P],
                                    C.c_int),
         "nimg_ln_modulate": ([I64, I64, I64, I32, P, P, P, P, C.c_float, P], C.c_int),
+        "nimg_moe_block_prologue_workspace_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
+        "nimg_moe_block_prologue": ([C.POINTER(MoeDesc), P, P, P, P, P, I32, P, P, P, P, P, SZ, P],
+                                    C.c_int),
+        "nimg_combine_residual": ([I64, I64, I64, I64, I32, I32, P, P, P, P, P, P, P, P, P],
+                                  C.c_int),
         "nimg_gate_res_ln_modulate": ([I64, I64, I64, I32, P, P, P, P, P, P, C.c_float, P],
                                       C.c_int),
         "nimg_gated_residual": ([I64, I64, I64, I32, P, P, P, P, P], C.c_int),

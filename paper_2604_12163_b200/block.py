@@ -27,7 +27,7 @@ from .errors import ConfigError, ShapeError
 from .moe import ExpertBank, _check_bank_shapes, bank_on_device
 from .router import RouterConfig, alloc_route_out, build_routing, capacity_for, make_desc, route_struct
 
-__all__ = ["moe_block_forward"]
+__all__ = ["moe_block_forward", "moe_block_prologue"]
 
 
 def moe_block_forward(x, sa_gate, r_attn, ff_scale, ff_gate, t_vec, layer: int,
@@ -72,3 +72,35 @@ def moe_block_forward(x, sa_gate, r_attn, ff_scale, ff_gate, t_vec, layer: int,
     if return_intermediates:
         res.append({k: outs[k] for k in ("h", "x_norm", "x_mod")})
     return res[0] if len(res) == 1 else tuple(res)
+
+
+def moe_block_prologue(x, sa_gate, r_attn, ff_scale, ff_gate, layer: int, cfg: RouterConfig):
+    """backbone.py:584-589 alone, with the kernels moe_block_forward uses:
+    returns (h, x_norm, x_mod, th_ff) where th_ff = tanh(ff_gate) in the
+    precision of the combine epilogue (f64 for fp32 activations, fp32 for
+    bf16). The expert-parallel block (ep.ep_moe_block_forward) runs the layer
+    between this and a residual combine, so its output equals the 1-GPU block."""
+    xt = to_device(x)
+    act = xt.dtype
+    B, S, d = xt.shape
+    ra = to_device(r_attn, act)
+    if tuple(ra.shape) != (B, S, d):
+        raise ShapeError(f"r_attn shape {tuple(ra.shape)} != {(B, S, d)}")
+    mods = [to_device(m, torch.float32) for m in (sa_gate, ff_scale, ff_gate)]
+    for m in mods:
+        if tuple(m.shape) != (B, d):
+            raise ShapeError(f"modulation shape {tuple(m.shape)} != {(B, d)}")
+    if d != cfg.d_model:
+        raise ConfigError(f"width {d} != d_model {cfg.d_model}")
+    cap = capacity_for(S, cfg.n_experts, cfg.capacity_factor)
+    desc = make_desc(B, S, d, cfg.n_experts, cap, d, d, cfg, act)
+    nbytes = C.c_size_t()
+    _lib.check(_lib.lib.nimg_moe_block_prologue_workspace_bytes(C.byref(desc), C.byref(nbytes)))
+    ws = workspace(nbytes.value)
+    h, xn, xm = (torch.empty((B, S, d), dtype=act, device=xt.device) for _ in range(3))
+    th = torch.empty((B, d), dtype=torch.float64 if act == torch.float32 else torch.float32,
+                     device=xt.device)
+    _lib.check(_lib.lib.nimg_moe_block_prologue(C.byref(desc), ptr(xt), ptr(ra), *(ptr(m) for m in mods),
+                                                int(layer), ptr(h), ptr(xn), ptr(xm), ptr(th),
+                                                ptr(ws), ws.numel(), stream_handle()))
+    return h, xn, xm, th

@@ -659,6 +659,57 @@ int nimg_moe_block_forward(const nimg_moe_desc* d, const nimg_block_ptrs* b, int
                           bf ? (const void*)th_ff_f : (const void*)th_ff);
 }
 
+int nimg_moe_block_prologue_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");
+  *bytes = block_extra_bytes(d);
+  return NIMG_OK;
+}
+
+int nimg_moe_block_prologue(const nimg_moe_desc* d, const void* x, const void* r_attn,
+                            const float* sa_gate, const float* ff_scale, const float* ff_gate,
+                            int32_t layer, void* h, void* x_norm, void* x_mod, void* th_ff, void* ws,
+                            size_t ws_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  NIMG_TRY(check_moe_desc(d));
+  if (!x || !r_attn || !sa_gate || !ff_scale || !ff_gate || !h || !x_norm || !x_mod || !th_ff)
+    return fail(NIMG_ERR_SHAPE, "null block pointer");
+  if (layer < 0) return fail(NIMG_ERR_CONFIG, "layer must be >= 0");
+  if (!ws || ws_bytes < block_extra_bytes(d)) return fail(NIMG_ERR_CONFIG, "workspace too small");
+  const size_t bd = (size_t)d->B * d->d;
+  const bool bf = d->act_dtype == NIMG_BF16;
+  uint8_t* w = static_cast<uint8_t*>(ws);
+  double* th_sa = reinterpret_cast<double*>(w);          w += align_up(bd * 8);
+  double* th_ff_d = reinterpret_cast<double*>(w);        w += align_up(bd * 8);
+  float* onep = reinterpret_cast<float*>(w);             w += align_up(bd * 4);
+  float* th_sa_f = reinterpret_cast<float*>(w);          w += align_up(bd * 4);
+  float* th_ff_f = reinterpret_cast<float*>(w);
+  // th_ff lands in the caller's buffer in the precision of the combine epilogue
+  if (bf) th_ff_f = static_cast<float*>(th_ff);
+  else th_ff_d = static_cast<double*>(th_ff);
+  float scale_t = (float)(1.0 / std::sqrt((double)layer + 1.0));
+  if (bf) scale_t = __bfloat162float(__float2bfloat16_rn(scale_t));
+  CUDA_TRY(launch_block_modvec(sa_gate, ff_scale, ff_gate, th_sa, th_ff_d, onep, th_sa_f, th_ff_f,
+                               (int64_t)bd, st));
+  CUDA_TRY(launch_block_prologue(bf, x, r_attn, th_sa, th_sa_f, onep, h, x_norm, x_mod, d->B * d->S,
+                                 (int)d->S, (int)d->d, scale_t, st));
+  return NIMG_OK;
+}
+
+int nimg_combine_residual(int64_t T, int64_t d, int64_t E, int64_t S, int32_t y_dtype,
+                          int32_t out_dtype, const void* y_routed, const void* y_shared,
+                          const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
+                          const void* hres, const void* th_ff, void* out, void* stream) {
+  if (T < 0 || d < 1 || E < 1 || S < 1 || T % S) return fail(NIMG_ERR_SHAPE, "bad combine shape");
+  if (T == 0) return NIMG_OK;
+  if (!y_shared || !comb_cnt || !comb_rows || !out || !gates || !hres || !th_ff)
+    return fail(NIMG_ERR_SHAPE, "null pointer");
+  CUDA_TRY(launch_combine(y_dtype == NIMG_BF16, out_dtype == NIMG_BF16, y_routed, y_shared, gates,
+                          comb_rows, comb_cnt, out, T, (int)d, (int)E, (cudaStream_t)stream, hres,
+                          th_ff, (int)S));
+  return NIMG_OK;
+}
+
 int nimg_profile_events(void* const* events, int32_t n) {
   if (n < 0 || n > 8 || (n > 0 && !events)) return fail(NIMG_ERR_CONFIG, "bad event list");
   for (int i = 0; i < n; ++i) g_events[i] = (cudaEvent_t)events[i];

@@ -221,14 +221,18 @@ class CudaBackend:
 
     name = "cuda"
 
-    def __init__(self, act_dtype: torch.dtype = torch.bfloat16):
+    def __init__(self, act_dtype: torch.dtype = torch.bfloat16, ep=None):
         if act_dtype not in (torch.bfloat16, torch.float32):
             raise ConfigError(f"unsupported activation dtype {act_dtype}")
         self.act = act_dtype
+        self.ep = ep          # ep.EPContext: MoE blocks expert-parallel over its ranks
         from .stages import CudaStages
         self._stages = CudaStages()
 
     def prepare_bank(self, bank: ExpertBank) -> ExpertBank:
+        if self.ep is not None and self.ep.world > 1:
+            from .ep import shard_bank
+            bank = shard_bank(bank, self.ep.rank, self.ep.world)
         return bank_on_device(bank, self.act)
 
     def prepare_dense(self, w1, w3, w2):
@@ -245,6 +249,12 @@ class CudaBackend:
         """backbone.py:583-606 through nimg_moe_block_forward."""
         from .block import moe_block_forward
         f32 = torch.float32
+        if self.ep is not None:
+            from .ep import ep_moe_block_forward
+            return ep_moe_block_forward(x.to(self.act).contiguous(), sa_gate.to(f32),
+                                        r_attn.to(self.act), ff_scale.to(f32), ff_gate.to(f32),
+                                        t_vec.to(f32), layer, rcfg, bank, w_r, self.ep,
+                                        return_routing=return_routing)
         return moe_block_forward(x.to(self.act).contiguous(), sa_gate.to(f32), r_attn.to(self.act),
                                  ff_scale.to(f32), ff_gate.to(f32), t_vec.to(f32), layer, rcfg,
                                  bank, w_r, return_routing=return_routing)

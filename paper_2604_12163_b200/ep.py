@@ -200,23 +200,42 @@ class PeerBuffer:
 
 
 class CETransport:
-    """Copy-engine exchange state for one (shape, dtype) of the EP layer."""
+    """Copy-engine exchange state: peer-shared receive / return buffers (grow
+    only) and the per-step flags. One transport serves every EP layer of a
+    model whatever its shape: each call views the buffers as (world, n, d) of
+    its own chunk size, and the per-call epochs order the reuse of every slot
+    across calls (a peer writes my receive slot for call k only after I
+    returned its chunk of call k-1, my return slot only after I combined k-1)."""
 
-    def __init__(self, group, rank, world, chunk_rows, d, act, ydt, device):
-        self.rank, self.world, self.chunk_rows, self.d = rank, world, chunk_rows, d
-        self.act_es = torch.empty((), dtype=act).element_size()
-        self.y_es = torch.empty((), dtype=ydt).element_size()
-        rows = world * chunk_rows
-        self.recv = PeerBuffer(rows * d * self.act_es, group, rank, world)
-        self.yback = PeerBuffer(rows * d * self.y_es, group, rank, world)
+    def __init__(self, group, rank, world, x_bytes, y_bytes, device):
+        self.rank, self.world, self.device = rank, world, device
+        self.x_cap, self.y_cap = x_bytes, y_bytes
+        self.recv = PeerBuffer(world * x_bytes, group, rank, world)
+        self.yback = PeerBuffer(world * y_bytes, group, rank, world)
         self.flags = PeerBuffer(3 * world * 4, group, rank, world)   # disp | ret | comb
-        self.recv_t = _view(self.recv.own, (world, chunk_rows, d), act, device)
-        self.yback_t = _view(self.yback.own, (world, chunk_rows, d), ydt, device)
         self.streams = [torch.cuda.Stream(device) for _ in range(world)]   # returns, per peer
         self.disp_stream = torch.cuda.Stream(device)
         self.epoch = 0
-        self.key = (chunk_rows, d, act, ydt)
+        self.key = None
+        self.reshaped = False
         dist.barrier(group=group)   # every buffer zeroed and mapped before first use
+
+    def set_shape(self, chunk_rows, d, act, ydt):
+        key = (chunk_rows, d, act, ydt)
+        # A new chunk size moves the slot boundaries in the receive buffer: my
+        # next chunk for q may overlap slots q has not consumed yet, which
+        # q's RET flag (it consumed MY chunk) does not cover. The next
+        # dispatch therefore also waits for q's COMB flag of the previous call
+        # (q has combined, so it consumed its whole receive buffer).
+        self.reshaped = self.key is not None and key != self.key
+        if key != self.key:
+            self.chunk_rows, self.d = chunk_rows, d
+            self.act_es = torch.empty((), dtype=act).element_size()
+            self.y_es = torch.empty((), dtype=ydt).element_size()
+            self.recv_t = _view(self.recv.own, (self.world, chunk_rows, d), act, self.device)
+            self.yback_t = _view(self.yback.own, (self.world, chunk_rows, d), ydt, self.device)
+            self.key = key
+        return self
 
     def flag(self, owner: int, kind: int, idx: int) -> int:
         return self.flags.ptrs[owner] + 4 * (kind * self.world + idx)
@@ -242,13 +261,19 @@ class EPContext:
         self._streams = None
 
     def ce(self, chunk_rows, d, act, ydt, device) -> CETransport:
-        key = (chunk_rows, d, act, ydt)
-        if self._ce is None or self._ce.key != key:
-            if self._ce is not None:
+        """The transport, grown (collectively: every rank makes the same calls)
+        only when a call needs larger chunks than any before."""
+        xb = chunk_rows * d * torch.empty((), dtype=act).element_size()
+        yb = chunk_rows * d * torch.empty((), dtype=ydt).element_size()
+        tp = self._ce
+        if tp is None or xb > tp.x_cap or yb > tp.y_cap:
+            if tp is not None:
+                xb, yb = max(xb, tp.x_cap), max(yb, tp.y_cap)
                 torch.cuda.synchronize()
-                self._ce.close()
-            self._ce = CETransport(self.group, self.rank, self.world, chunk_rows, d, act, ydt, device)
-        return self._ce
+                dist.barrier(group=self.group)   # no peer still copies into the old buffers
+                tp.close()
+            self._ce = tp = CETransport(self.group, self.rank, self.world, xb, yb, device)
+        return tp.set_shape(chunk_rows, d, act, ydt)
 
     @property
     def ret_group(self):
@@ -271,12 +296,27 @@ def _mark(timeline, name):
         timeline.append((name, ev))
 
 
+def ep_moe_block_forward(x, sa_gate, r_attn, ff_scale, ff_gate, t_vec, layer: int,
+                         cfg: RouterConfig, bank_local: ExpertBank, w_r, ctx: "EPContext",
+                         return_routing: bool = False):
+    """Expert-parallel MoE branch of the backbone (backbone.py:583-606) for
+    this rank's samples: the 1-GPU block's prologue kernels, the EP layer, and
+    the gated residual in the combine epilogue -- the same kernels as
+    block.moe_block_forward, so the result equals the 1-GPU block."""
+    from .block import moe_block_prologue
+    h, x_norm, x_mod, th_ff = moe_block_prologue(x, sa_gate, r_attn, ff_scale, ff_gate, layer, cfg)
+    return ep_moe_forward(x_norm, x_mod, t_vec, cfg, bank_local, w_r, ctx,
+                          return_routing=return_routing, residual=(h, th_ff))
+
+
 def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBank, w_r,
-                   ctx: EPContext, stages=None, return_routing: bool = False, timeline=None):
+                   ctx: EPContext, stages=None, return_routing: bool = False, timeline=None,
+                   residual=None):
     """Expert-parallel moe_forward (moe.py:138-164) for this rank's samples.
 
     x_norm, x_mod: (B_l, S, d) local samples; bank_local: this rank's El
     experts (shard_bank) + the shared expert; w_r, t_emb as in moe_forward.
+    residual = (h, th_ff): the combine adds backbone.py:606 in its epilogue.
     """
     if stages is None:
         from .stages import CudaStages
@@ -318,7 +358,8 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
     else:
         y_back, y_sh = _overlapped_exchange(plan, ctx, stages, xg, xm, w, timeline)
     _mark(timeline, "returned")
-    out = stages.combine(y_back, y_sh, r, act).view(B_l, S, d)
+    out = (stages.combine(y_back, y_sh, r, act) if residual is None else
+           stages.combine(y_back, y_sh, r, act, residual=residual)).view(B_l, S, d)
     if ctx.overlap and ctx.transport == "ce":
         ce_after_combine(ctx)
     _mark(timeline, "combined")
@@ -408,6 +449,8 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
         sh = st.cuda_stream
         if k > 1:   # q consumed my previous chunk
             _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, RET, q), k - 1, sh))
+            if tp.reshaped:   # ... and, after a chunk-size change, every chunk (see set_shape)
+                _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, COMB, q), k - 1, sh))
         if timeline is not None:
             ev0 = torch.cuda.Event(enable_timing=True)
             ev0.record(st)

@@ -89,13 +89,24 @@ class CudaStages:
         return y_routed, y_shared
 
     def combine(self, y_routed: torch.Tensor, y_shared: torch.Tensor, r: dict,
-                out_dtype: torch.dtype) -> torch.Tensor:
-        """moe.py:156-161: deterministic expert-ascending weighted sum + shared."""
+                out_dtype: torch.dtype, residual=None) -> torch.Tensor:
+        """moe.py:156-161: deterministic expert-ascending weighted sum + shared.
+        residual = (h (B, S, d), th_ff (B, d)) adds backbone.py:606 in the
+        epilogue: out = h + th_ff * (that)."""
         T, d = y_shared.shape
         E = r["comb_rows"].shape[1]
         out = torch.empty((T, d), dtype=out_dtype, device=y_shared.device)
-        _lib.check(_lib.lib.nimg_combine(T, d, E, nimg_dtype(y_shared.dtype), nimg_dtype(out_dtype),
-                                         ptr(y_routed), ptr(y_shared), ptr(r["gates"]),
-                                         ptr(r["comb_rows"]), ptr(r["comb_cnt"]), ptr(out),
-                                         stream_handle()))
+        if residual is None:
+            _lib.check(_lib.lib.nimg_combine(T, d, E, nimg_dtype(y_shared.dtype),
+                                             nimg_dtype(out_dtype), ptr(y_routed), ptr(y_shared),
+                                             ptr(r["gates"]), ptr(r["comb_rows"]),
+                                             ptr(r["comb_cnt"]), ptr(out), stream_handle()))
+            return out
+        h, th = residual
+        S = h.shape[1]
+        _lib.check(_lib.lib.nimg_combine_residual(T, d, E, S, nimg_dtype(y_shared.dtype),
+                                                  nimg_dtype(out_dtype), ptr(y_routed),
+                                                  ptr(y_shared), ptr(r["gates"]),
+                                                  ptr(r["comb_rows"]), ptr(r["comb_cnt"]), ptr(h),
+                                                  ptr(th), ptr(out), stream_handle()))
         return out

@@ -134,3 +134,88 @@ def test_ep_oversubscribed_ce_bitwise(world):
     res = _run(world, (world, 512, 2048, 64, 1344, 4.0), modes=("ce",))
     for r in range(world):
         assert res[r] == {"ce": True}, res
+
+
+def _stack_worker(rank, world, port, q, dtype_name):
+    """MoEDiT with expert-parallel MoE blocks vs the 1-GPU stack on the same
+    samples: bitwise (same prologue / combine kernels, EP layer == 1-GPU)."""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    ngpu = torch.cuda.device_count()
+    torch.cuda.set_device(rank % ngpu)
+    if world > ngpu:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", rank % ngpu))
+    try:
+        from paper_2604_12163_b200 import dit as D
+        from paper_2604_12163_b200.ep import EPContext
+        from paper_2604_12163_b200.router import StageId
+        dt = getattr(torch, dtype_name)
+        # S1024 schedule: layers 3-4 at C=4, layer 5 at C=2 -> the EP chunk size
+        # changes inside a step and back at the next (transport slot reuse)
+        cfg = D.ModelConfig(n_layers=6, d_model=256, n_q_heads=4, n_kv_heads=1, head_dim=64,
+                            n_experts=8, expert_hidden=112, dense_layers=3, latent_channels=16,
+                            patch=2, dtype="float32", seed=1)
+        params = D.init_parameters(cfg)
+        rng = np.random.default_rng(4)
+        for k in params:   # non-identity blocks
+            if "mod." in k:
+                params[k][...] = rng.standard_normal(params[k].shape) * 0.1
+        B = 2 * world
+        z = np.random.default_rng(5).standard_normal((B, 16, 32, 32)).astype(np.float32)
+        t = np.linspace(0.1, 0.9, B)
+        prompts = ["a cat", "two dogs on a beach", "sky", "red car at night"] * world
+        sl = slice(2 * rank, 2 * rank + 2)
+        single = D.MoEDiT(cfg, params, compute_dtype=dt, backend=D.CudaBackend(dt))
+        ctx1 = single.precompute_text_kv(prompts[sl])
+        ref, _ = single.forward(z[sl], t[sl], ctx1, StageId.S1024, return_aux=False)
+        ep = D.MoEDiT(cfg, params, compute_dtype=dt, backend=D.CudaBackend(dt, ep=EPContext()))
+        ctx2 = ep.precompute_text_kv(prompts[sl])
+        ok = True
+        for _ in range(3):
+            out, _ = ep.forward(z[sl], t[sl], ctx2, StageId.S1024, return_aux=False)
+            torch.cuda.synchronize()
+            ok = ok and bool(torch.equal(out, ref))
+        q.put((rank, {"stack": ok}))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_stack(world, dtype_name):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_stack_worker, args=(r, world, port, q, dtype_name))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    import queue as _q
+    import time as _t
+    deadline = _t.time() + 600
+    while len(res) < world:
+        try:
+            r, v = q.get(timeout=5)
+            res[r] = v
+        except _q.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs) or _t.time() > deadline:
+                for p in procs:
+                    p.kill()
+                raise AssertionError(f"EP stack worker failed ({[p.exitcode for p in procs]})")
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("dtype_name", ["bfloat16", "float32"])
+def test_ep_stack_matches_single_gpu(dtype_name):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    world = 2
+    res = _run_stack(world, dtype_name)
+    for r in range(world):
+        assert res[r] == {"stack": True}, res
