@@ -312,52 +312,61 @@ router_scores_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
 // x rows of 36 doubles (288 B == 32 mod 128), W rows of 72 doubles (576 B ==
 // 64 mod 128).
 constexpr int DM_TM = 64, DM_KC = 32, DM_XS = 36, DM_WS = 72, DM_EP = 64;
-// Router prep for the DMMA router (E <= 64), one short kernel with no
-// counters: blocks [0, B) compute tb[b, e] = sum_k t_emb[b, k] * W_r[d + k, e]
-// in f64 (router.py:120-122; thread (e, slice q) sums 1/16 of k, slices folded
-// in a fixed order, deterministic); blocks [B, B + RP2_CONV) write
-// wd[k, e] = f64(W_r[k, e]) for the x half, E padded to 64.
+// Router prep for the DMMA router (E <= 64), one short kernel, no counters:
+// blocks [0, B * KS): block (b, ks) sums its k-range of the t half
+// part[b, ks, e] = sum_k t_emb[b, k] * W_r[d + k, e] in f64 (router.py:120-122)
+// -- thread (e, q) sums one of 4 sub-slices, folded in a fixed order; the
+// scores kernel folds the KS partials per sample in ks order (deterministic).
+// Blocks [B * KS, + RP2_CONV) write wd[k, e] = f64(W_r[k, e]) for the x half,
+// E padded to 64. Short dependent chains: the kernel is latency-bound.
 constexpr int RP2_CONV = 64;
-__global__ void __launch_bounds__(1024)
+constexpr int RP2_KS_MAX = 8;
+__host__ __device__ inline int rp2_ks(int d) {
+  const int nkc = (d + 63) / 64;   // == router_part_bytes' chunk count: the partials fit
+  return nkc < RP2_KS_MAX ? nkc : RP2_KS_MAX;
+}
+__global__ void __launch_bounds__(256)
 router_prep_dmma_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
-                        double* __restrict__ tb, double* __restrict__ wd, int B, int d, int E) {
+                        double* __restrict__ part, double* __restrict__ wd, int B, int d, int E) {
   pdl_trigger();
-  if ((int)blockIdx.x >= B) {
+  const int KS = rp2_ks(d);
+  if ((int)blockIdx.x >= B * KS) {
     const int64_t n = (int64_t)d * DM_EP;
     const int64_t stride = (int64_t)RP2_CONV * blockDim.x;
-    for (int64_t i = (int64_t)(blockIdx.x - B) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    for (int64_t i = (int64_t)(blockIdx.x - B * KS) * blockDim.x + threadIdx.x; i < n; i += stride) {
       const int64_t k = i / DM_EP;
       const int e = (int)(i % DM_EP);
       wd[i] = e < E ? (double)__ldg(w_r + k * E + e) : 0.0;
     }
     return;
   }
-  __shared__ double part[16][64];
-  const int b = blockIdx.x, e = threadIdx.x & 63, q = threadIdx.x >> 6;
-  const int kq = (d + 15) / 16, k0 = q * kq, k1 = min(d, k0 + kq);
+  __shared__ double sp[4][64];
+  const int b = blockIdx.x / KS, ks = blockIdx.x % KS;
+  const int e = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int nsl = 4 * KS, sl = ks * 4 + q;
+  const int klen = (d + nsl - 1) / nsl, k0 = sl * klen, k1 = min(d, k0 + klen);
   double acc = 0.0;
   if (e < E) {
     const float* t = t_emb + (int64_t)b * d;
     const float* w = w_r + (int64_t)d * E + e;
-#pragma unroll 8
+#pragma unroll 16
     for (int k = k0; k < k1; ++k) acc = fma((double)__ldg(t + k), (double)__ldg(w + (int64_t)k * E), acc);
   }
-  part[q][e] = acc;
+  sp[q][e] = acc;
   __syncthreads();
-  if (q == 0 && e < E) {
-    double r = part[0][e];
-#pragma unroll
-    for (int j = 1; j < 16; ++j) r += part[j][e];
-    tb[(int64_t)b * E + e] = r;
-  }
+  if (q == 0 && e < E)
+    part[((int64_t)b * KS + ks) * E + e] = ((sp[0][e] + sp[1][e]) + sp[2][e]) + sp[3][e];
 }
 
 __host__ __device__ inline size_t dmma_stage_bytes() {
   return (size_t)DM_KC * DM_WS * 8 + (size_t)DM_TM * DM_XS * 8;
 }
+// epilogue smem: ex/sc/lg (TM * E * 16) + folded t-bias of the <= TM samples a
+// CTA can span (TM * E * 8) + max/sum (TM * 16)
+__host__ __device__ inline size_t dmma_tbs_offset(int E) { return (size_t)DM_TM * E * 16; }
 __host__ __device__ inline size_t dmma_router_smem(int E) {
   const size_t stage = 2 * dmma_stage_bytes();
-  const size_t post = (size_t)DM_TM * E * (8 + 4 + 4);
+  const size_t post = (size_t)DM_TM * E * (8 + 4 + 4) + (size_t)DM_TM * E * 8;
   const size_t need = (stage > post ? stage : post) + (size_t)DM_TM * 16;
   // The grid is sized for exactly 2 CTAs per SM; registers and 74 KB would
   // admit 3, and a CTA placed early (PDL) on a half-busy GPU would then stack
@@ -375,11 +384,11 @@ NIMG_DEV void dmma_8x8x4(double& d0, double& d1, double a, double b) {
 template <typename TX, bool VEC>
 __global__ void __launch_bounds__(128)
 router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ wd,
-                          const double* __restrict__ tb, float* __restrict__ logits,
+                          const double* __restrict__ part, float* __restrict__ logits,
                           float* __restrict__ scores_bes, int B, int S, int d, int E,
                           int frags_per_cta) {
   // PDL secondary of router_prep_dmma_kernel: only the layer input x_norm is
-  // read before pdl_wait(); wd and tb come from the prep kernel.
+  // read before pdl_wait(); wd and the t-bias partials come from the prep.
   pdl_trigger();
   // CTA c owns 8-row fragments [c*fpc, (c+1)*fpc) (fpc <= 8); the grid is sized
   // to whole multiples of the SM count (>= 2 CTAs per SM) so per-SM DMMA work
@@ -487,6 +496,22 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
     __syncthreads();
   }
 
+  // t-bias of the samples this CTA spans: fold the prep's KS partials in ks
+  // order (deterministic) into smem once (the staging buffers are free now)
+  const int64_t b_first = t0 / S;
+  const int nb = (int)((t0 + rows - 1) / S - b_first + 1);
+  double* tbs = reinterpret_cast<double*>(sm + dmma_tbs_offset(E));
+  {
+    const int KS = rp2_ks(d);
+    for (int i = tid; i < nb * E; i += 128) {
+      const double* pp = part + ((b_first + i / E) * KS) * E + (i % E);
+      double r = pp[0];
+      for (int ks = 1; ks < KS; ++ks) r += pp[(int64_t)ks * E];
+      tbs[i] = r;
+    }
+  }
+  __syncthreads();
+
   if (E == DM_EP) {
     // ---- register epilogue (E == 64). Lane (ar, ac) holds, for row ar of each
     // fragment, columns n*8 + 2*ac + j. numpy's pairwise sum over 64 terms uses
@@ -507,7 +532,7 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int e = n * 8 + 2 * ac + j;
-          lg[n][j] = (float)(acc[m][n][j] + __ldg(tb + b * E + e));   // tensor.py:286-287
+          lg[n][j] = (float)(acc[m][n][j] + tbs[(b - b_first) * E + e]);   // tensor.py:286-287
           mx = fmax(mx, (double)lg[n][j]);
         }
       mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
@@ -552,7 +577,7 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int e = n * 8 + ac * 2 + j;
-          if (e < E) lg[tok * E + e] = (float)(acc[m][n][j] + tb[b * E + e]);  // tensor.py:286-287
+          if (e < E) lg[tok * E + e] = (float)(acc[m][n][j] + tbs[(b - b_first) * E + e]);  // tensor.py:286-287
         }
     }
   }
@@ -949,8 +974,8 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
   const int EP = dmma ? DM_EP : router_geom(E).EP;
   const int nkc = (d + RP_KCH - 1) / RP_KCH;
   // the first kernel of the chain: an ordinary launch (full stream order)
-  if (dmma) router_prep_dmma_kernel<<<B + RP2_CONV, 1024, 0, s>>>(t_emb, w_r, tb, wd, B, d, E);
-  // (conversion blocks: RP2_CONV x 1024 threads, 2 elements each at d = 2048)
+  if (dmma) router_prep_dmma_kernel<<<B * rp2_ks(d) + RP2_CONV, 256, 0, s>>>(t_emb, w_r, part, wd,
+                                                                          B, d, E);
   else router_prep_kernel<<<dim3(nkc + RP_CONV_BLOCKS, B), 64, 0, s>>>(t_emb, w_r, tb, part, wd,
                                                                        counter, B, d, E, EP);
   cudaError_t err = cudaGetLastError();
@@ -981,7 +1006,7 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
     if (err != cudaSuccess) return err;                                                        \
     err = launch_pdl(router_scores_dmma_kernel<TX, V>, dim3(grid), dim3(128), smem, s,        \
-                     reinterpret_cast<const TX*>(x_norm), wd, tb, logits, scores_bes, B, S, d,   \
+                     reinterpret_cast<const TX*>(x_norm), wd, part, logits, scores_bes, B, S, d, \
                      E, (int)fpc);                                                              \
     if (err != cudaSuccess) return err;                                                        \
   } while (0)
