@@ -150,3 +150,14 @@ def make_latent(seed: int, B: int, C: int, H: int, W: int):
 
 DIT_PROMPTS = ("a red fox in fresh snow at dawn", "two cups of coffee on a wooden table",
                "mountain lake")
+
+
+def make_bwd_inputs(p: dict):
+    """Layer inputs plus a seeded upstream gradient g_out (B,S,d) in the
+    activation dtype's values (bf16-representable in bf16 mode)."""
+    inp = make_layer_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"],
+                            layer=p.get("layer", 3), mode=p["mode"])
+    rng = np.random.default_rng(p["seed"] + 1000)
+    g = rng.standard_normal((p["B"], p["S"], p["d"])).astype(np.float32)
+    inp["g_out"] = bf16_round(g) if p["mode"] == "bf16" else g
+    return inp

@@ -23,6 +23,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
 from oracle.workloads import (DIT_PROMPTS, digest, make_block_inputs,  # noqa: E402
+                              make_bwd_inputs,
                               make_latent, make_layer_inputs, make_router_inputs,
                               perturb_modulation)
 from tests.refimport import load_reference  # noqa: E402
@@ -64,7 +65,15 @@ CASES = {
                                          head_dim=32, n_experts=4, expert_hidden=64,
                                          dense_layers=3, latent_channels=4, patch=2,
                                          dtype="float32", seed=3))),
+    # backward of the layer: reference tape gradients of
+    # sum(moe_forward(...) * g_out) for a seeded upstream gradient g_out
+    "bwd_small_fp32": ("moe_bwd", dict(seed=20, B=2, S=64, d=64, E=4, h=64, C=2.0, mode="fp32")),
+    "bwd_ragged_fp32": ("moe_bwd", dict(seed=21, B=3, S=37, d=24, E=5, h=20, C=1.7, mode="fp32",
+                                        gate_scale=1.7)),
+    "bwd_tc_bf16": ("moe_bwd", dict(seed=22, B=2, S=128, d=128, E=4, h=64, C=2.0, mode="bf16")),
 }
+
+GRAD_NAMES = ("x_norm", "x_mod", "t_emb", "w_r", "w1", "w3", "w2", "sw1", "sw3", "sw2")
 
 
 def inputs_for(kind, p):
@@ -73,6 +82,8 @@ def inputs_for(kind, p):
         return {"z": z, "t": t}
     if kind == "block":
         return make_block_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"], mode=p["mode"])
+    if kind == "moe_bwd":
+        return make_bwd_inputs(p)
     if kind == "moe":
         return make_layer_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"],
                                  layer=p.get("layer", 3), mode=p["mode"])
@@ -133,7 +144,28 @@ def run_reference_dit(p):
     return res
 
 
+def run_reference_bwd(ref, p, inp):
+    """Reference Tape + backward (tensor.py:590-628) through moe_forward."""
+    nt = ref.tensor
+    T, f32 = nt.Tensor, np.float32
+    B, S, d = inp["x_mod"].shape
+    ts = {k: T(inp[k], requires_grad=True, dtype=f32) for k in GRAD_NAMES}
+    cfg = ref.router.RouterConfig(d_model=d, n_experts=p["E"], capacity_factor=p["C"],
+                                  gate_scale=p.get("gate_scale", 1.0))
+    bank = ref.moe.ExpertBank(ts["w1"], ts["w3"], ts["w2"], ts["sw1"], ts["sw3"], ts["sw2"])
+    with nt.Tape() as tape:
+        out = ref.moe.moe_forward(ts["x_mod"], ts["x_norm"], ts["x_mod"], ts["t_emb"], cfg, bank,
+                                  ts["w_r"])
+        loss = nt.sum(nt.mul(out, T(inp["g_out"], dtype=f32)))
+    nt.backward(tape, loss)
+    res = {f"grad_{k}": ts[k].grad for k in GRAD_NAMES}
+    res["out"] = out.data
+    return res
+
+
 def run_reference(ref, kind, p, inp):
+    if kind == "moe_bwd":
+        return run_reference_bwd(ref, p, inp)
     if kind == "dit":
         return run_reference_dit(p)
     if kind == "block":

@@ -8,7 +8,7 @@ import os
 
 import numpy as np
 
-from oracle.workloads import (digest, make_block_inputs, make_latent, make_layer_inputs,
+from oracle.workloads import (digest, make_block_inputs, make_bwd_inputs, make_latent, make_layer_inputs,
                               make_router_inputs)
 
 GOLDEN_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
@@ -28,6 +28,8 @@ def case(name: str):
         inp = {"z": z, "t": t}
     elif kind == "block":
         inp = make_block_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"], mode=p["mode"])
+    elif kind == "moe_bwd":
+        inp = make_bwd_inputs(p)
     elif kind == "moe":
         inp = make_layer_inputs(p["seed"], p["B"], p["S"], p["d"], p["E"], p["h"],
                                 layer=p.get("layer", 3), mode=p["mode"])

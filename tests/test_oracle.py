@@ -185,3 +185,80 @@ def test_zero_w2_gives_shared_only():                        # test_moe.py:147-1
     out = O.moe_forward(rng.normal(size=(1, 6, d)), xm, rng.normal(size=(1, d)),
                         rng.normal(size=(2 * d, E)), w1, w3, w2, s1, s3, s2, capacity_factor=1.0)
     np.testing.assert_array_equal(out.reshape(-1, d), O.swiglu_arrays(xm.reshape(-1, d), s1, s3, s2))
+
+
+# ------------------------------------------------------------------ backward
+GRAD_NAMES = ("x_norm", "x_mod", "t_emb", "w_r", "w1", "w3", "w2", "sw1", "sw3", "sw2")
+
+
+@pytest.mark.parametrize("name", G.names("moe_bwd"))
+def test_oracle_backward_matches_reference_golden(name):
+    """Reference Tape + backward through moe_forward (tensor.py:590-628) vs
+    the oracle's restated pullbacks: bit-exact f64 gradients."""
+    kind, p, inp, exp = G.case(name)
+    g = O.moe_backward(*(inp[k] for k in GRAD_NAMES), inp["g_out"], capacity_factor=p["C"],
+                       gate_scale=p.get("gate_scale", 1.0))
+    for k in GRAD_NAMES:
+        np.testing.assert_array_equal(g[k], exp[f"grad_{k}"], err_msg=k)
+
+
+def test_oracle_backward_vs_finite_differences():
+    """test_moe.py:220-236 restated on the oracle: central differences of the
+    oracle forward against the oracle backward (f64 inputs)."""
+    rng = np.random.default_rng(11)
+    B, S, d, E, C, h = 1, 5, 3, 2, 1.5, 4
+    a = {"x_norm": rng.normal(size=(B, S, d)), "x_mod": rng.normal(size=(B, S, d)),
+         "t_emb": rng.normal(size=(B, d)), "w_r": rng.normal(size=(2 * d, E)),
+         "w1": rng.normal(size=(E, h, d)), "w3": rng.normal(size=(E, h, d)),
+         "w2": rng.normal(size=(E, d, h)), "sw1": rng.normal(size=(h, d)),
+         "sw3": rng.normal(size=(h, d)), "sw2": rng.normal(size=(d, h))}
+
+    def loss(v):
+        out = O.moe_forward(v["x_norm"], v["x_mod"], v["t_emb"], v["w_r"], v["w1"], v["w3"],
+                            v["w2"], v["sw1"], v["sw3"], v["sw2"], capacity_factor=C)
+        return float((out * out).sum())
+
+    out = O.moe_forward(*(a[k] for k in GRAD_NAMES), capacity_factor=C)
+    g = O.moe_backward(*(a[k] for k in GRAD_NAMES), 2.0 * out, capacity_factor=C)
+    hstep = 1e-5
+    for k in ("x_mod", "w_r", "w1", "w3", "w2", "sw1"):
+        flat = a[k].reshape(-1)
+        num = np.zeros_like(flat)
+        for i in range(flat.size):
+            keep = flat[i]
+            flat[i] = keep + hstep
+            fp = loss(a)
+            flat[i] = keep - hstep
+            fm = loss(a)
+            flat[i] = keep
+            num[i] = (fp - fm) / (2 * hstep)
+        an = g[k].reshape(-1)
+        rel = np.abs(an - num) / np.maximum(1e-8, np.abs(an) + np.abs(num))
+        assert rel.max() <= 1e-5, (k, rel.max())
+
+
+@pytest.mark.skipif(not reference_available(), reason="reference tree not mounted")
+@pytest.mark.parametrize("seed,B,S,d,E,h,C,gs", [(31, 2, 9, 6, 3, 5, 1.5, 1.0),
+                                                 (32, 1, 16, 8, 4, 8, 4.0, 0.5)])
+def test_oracle_backward_matches_live_reference(seed, B, S, d, E, h, C, gs):
+    ref = load_reference()
+    nt = ref.tensor
+    rng = np.random.default_rng(seed)
+    a = {"x_norm": rng.normal(size=(B, S, d)), "x_mod": rng.normal(size=(B, S, d)),
+         "t_emb": rng.normal(size=(B, d)), "w_r": rng.normal(size=(2 * d, E)),
+         "w1": rng.normal(size=(E, h, d)), "w3": rng.normal(size=(E, h, d)),
+         "w2": rng.normal(size=(E, d, h)), "sw1": rng.normal(size=(h, d)),
+         "sw3": rng.normal(size=(h, d)), "sw2": rng.normal(size=(d, h))}
+    a = {k: v.astype(np.float32) for k, v in a.items()}
+    gout = rng.normal(size=(B, S, d)).astype(np.float32)
+    ts = {k: nt.Tensor(v, requires_grad=True, dtype=np.float32) for k, v in a.items()}
+    cfg = ref.router.RouterConfig(d_model=d, n_experts=E, capacity_factor=C, gate_scale=gs)
+    bank = ref.moe.ExpertBank(ts["w1"], ts["w3"], ts["w2"], ts["sw1"], ts["sw3"], ts["sw2"])
+    with nt.Tape() as tape:
+        out = ref.moe.moe_forward(ts["x_mod"], ts["x_norm"], ts["x_mod"], ts["t_emb"], cfg, bank,
+                                  ts["w_r"])
+        loss = nt.sum(nt.mul(out, nt.Tensor(gout, dtype=np.float32)))
+    nt.backward(tape, loss)
+    g = O.moe_backward(*(a[k] for k in GRAD_NAMES), gout, capacity_factor=C, gate_scale=gs)
+    for k in GRAD_NAMES:
+        np.testing.assert_array_equal(g[k], ts[k].grad, err_msg=k)
