@@ -94,8 +94,10 @@ int nimg_device_sms(int* sms);
 
 /* Profiling hook: up to 8 cudaEvent_t (as void*) recorded on the launch stream
  * by nimg_moe_forward at its stage boundaries: [0] start, [1] routed,
- * [2] gathered, [3] GEMM1 done, [4] GEMM2 done, [5] combined. n = 0 turns it
- * off. Thread-local; no reference counterpart (instrumentation only). */
+ * [2] gathered, [3] GEMM1 done, [4] GEMM2 done, [5] combined; by
+ * nimg_moe_backward: [0] start, [1] combine + router pullbacks, [2] dH,
+ * [3] dW2, [4] dX, [5] dW1/dW3, [6] g_x_mod. n = 0 turns it off.
+ * Thread-local; no reference counterpart (instrumentation only). */
 int nimg_profile_events(void* const* events, int32_t n);
 
 /* router.py:70-74  capacity_for(S, E, C) = min(ceil(C*S/E), S) */
@@ -108,6 +110,37 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
  * weighted combine + shared expert -> out. */
 int nimg_moe_forward(const nimg_moe_desc* desc, const nimg_moe_ptrs* ptrs, void* ws,
                      size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ training
+ * The layer's backward: what reference backward(tape, loss) (tensor.py:590-628)
+ * accumulates through moe_forward (moe.py:138-164) -- the swiglu pullback
+ * (moe.py:53-62), the gate chain and softmax pullbacks (router.py:137-143,
+ * tensor.py:467-477) and the router matmul pullback (tensor.py:280-296).
+ *
+ * nimg_moe_forward_train is nimg_moe_forward that also keeps, in a
+ * caller-owned state blob, what the pullback needs (gathered rows, h1 | h3,
+ * pre, routed expert outputs). The route outputs (ptrs->route) must stay
+ * alive until nimg_moe_backward. bf16 layers with d, h, h_shared multiples
+ * of 64 run the tcgen05 path (bf16 intermediates); all others the CUDA-core
+ * path (fp32 intermediates). */
+typedef struct nimg_moe_grads {
+  const void* g_out; /* (B,S,d) act: d loss / d out                       */
+  void* g_x_norm;    /* (B,S,d) act                                        */
+  void* g_x_mod;     /* (B,S,d) act                                        */
+  float* g_t_emb;    /* (B,d)  fp32                                        */
+  float* g_w_r;      /* (2d,E) fp32                                        */
+  float *g_w1, *g_w3, *g_w2;    /* (E,h,d), (E,h,d), (E,d,h) fp32        */
+  float *g_sw1, *g_sw3, *g_sw2; /* (hs,d), (hs,d), (d,hs) fp32            */
+} nimg_moe_grads;
+int nimg_moe_train_state_bytes(const nimg_moe_desc* desc, size_t* bytes);
+int nimg_moe_forward_train(const nimg_moe_desc* desc, const nimg_moe_ptrs* ptrs, void* state,
+                           size_t state_bytes, void* ws, size_t ws_bytes, void* stream);
+int nimg_moe_backward_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
+/* ptrs: the same inputs / routing buffers as the forward (out unused). Writes
+ * every gradient in full (no accumulation into existing values). */
+int nimg_moe_backward(const nimg_moe_desc* desc, const nimg_moe_ptrs* ptrs, const void* state,
+                      size_t state_bytes, const nimg_moe_grads* grads, void* ws, size_t ws_bytes,
+                      void* stream);
 
 /* The backbone's MoE branch around the layer (backbone.py:583-606):
  *   h = x + tanh(sa_gate) r_attn;  x_norm = rmsnorm(h) / sqrt(layer+1);

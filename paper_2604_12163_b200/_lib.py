@@ -27,6 +27,8 @@ EXPORTS = (
     "nimg_moe_block_workspace_bytes", "nimg_moe_block_forward",
     "nimg_ln_modulate", "nimg_gate_res_ln_modulate", "nimg_gated_residual", "nimg_qk_norm_rope",
     "nimg_moe_block_prologue_workspace_bytes", "nimg_moe_block_prologue", "nimg_combine_residual",
+    "nimg_moe_train_state_bytes", "nimg_moe_forward_train", "nimg_moe_backward_workspace_bytes",
+    "nimg_moe_backward",
 )
 
 
@@ -57,6 +59,13 @@ class BlockPtrs(C.Structure):
                 ("sw1", C.c_void_p), ("sw3", C.c_void_p), ("sw2", C.c_void_p), ("h", C.c_void_p),
                 ("x_norm", C.c_void_p), ("x_mod", C.c_void_p), ("out", C.c_void_p),
                 ("route", RouteOut)]
+
+
+class MoeGrads(C.Structure):
+    _fields_ = [("g_out", C.c_void_p), ("g_x_norm", C.c_void_p), ("g_x_mod", C.c_void_p),
+                ("g_t_emb", C.c_void_p), ("g_w_r", C.c_void_p), ("g_w1", C.c_void_p),
+                ("g_w3", C.c_void_p), ("g_w2", C.c_void_p), ("g_sw1", C.c_void_p),
+                ("g_sw3", C.c_void_p), ("g_sw2", C.c_void_p)]
 
 
 class FfnDesc(C.Structure):
@@ -108,6 +117,12 @@ def _load():
                                       C.c_int),
         "nimg_gated_residual": ([I64, I64, I64, I32, P, P, P, P, P], C.c_int),
         "nimg_qk_norm_rope": ([I64, I64, I64, I64, I32, P, I64, P, P, P, C.c_float, P], C.c_int),
+        "nimg_moe_train_state_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
+        "nimg_moe_forward_train": ([C.POINTER(MoeDesc), C.POINTER(MoePtrs), P, SZ, P, SZ, P],
+                                   C.c_int),
+        "nimg_moe_backward_workspace_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
+        "nimg_moe_backward": ([C.POINTER(MoeDesc), C.POINTER(MoePtrs), P, SZ,
+                               C.POINTER(MoeGrads), P, SZ, P], C.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

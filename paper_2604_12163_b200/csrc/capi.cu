@@ -261,21 +261,37 @@ bool use_pair_kernels() {
 
 // gather_idx != null (tcgen05 path only): routed row r of GEMM1's A operand is
 // row gather_idx[r] of xr, which then has gather_src_rows rows (TMA gather4).
+// Training forward: `pre` lands in caller buffers (kept for the weight
+// gradient of GEMM2) and GEMM1 also stores h1 | h3 (the SwiGLU pullback's
+// inputs); force_simt keeps the whole layer on the CUDA-core path (fp32
+// intermediates) when the tcgen05 backward cannot take the shape.
+struct FfnTrain {
+  bool force_simt;
+  void *pre_r, *pre_s, *h_r, *h_s;
+};
+
 int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex,
                     const void* xr, const void* w1, const void* w3, const void* w2, void* yr,
                     const void* xs, const void* sw1, const void* sw3, const void* sw2, void* ys,
                     void* ws, size_t ws_bytes, cudaStream_t st,
-                    const int32_t* gather_idx = nullptr, int64_t gather_src_rows = 0) {
+                    const int32_t* gather_idx = nullptr, int64_t gather_src_rows = 0,
+                    const FfnTrain* tr = nullptr) {
   NIMG_TRY(check_ffn(f, off, ex));
-  if (ws_bytes < ffn_ws_bytes(f)) return fail(NIMG_ERR_CONFIG, "workspace too small");
+  if (!tr && ws_bytes < ffn_ws_bytes(f)) return fail(NIMG_ERR_CONFIG, "workspace too small");
   const bool has_r = f->n_rows > 0, has_s = f->n_shared_rows > 0;
   if (!has_r && !has_s) return NIMG_OK;
   if ((has_r && (!xr || !w1 || !w3 || !w2 || !yr)) || (has_s && (!xs || !sw1 || !sw3 || !sw2 || !ys)))
     return fail(NIMG_ERR_SHAPE, "null tensor pointer");
-  const bool tc = ffn_use_tc(f);
+  const bool tc = ffn_use_tc(f) && !(tr && tr->force_simt);
   const size_t e = tc ? 2 : 4;
   uint8_t* pre_r = static_cast<uint8_t*>(ws);
   uint8_t* pre_s = pre_r + align_up((size_t)f->n_rows * f->h * e);
+  if (tr) {
+    pre_r = static_cast<uint8_t*>(tr->pre_r);
+    pre_s = static_cast<uint8_t*>(tr->pre_s);
+  }
+  void* h_r = tr ? tr->h_r : nullptr;
+  void* h_s = tr ? tr->h_s : nullptr;
   const int d = (int)f->d, h = (int)f->h, hs = (int)(has_s ? f->h_shared : f->h);
 
   if (tc) {
@@ -310,8 +326,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       }
       if (!has_r) { tm.a[0] = tm.a[1]; tm.b[0] = tm.b[1]; tm.b3[0] = tm.b3[1]; }
       if (!has_s) { tm.a[1] = tm.a[rb]; tm.b[1] = tm.b[rb]; tm.b3[1] = tm.b3[rb]; }
-      p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0, gather_idx, gather_idx ? xr : nullptr};
-      p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, nullptr, nullptr};
+      p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0, gather_idx, gather_idx ? xr : nullptr, h_r};
+      p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, nullptr, nullptr, h_s};
       if (pair) CUDA_TRY(launch_grouped_tc_pair(0, tm, p, sms, st));
       else CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
       mark(3, st);
@@ -352,8 +368,10 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
     SimtParams p;
     memset(&p, 0, sizeof(p));
     NIMG_TRY(fill_segments(p, f, off, ex, bm, (h + bn - 1) / bn, (hs + bn - 1) / bn));
-    p.bank[0] = SimtBank{xr, d, w1, w3, reinterpret_cast<float*>(pre_r), h, d, h, (h + bn - 1) / bn, 0};
-    p.bank[1] = SimtBank{xs, d, sw1, sw3, reinterpret_cast<float*>(pre_s), hs, d, hs, (hs + bn - 1) / bn, 0};
+    p.bank[0] = SimtBank{xr, d, w1, w3, reinterpret_cast<float*>(pre_r), h, d, h, (h + bn - 1) / bn, 0,
+                         static_cast<float*>(h_r)};
+    p.bank[1] = SimtBank{xs, d, sw1, sw3, reinterpret_cast<float*>(pre_s), hs, d, hs, (hs + bn - 1) / bn, 0,
+                         static_cast<float*>(h_s)};
     CUDA_TRY(launch_grouped_simt(0, bf, p, st));
     mark(3, st);
   }
@@ -407,6 +425,92 @@ bool use_fused_gather(int32_t path, int64_t d) {
     return e && e[0] == '1';
   }();
   return on && path == NIMG_PATH_TCGEN05 && d % 64 == 0;
+}
+
+// ------------------------------------------------------------- training state
+// tcgen05 training path: bf16 layer whose backward GEMMs tile cleanly
+// (K = h and 2h split at 64-column boxes); else the CUDA-core path with fp32
+// intermediates.
+bool train_use_tc(const nimg_moe_desc* d) {
+  return d->act_dtype == NIMG_BF16 && d->d % 64 == 0 && d->h % 64 == 0 && d->h_shared % 64 == 0;
+}
+
+struct TrainState {
+  bool tc;
+  void *xg, *h_r, *h_s, *pre_r, *pre_s, *y_r;
+  size_t bytes;
+};
+TrainState train_state_layout(const nimg_moe_desc* d, void* base) {
+  TrainState s{};
+  s.tc = train_use_tc(d);
+  const size_t R = (size_t)d->E * d->B * d->cap, T = (size_t)d->B * d->S;
+  const size_t ea = elt(d->act_dtype), ei = s.tc ? 2 : 4;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { void* q = p ? p + o : nullptr; o += align_up(bytes); return q; };
+  s.xg = take(R * d->d * ea);
+  s.h_r = take(R * 2 * d->h * ei);
+  s.h_s = take(T * 2 * d->h_shared * ei);
+  s.pre_r = take(R * d->h * ei);
+  s.pre_s = take(T * d->h_shared * ei);
+  s.y_r = take(R * d->d * ei);
+  s.bytes = o;
+  return s;
+}
+
+struct BwdWs {
+  void *dy_r, *dy_s, *dh_r, *dh_s, *dx_r, *dx_s;
+  float *dlogits, *colsum, *part;
+  size_t bytes;
+};
+BwdWs bwd_ws_layout(const nimg_moe_desc* d, void* base) {
+  BwdWs w{};
+  const bool tc = train_use_tc(d);
+  const size_t R = (size_t)d->E * d->B * d->cap, T = (size_t)d->B * d->S;
+  const size_t ei = tc ? 2 : 4;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t o = 0;
+  auto take = [&](size_t bytes) { void* q = p ? p + o : nullptr; o += align_up(bytes); return q; };
+  w.dy_r = take(R * d->d * ei);
+  w.dy_s = tc ? nullptr : take(T * d->d * ei);   // tcgen05: g_out itself is the shared A operand
+  w.dh_r = take(R * 2 * d->h * ei);
+  w.dh_s = take(T * 2 * d->h_shared * ei);
+  w.dx_r = take(R * d->d * ei);
+  w.dx_s = take(T * d->d * ei);
+  w.dlogits = static_cast<float*>(take(T * d->E * 4));
+  w.colsum = static_cast<float*>(take((size_t)d->B * d->E * 4));
+  w.part = static_cast<float*>(take(router_bwd_part_bytes((int64_t)T, (int)d->d, (int)d->E)));
+  w.bytes = o;
+  return w;
+}
+
+// Segment table of one backward grouped launch. W modes put the shared bank
+// first (its tiles reduce over all T rows: longest first).
+int fill_bwd_segments(BwdParams& p, int mode, const nimg_moe_desc* d, int bm, int bn) {
+  const bool wm = mode == BWD_W2 || mode == BWD_W1;
+  const int64_t rows_e = d->B * d->cap, T = d->B * d->S;
+  int n = 0;
+  int64_t tiles = 0;
+  auto add = [&](int bank, int64_t row0, int64_t rows, int expert) {
+    BwdBank& bk = p.bank[bank];
+    p.seg_row0[n] = (int)row0;
+    p.seg_rows[n] = (int)rows;
+    p.seg_expert[n] = expert;
+    p.seg_bank[n] = bank;
+    p.seg_tile0[n] = (int)tiles;
+    bk.ntn = (bk.N + bn - 1) / bn;
+    bk.ntm = wm ? (bk.M + bm - 1) / bm : 0;
+    tiles += wm ? (int64_t)bk.ntm * bk.ntn : (rows + bm - 1) / bm * bk.ntn;
+    ++n;
+  };
+  if (wm) add(1, 0, T, 0);
+  for (int e = 0; e < d->E; ++e) add(0, e * rows_e, rows_e, e);
+  if (!wm) add(1, 0, T, 0);
+  p.nseg = n;
+  p.seg_tile0[n] = (int)tiles;
+  if (tiles >= ((int64_t)1 << 31)) return fail(NIMG_ERR_CONFIG, "too many tiles");
+  p.total_tiles = (int)tiles;
+  return NIMG_OK;
 }
 
 nimg_ffn_desc layer_ffn_desc(const nimg_moe_desc* d) {
@@ -563,9 +667,12 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   return NIMG_OK;
 }
 
-// moe.py:138-164; with resid_h, the combine writes h + th_ff * moe (backbone.py:606)
+// moe.py:138-164; with resid_h, the combine writes h + th_ff * moe (backbone.py:606).
+// state != null: training forward -- the gathered rows, h1 | h3, pre and the
+// routed expert outputs land in the caller's state blob (train_state_layout).
 static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, size_t ws_bytes,
-                            cudaStream_t st, const void* resid_h, const void* th_ff) {
+                            cudaStream_t st, const void* resid_h, const void* th_ff,
+                            void* state = nullptr) {
   NIMG_TRY(check_moe_desc(d));
   if (!p) return fail(NIMG_ERR_SHAPE, "null pointers");
   size_t need = 0;
@@ -574,13 +681,22 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   const nimg_ffn_desc f = layer_ffn_desc(d);
   int32_t path, ydt;
   nimg_ffn_path(&f, &path, &ydt);
-  const bool fused_gather = use_fused_gather(path, d->d);
+  FfnTrain tr{};
+  TrainState ts{};
+  if (state) {
+    ts = train_state_layout(d, state);
+    tr = FfnTrain{!ts.tc, ts.pre_r, ts.pre_s, ts.h_r, ts.h_s};
+    ydt = ts.tc ? NIMG_BF16 : NIMG_F32;
+    path = ts.tc ? NIMG_PATH_TCGEN05 : NIMG_PATH_SIMT;
+  }
+  const bool fused_gather = !state && use_fused_gather(path, d->d);
   uint8_t* w = static_cast<uint8_t*>(ws);
   void* route_ws = w;                 w += route_ws_bytes(d);
   void* xg = w;                       if (!fused_gather) w += align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
   void* ffn_ws = w;                   w += ffn_ws_bytes(&f);
   void* yr = w;                       w += align_up((size_t)f.n_rows * d->d * elt(ydt));
   void* ys = w;
+  if (state) { xg = ts.xg; yr = ts.y_r; }
 
   mark(0, st);
   NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st));
@@ -595,7 +711,8 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   // fused path: GEMM1 gathers x_mod rows by token_flat itself (TMA gather4)
   NIMG_TRY(expert_ffn_impl(&f, off, nullptr, fused_gather ? p->x_mod : xg, p->w1, p->w3, p->w2, yr,
                            p->x_mod, p->sw1, p->sw3, p->sw2, ys, ffn_ws, ffn_ws_bytes(&f), st,
-                           fused_gather ? p->route.token_flat : nullptr, d->B * d->S));
+                           fused_gather ? p->route.token_flat : nullptr, d->B * d->S,
+                           state ? &tr : nullptr));
   mark(4, st);
   CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys, p->route.gates,
                           p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,
@@ -607,6 +724,155 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
 int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, size_t ws_bytes,
                      void* stream) {
   return moe_forward_impl(d, p, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+// ------------------------------------------------------------------ training
+int nimg_moe_train_state_bytes(const nimg_moe_desc* d, size_t* bytes) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");
+  *bytes = train_state_layout(d, nullptr).bytes;
+  return NIMG_OK;
+}
+
+int nimg_moe_forward_train(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* state,
+                           size_t state_bytes, void* ws, size_t ws_bytes, void* stream) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!state || state_bytes < train_state_layout(d, nullptr).bytes)
+    return fail(NIMG_ERR_CONFIG, "training state too small");
+  return moe_forward_impl(d, p, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr, state);
+}
+
+int nimg_moe_backward_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");
+  *bytes = bwd_ws_layout(d, nullptr).bytes;
+  return NIMG_OK;
+}
+
+static int bwd_grouped(int mode, bool tc, bool b_bf16, BwdParams& P, const TmapSet& tm, int sms,
+                       const nimg_moe_desc* d, cudaStream_t st) {
+  const int bm = tc ? 128 : simt_bwd_bm();
+  const int bn = tc ? tc_bwd_bn(mode) : simt_bwd_bn();
+  NIMG_TRY(fill_bwd_segments(P, mode, d, bm, bn));
+  if (tc) CUDA_TRY(launch_grouped_tc_bwd(mode, tm, P, sms, st));
+  else CUDA_TRY(launch_grouped_simt_bwd(mode, b_bf16, P, st));
+  return NIMG_OK;
+}
+
+// The layer's pullback (moe.py:138-164 under backward(tape, loss),
+// tensor.py:590-628): see backward_kernels.cu / grouped_gemm_bwd_sm100.cu.
+int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void* state,
+                      size_t state_bytes, const nimg_moe_grads* g, void* ws, size_t ws_bytes,
+                      void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  NIMG_TRY(check_moe_desc(d));
+  if (!p || !g) return fail(NIMG_ERR_SHAPE, "null pointers");
+  if (d->E + 2 > kMaxSeg) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
+  const TrainState ts = train_state_layout(d, const_cast<void*>(state));
+  if (!state || state_bytes < ts.bytes) return fail(NIMG_ERR_CONFIG, "training state too small");
+  const BwdWs w = bwd_ws_layout(d, ws);
+  if (!ws || ws_bytes < w.bytes) return fail(NIMG_ERR_CONFIG, "workspace too small (%zu < %zu)", ws_bytes, w.bytes);
+  if (!g->g_out || !g->g_x_norm || !g->g_x_mod || !g->g_t_emb || !g->g_w_r || !g->g_w1 || !g->g_w3 ||
+      !g->g_w2 || !g->g_sw1 || !g->g_sw3 || !g->g_sw2)
+    return fail(NIMG_ERR_SHAPE, "null gradient pointer");
+  const nimg_route_out& ro = p->route;
+  if (!ro.logits || !ro.gates || !ro.gate_raw || !ro.comb_rows || !ro.comb_cnt)
+    return fail(NIMG_ERR_SHAPE, "null routing pointer");
+  const bool tc = ts.tc, bf = d->act_dtype == NIMG_BF16;
+  const int64_t T = d->B * d->S, R = d->E * d->B * d->cap, rows_e = d->B * d->cap;
+  const int dd = (int)d->d, h = (int)d->h, hs = (int)d->h_shared, E = (int)d->E;
+  if (tc) {
+    const void* ptrs[] = {g->g_out, p->x_mod, p->w1, p->w3, p->w2, p->sw1, p->sw3, p->sw2, g->g_x_mod};
+    for (const void* q : ptrs)
+      if (!aligned16(q)) return fail(NIMG_ERR_SHAPE, "tensor not 16-byte aligned");
+  }
+  int sms = 0;
+  NIMG_TRY(device_sms(&sms));
+  mark(0, st);
+  // 1. combine / gate / softmax pullback -> dY rows, dlogits
+  CUDA_TRY(launch_combine_bwd(bf, tc, tc, g->g_out, ts.y_r, ro.gates, ro.gate_raw, ro.comb_rows,
+                              ro.comb_cnt, ro.logits, w.dy_r, w.dy_s, w.dlogits, T, dd, E,
+                              (int)rows_e, d->gate_eps, d->gate_scale, st));
+  // 2. router pullback -> g_x_norm, g_t_emb, g_w_r
+  CUDA_TRY(launch_router_bwd(bf, p->x_norm, p->t_emb, p->w_r, w.dlogits, g->g_x_norm, g->g_w_r,
+                             g->g_t_emb, w.part, w.colsum, (int)d->B, (int)d->S, dd, E, st));
+  mark(1, st);
+  const void* dys = tc ? g->g_out : w.dy_s;
+  TmapSet tm;
+  // 3. dH = SwiGLU'(dY W2)
+  {
+    BwdParams P;
+    memset(&P, 0, sizeof(P));
+    memset(&tm, 0, sizeof(tm));
+    P.bank[0] = BwdBank{w.dy_r, dd, p->w2, nullptr, 0, ts.h_r, w.dh_r, nullptr, 2 * (int64_t)h, 0, h, dd, h, 0, 0};
+    P.bank[1] = BwdBank{dys, dd, p->sw2, nullptr, 0, ts.h_s, w.dh_s, nullptr, 2 * (int64_t)hs, 0, hs, dd, hs, 0, 0};
+    if (tc) {
+      NIMG_TRY(map_2d(&tm.a[0], w.dy_r, R, dd, 128));
+      NIMG_TRY(map_3d(&tm.b[0], p->w2, E, dd, h, 64));
+      NIMG_TRY(map_2d(&tm.a[1], dys, T, dd, 128));
+      NIMG_TRY(map_3d(&tm.b[1], p->sw2, 1, dd, hs, 64));
+      tm.b3[0] = tm.b[0]; tm.b3[1] = tm.b[1];
+    }
+    NIMG_TRY(bwd_grouped(BWD_D2, tc, bf, P, tm, sms, d, st));
+  }
+  mark(2, st);
+  // 4. dW2 = dY^T pre
+  {
+    BwdParams P;
+    memset(&P, 0, sizeof(P));
+    memset(&tm, 0, sizeof(tm));
+    P.bank[0] = BwdBank{w.dy_r, dd, ts.pre_r, nullptr, h, nullptr, g->g_w2, nullptr, 0, dd, h, 0, h, 0, 0};
+    P.bank[1] = BwdBank{dys, dd, ts.pre_s, nullptr, hs, nullptr, g->g_sw2, nullptr, 0, dd, hs, 0, hs, 0, 0};
+    if (tc) {
+      NIMG_TRY(map_3d(&tm.a[0], w.dy_r, E, rows_e, dd, 64));
+      NIMG_TRY(map_3d(&tm.b[0], ts.pre_r, E, rows_e, h, 64));
+      NIMG_TRY(map_3d(&tm.a[1], dys, 1, T, dd, 64));
+      NIMG_TRY(map_3d(&tm.b[1], ts.pre_s, 1, T, hs, 64));
+      tm.b3[0] = tm.b[0]; tm.b3[1] = tm.b[1];
+    }
+    NIMG_TRY(bwd_grouped(BWD_W2, tc, false, P, tm, sms, d, st));
+  }
+  mark(3, st);
+  // 5. dX = dH [W1; W3]
+  {
+    BwdParams P;
+    memset(&P, 0, sizeof(P));
+    memset(&tm, 0, sizeof(tm));
+    P.bank[0] = BwdBank{w.dh_r, 2 * (int64_t)h, p->w1, p->w3, 0, nullptr, w.dx_r, nullptr, dd, 0, dd, 2 * h, h, 0, 0};
+    P.bank[1] = BwdBank{w.dh_s, 2 * (int64_t)hs, p->sw1, p->sw3, 0, nullptr, w.dx_s, nullptr, dd, 0, dd, 2 * hs, hs, 0, 0};
+    if (tc) {
+      NIMG_TRY(map_2d(&tm.a[0], w.dh_r, R, 2 * h, 128));
+      NIMG_TRY(map_3d(&tm.b[0], p->w1, E, h, dd, 64));
+      NIMG_TRY(map_3d(&tm.b3[0], p->w3, E, h, dd, 64));
+      NIMG_TRY(map_2d(&tm.a[1], w.dh_s, T, 2 * hs, 128));
+      NIMG_TRY(map_3d(&tm.b[1], p->sw1, 1, hs, dd, 64));
+      NIMG_TRY(map_3d(&tm.b3[1], p->sw3, 1, hs, dd, 64));
+    }
+    NIMG_TRY(bwd_grouped(BWD_D1, tc, bf, P, tm, sms, d, st));
+  }
+  mark(4, st);
+  // 6. [dW1; dW3] = dH^T X
+  {
+    BwdParams P;
+    memset(&P, 0, sizeof(P));
+    memset(&tm, 0, sizeof(tm));
+    P.bank[0] = BwdBank{w.dh_r, 2 * (int64_t)h, ts.xg, nullptr, dd, nullptr, g->g_w1, g->g_w3, 0, 2 * h, dd, 0, h, 0, 0};
+    P.bank[1] = BwdBank{w.dh_s, 2 * (int64_t)hs, p->x_mod, nullptr, dd, nullptr, g->g_sw1, g->g_sw3, 0, 2 * hs, dd, 0, hs, 0, 0};
+    if (tc) {
+      NIMG_TRY(map_3d(&tm.a[0], w.dh_r, E, rows_e, 2 * h, 64));
+      NIMG_TRY(map_3d(&tm.b[0], ts.xg, E, rows_e, dd, 64));
+      NIMG_TRY(map_3d(&tm.a[1], w.dh_s, 1, T, 2 * hs, 64));
+      NIMG_TRY(map_3d(&tm.b[1], p->x_mod, 1, T, dd, 64));
+      tm.b3[0] = tm.b[0]; tm.b3[1] = tm.b[1];
+    }
+    NIMG_TRY(bwd_grouped(BWD_W1, tc, bf, P, tm, sms, d, st));
+  }
+  mark(5, st);
+  // 7. gather pullback: g_x_mod[t] = dX_shared[t] + sum of its routed dX rows
+  CUDA_TRY(launch_combine(tc, bf, w.dx_r, w.dx_s, nullptr, ro.comb_rows, ro.comb_cnt, g->g_x_mod, T,
+                          dd, E, st));
+  mark(6, st);
+  return NIMG_OK;
 }
 
 static size_t block_extra_bytes(const nimg_moe_desc* d) {

@@ -239,6 +239,21 @@ NIMG_DEV uint64_t make_sdesc_k128(uint32_t smem_addr) {
   return d;
 }
 
+// UMMA shared-memory descriptor, MN-major operand, 128B swizzle (canonical
+// ((8,n),(8,k)):((1,LBO),(8,SBO)) in 16-B units): each k row holds 64
+// MN-contiguous bf16 (128 B), 8 k rows form a 1024-B swizzle atom (SBO apart),
+// and successive 64-wide MN chunks sit `lbo_bytes` apart. This is exactly
+// what a TMA box {64 (MN), k rows} with SWIZZLE_128B lands.
+NIMG_DEV uint64_t make_sdesc_mn128(uint32_t smem_addr, uint32_t lbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;   // LBO: MN-chunk stride
+  d |= (uint64_t)(1024 >> 4) << 32;                    // SBO: 8-k-row group stride
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
 // Instruction descriptor: kind::f16, A/B bf16, D fp32, K-major A and B.
 __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
   return (1u << 4)                       // D format f32
@@ -246,6 +261,10 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
          | (1u << 10)                    // B bf16
          | ((uint32_t)(N >> 3) << 17)    // N
          | ((uint32_t)(M >> 4) << 24);   // M
+}
+// Same with per-operand major-ness (bit 15: A MN-major, bit 16: B MN-major).
+__host__ __device__ constexpr uint32_t make_idesc_bf16_major(int M, int N, bool a_mn, bool b_mn) {
+  return make_idesc_bf16(M, N) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16);
 }
 
 // ---------------------------------------------------------------- numpy sum

@@ -96,7 +96,14 @@ __global__ void __launch_bounds__(NT) grouped_simt_kernel(const __grid_constant_
       const int c = n0 + tx * 4 + j;
       if (c >= bk.N) continue;
       float v = acc[i][j];
-      if (MODE == 0) v = v / (1.0f + expf(-v)) * acc3[i][j];
+      if (MODE == 0) {
+        if (bk.h_out != nullptr) {   // training forward: keep h1 | h3 for the pullback
+          float* hrow = bk.h_out + (int64_t)(row0 + r) * (2 * bk.N);
+          hrow[c] = v;
+          hrow[bk.N + c] = acc3[i][j];
+        }
+        v = v / (1.0f + expf(-v)) * acc3[i][j];
+      }
       o[c] = v;
     }
   }

@@ -76,6 +76,24 @@ NIMG_DEV void decode_tile(const GroupedParams& p, int t, TileInfo& ti) {
 
 NIMG_DEV float silu_mul(float a, float g) { return a / (1.0f + __expf(-a)) * g; }
 
+// Training forward: h1 (16 columns at n) and h3 of one row -> h_out row (h1 | h3).
+NIMG_DEV void store_h1h3(const GBank& bk, int64_t row, int n, const uint32_t (&a)[16],
+                         const uint32_t (&g)[16]) {
+  uint32_t p1[8], p3[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    p1[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
+    p3[j] = pack_bf16x2(__uint_as_float(g[2 * j]), __uint_as_float(g[2 * j + 1]));
+  }
+  bf16* hrow = reinterpret_cast<bf16*>(bk.h_out) + row * (int64_t)(2 * bk.N);
+  uint4* d1 = reinterpret_cast<uint4*>(hrow + n);
+  uint4* d3 = reinterpret_cast<uint4*>(hrow + bk.N + n);
+  d1[0] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+  d1[1] = make_uint4(p1[4], p1[5], p1[6], p1[7]);
+  d3[0] = make_uint4(p3[0], p3[1], p3[2], p3[3]);
+  d3[1] = make_uint4(p3[4], p3[5], p3[6], p3[7]);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
 grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ GroupedParams p) {
@@ -209,6 +227,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
             dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            if (bk.h_out != nullptr) store_h1h3(bk, ti.a_row + r, ti.n0 + c * 16, a, g);
           }
         }
       } else {
@@ -462,11 +481,10 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
       bf16* orow = reinterpret_cast<bf16*>(bk.out) + (int64_t)(ti.a_row + row) * bk.out_ld + ti.n0;
 #pragma unroll 1
       for (int c = 0; c < C::BN_OUT / 16; ++c) {
-        uint32_t a[16];
+        uint32_t a[16], g[16];
         tmem_ld16(tb + c * 16, a);
         uint32_t pk[8];
         if (MODE == 0) {
-          uint32_t g[16];
           tmem_ld16(tb + C::B_ROWS + c * 16, g);
           tmem_ld_wait();
 #pragma unroll
@@ -483,6 +501,8 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
           dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          if (MODE == 0 && bk.h_out != nullptr)   // training forward: keep h1 | h3
+            store_h1h3(bk, ti.a_row + row, ti.n0 + c * 16, a, g);
         }
       }
       tc_fence_before();

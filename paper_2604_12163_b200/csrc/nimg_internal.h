@@ -21,6 +21,7 @@ struct GBank {
   int pad_;
   const int32_t* a_idx;  // GEMM1 only: A row r is source row a_idx[r]; null = contiguous
   const void* a_src;     // gather source rows (bf16, K elements per row) when a_idx != null
+  void* h_out;           // GEMM1, training forward: h1 | h3 rows (2N bf16 per row) or null
 };
 
 // Segments [0, nseg0) use bank 0, [nseg0, nseg) bank 1. Segment i covers rows
@@ -51,6 +52,7 @@ struct SimtBank {
   float* out;        // [rows, N] fp32
   int64_t out_ld;
   int K, N, ntn, pad_;
+  float* h_out;      // GEMM1, training forward: h1 | h3 rows (2N fp32 per row) or null
 };
 struct SimtParams {
   SimtBank bank[2];
@@ -60,6 +62,51 @@ struct SimtParams {
   int seg_rows[kMaxSeg];
   int seg_expert[kMaxSeg];
 };
+
+// Backward grouped GEMMs (backward_kernels.cu SIMT, grouped_gemm_bwd_sm100.cu
+// tcgen05). Modes: see backward_kernels.cu.
+enum { BWD_D2 = 0, BWD_D1 = 1, BWD_W2 = 2, BWD_W1 = 3 };
+struct BwdBank {
+  const void* a;     // D2: dY rows [rows, K=d]; D1: dH rows [rows, 2h]; W2: dY rows [rows, M=d];
+                     // W1: dH rows [rows, M=2h]
+  int64_t a_ld;
+  const void* b;     // D2: W2 [E][d][h]; D1: W1 [E][h][d]; W modes: row operand (pre / X) [rows, N]
+  const void* b3;    // D1: W3 [E][h][d]
+  int64_t b_ld;      // W modes: row stride of b
+  const void* aux;   // D2: H rows (h1 | h3, 2h per row)
+  void* out;         // D2: dH rows (2h); D1: dX rows (out_ld); W2: dW2 [E][d][h]; W1: dW1 [E][h][d]
+  void* out3;        // W1: dW3 [E][h][d]
+  int64_t out_ld;
+  int M, N, K, h;    // D modes: K (= d or 2h), N; W modes: M, N (K = segment rows)
+  int ntn, ntm;
+};
+struct BwdParams {
+  BwdBank bank[2];
+  int nseg, total_tiles;
+  int seg_tile0[kMaxSeg + 1];
+  int seg_row0[kMaxSeg];
+  int seg_rows[kMaxSeg];
+  int seg_expert[kMaxSeg];
+  int seg_bank[kMaxSeg];
+};
+int simt_bwd_bm();
+int simt_bwd_bn();
+cudaError_t launch_grouped_simt_bwd(int mode, bool b_bf16, const BwdParams& p, cudaStream_t s);
+// tcgen05 backward GEMMs (bf16 operands, MN-major where the pullback needs a
+// transposed operand): tile rows 128, N tile tc_bwd_bn(mode).
+int tc_bwd_bn(int mode);
+cudaError_t launch_grouped_tc_bwd(int mode, const TmapSet& tm, const BwdParams& p, int num_sms,
+                                  cudaStream_t stream);
+cudaError_t launch_combine_bwd(bool g_bf16, bool y_bf16, bool dy_bf16, const void* g_out,
+                               const void* yr, const float* gates, const float* gate_raw,
+                               const int32_t* comb_rows, const int32_t* comb_cnt,
+                               const float* logits, void* dyr, void* dys, float* dlogits, int64_t T,
+                               int d, int E, int rows_per_expert, float eps32, float alpha32,
+                               cudaStream_t s);
+size_t router_bwd_part_bytes(int64_t T, int d, int E);
+cudaError_t launch_router_bwd(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
+                              const float* dl, void* dx, float* g_wr, float* g_t, float* part,
+                              float* colsum, int B, int S, int d, int E, cudaStream_t s);
 
 // Launch with programmatic stream serialization (PDL) unless NIMG_PDL=0. The
 // kernel must call pdl_wait() before touching global memory (common.cuh).

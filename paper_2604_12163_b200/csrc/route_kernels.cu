@@ -897,7 +897,7 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
   for (int k = lane; k < cnt; k += 32) {
     const int32_t r = comb_rows[t * E + k];
     rows[k] = r;
-    gl[k] = gates[r];
+    gl[k] = gates != nullptr ? gates[r] : 1.0f;   // null: unit gates (gather pullback)
   }
   __syncwarp();
   constexpr int STEP = 32 * VEC;

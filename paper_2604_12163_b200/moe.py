@@ -152,7 +152,10 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
     """moe.py:138-164 -- route on x_norm + t_emb, experts on x_mod.
 
     Returns (B, S, d) in the activation dtype of x_mod (fp32 or bf16); with
-    return_routing, (out, decisions, routing) like the reference.
+    return_routing, (out, decisions, routing) like the reference. When grad
+    mode is on and any input or expert weight requires grad, the layer is
+    recorded on the autograd tape (training forward + nimg_moe_backward), the
+    way the reference's moe_forward records tape nodes.
     """
     B, S, d = x.shape
     cfg.validate_weight(w_r)
@@ -175,6 +178,14 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
     _, h, hs = _check_bank_shapes(w.w1, w.w3, w.w2, w.shared_w1, w.shared_w3, w.shared_w2, d)
 
     desc = make_desc(B, S, d, E, cap, h, hs, cfg, act)
+    if _wants_grad(xn, xm, te, wr, w.w1, w.w3, w.w2, w.shared_w1, w.shared_w3, w.shared_w2):
+        meta = {"desc": desc, "shape": (B, S, d, E, cap, h, hs)}
+        out = _MoELayerFn.apply(meta, xn, xm, te, wr, w.w1, w.w3, w.w2, w.shared_w1,
+                                w.shared_w3, w.shared_w2)
+        if return_routing:
+            decisions, routing = build_routing(meta["route"], B, S, E, cap)
+            return out, decisions, routing
+        return out
     nbytes = C.c_size_t()
     _lib.check(_lib.lib.nimg_moe_workspace_bytes(C.byref(desc), C.byref(nbytes)))
     ws = workspace(nbytes.value)
@@ -189,6 +200,67 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
         decisions, routing = build_routing(r, B, S, E, cap)
         return out, decisions, routing
     return out
+
+
+def _wants_grad(*ts) -> bool:
+    return torch.is_grad_enabled() and any(isinstance(t, torch.Tensor) and t.requires_grad
+                                           for t in ts)
+
+
+def _sizeof(fn, desc) -> int:
+    n = C.c_size_t()
+    _lib.check(fn(C.byref(desc), C.byref(n)))
+    return n.value
+
+
+class _MoELayerFn(torch.autograd.Function):
+    """moe_forward on the autograd tape: nimg_moe_forward_train keeps what the
+    pullback needs; backward() is nimg_moe_backward -- the gradients the
+    reference's backward(tape, loss) accumulates through moe.py:138-164
+    (tensor.py:590-628): x_norm, x_mod, t_emb, w_r and every expert weight."""
+
+    @staticmethod
+    def forward(ctx, meta, xn, xm, te, wr, w1, w3, w2, sw1, sw3, sw2):
+        desc = meta["desc"]
+        B, S, d, E, cap, h, hs = meta["shape"]
+        dev = xm.device
+        ws = workspace(_sizeof(_lib.lib.nimg_moe_workspace_bytes, desc))
+        state = workspace(_sizeof(_lib.lib.nimg_moe_train_state_bytes, desc))
+        out = torch.empty((B, S, d), dtype=xm.dtype, device=dev)
+        r = alloc_route_out(B, S, E, cap, dev)
+        ptrs = _lib.MoePtrs(ptr(xn), ptr(xm), ptr(te), ptr(wr), ptr(w1), ptr(w3), ptr(w2),
+                            ptr(sw1), ptr(sw3), ptr(sw2), ptr(out), route_struct(r))
+        _lib.check(_lib.lib.nimg_moe_forward_train(C.byref(desc), C.byref(ptrs), ptr(state),
+                                                   state.numel(), ptr(ws), ws.numel(),
+                                                   stream_handle()))
+        meta["route"] = r
+        ctx.meta, ctx.r, ctx.state = meta, r, state
+        ctx.save_for_backward(xn, xm, te, wr, w1, w3, w2, sw1, sw3, sw2)
+        return out
+
+    @staticmethod
+    def backward(ctx, g_out):
+        xn, xm, te, wr, w1, w3, w2, sw1, sw3, sw2 = ctx.saved_tensors
+        desc, r = ctx.meta["desc"], ctx.r
+        g_out = g_out.to(xm.dtype).contiguous()
+        ws = workspace(_sizeof(_lib.lib.nimg_moe_backward_workspace_bytes, desc))
+        f32 = torch.float32
+        g = {"x_norm": torch.empty_like(xn), "x_mod": torch.empty_like(xm),
+             "t_emb": torch.empty(te.shape, dtype=f32, device=xm.device),
+             "w_r": torch.empty(wr.shape, dtype=f32, device=xm.device)}
+        for k, t in (("w1", w1), ("w3", w3), ("w2", w2), ("sw1", sw1), ("sw3", sw3),
+                     ("sw2", sw2)):
+            g[k] = torch.empty(t.shape, dtype=f32, device=xm.device)
+        ptrs = _lib.MoePtrs(ptr(xn), ptr(xm), ptr(te), ptr(wr), ptr(w1), ptr(w3), ptr(w2),
+                            ptr(sw1), ptr(sw3), ptr(sw2), None, route_struct(r))
+        grads = _lib.MoeGrads(ptr(g_out), *(ptr(g[k]) for k in ("x_norm", "x_mod", "t_emb", "w_r",
+                                                                 "w1", "w3", "w2", "sw1", "sw3",
+                                                                 "sw2")))
+        _lib.check(_lib.lib.nimg_moe_backward(C.byref(desc), C.byref(ptrs), ptr(ctx.state),
+                                              ctx.state.numel(), C.byref(grads), ptr(ws),
+                                              ws.numel(), stream_handle()))
+        return (None, g["x_norm"], g["x_mod"], g["t_emb"], g["w_r"], g["w1"], g["w3"], g["w2"],
+                g["sw1"], g["sw3"], g["sw2"])
 
 
 class MoEPlan:

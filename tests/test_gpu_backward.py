@@ -1,0 +1,151 @@
+"""GPU parity of the layer's backward: the CUDA pullback
+(operator API -> autograd -> nimg_moe_backward) against gradients written by
+the reference's own Tape/backward (tests/golden/bwd_*.npz) and against the
+CPU oracle's restated pullbacks at full width.
+
+Bars: Frobenius rel-err per gradient <= 1e-4 (fp32 mode: CUDA-core path,
+fp32 intermediates) and <= 2e-2 (bf16 mode: tcgen05 path, bf16 intermediates,
+fp32 accumulation) -- the north star's layer-output tolerances applied to
+each gradient.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import nimg_oracle as O
+from oracle.workloads import bf16_round, make_layer_inputs
+from tests import golden_cases as G
+from tests.gpu_helpers import TOL_BF16, TOL_FP32, np_of, rel_fro, to_gpu
+
+pytestmark = pytest.mark.gpu
+
+GRADS = ("x_norm", "x_mod", "t_emb", "w_r", "w1", "w3", "w2", "sw1", "sw3", "sw2")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2604_12163_b200 import _lib as L
+    return L
+
+
+def _run(inp, p, g_out, mode):
+    """Product path: reference-style Tape / backward over moe_forward."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    from paper_2604_12163_b200 import tensor as nt
+    g = to_gpu(inp, mode)
+    for k in GRADS:
+        g[k].requires_grad_(True)
+    cfg = R.RouterConfig(d_model=p["d"], n_experts=p["E"], capacity_factor=p["C"],
+                         gate_scale=p.get("gate_scale", 1.0))
+    bank = M.ExpertBank(g["w1"], g["w3"], g["w2"], g["sw1"], g["sw3"], g["sw2"])
+    act = torch.bfloat16 if mode == "bf16" else torch.float32
+    gt = torch.from_numpy(np.ascontiguousarray(g_out)).cuda().to(act)
+    with nt.Tape() as tape:
+        out = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg, bank, g["w_r"])
+        loss = (out.float() * gt.float()).sum()
+    nt.backward(tape, loss)
+    torch.cuda.synchronize()
+    return out, {k: g[k].grad for k in GRADS}
+
+
+@pytest.mark.parametrize("name", G.names("moe_bwd"))
+def test_backward_vs_reference_golden(name):
+    kind, p, inp, exp = G.case(name)
+    tol = TOL_BF16 if p["mode"] == "bf16" else TOL_FP32
+    out, grads = _run(inp, p, inp["g_out"], p["mode"])
+    assert rel_fro(np_of(out), exp["out"]) <= tol
+    for k in GRADS:
+        err = rel_fro(np_of(grads[k]), exp[f"grad_{k}"])
+        assert err <= tol, (k, err)
+
+
+def test_backward_full_width_bf16_vs_oracle():
+    """d=2048, h=1344, E=64 (cfg2 width) on one sample: tcgen05 pullback GEMMs
+    against the oracle's f64 pullbacks."""
+    B, S, d, E, h, C = 1, 512, 2048, 64, 1344, 4.0
+    inp = make_layer_inputs(41, B, S, d, E, h, layer=17, mode="bf16")
+    g_out = bf16_round(np.random.default_rng(42).standard_normal((B, S, d)).astype(np.float32))
+    p = dict(d=d, E=E, C=C)
+    out, grads = _run(inp, p, g_out, "bf16")
+    ref = O.moe_backward(*(inp[k] for k in GRADS), g_out, capacity_factor=C)
+    for k in GRADS:
+        err = rel_fro(np_of(grads[k]), ref[k])
+        assert err <= TOL_BF16, (k, err)
+
+
+def test_backward_cuda_core_path_bf16_ragged_width():
+    """bf16 layer whose h is not a multiple of 64: the training path runs on
+    CUDA cores (fp32 intermediates) -- same bar."""
+    B, S, d, E, h, C = 2, 96, 192, 8, 80, 2.0
+    inp = make_layer_inputs(43, B, S, d, E, h, mode="bf16")
+    g_out = bf16_round(np.random.default_rng(44).standard_normal((B, S, d)).astype(np.float32))
+    out, grads = _run(inp, dict(d=d, E=E, C=C), g_out, "bf16")
+    ref = O.moe_backward(*(inp[k] for k in GRADS), g_out, capacity_factor=C)
+    for k in GRADS:
+        err = rel_fro(np_of(grads[k]), ref[k])
+        assert err <= TOL_BF16, (k, err)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_backward_deterministic(mode):
+    """Fixed-order reductions everywhere (no atomics): two passes, same bits."""
+    B, S, d, E, h, C = 2, 128, 256, 8, 128, 2.0
+    inp = make_layer_inputs(45, B, S, d, E, h, mode=mode)
+    g_out = bf16_round(np.random.default_rng(46).standard_normal((B, S, d)).astype(np.float32))
+    p = dict(d=d, E=E, C=C)
+    _, g1 = _run(inp, p, g_out, mode)
+    _, g2 = _run(inp, p, g_out, mode)
+    for k in GRADS:
+        assert torch.equal(g1[k], g2[k]), k
+
+
+@pytest.mark.parametrize("mode", ["fp32", "bf16"])
+def test_training_forward_matches_inference_forward(mode):
+    """The taped forward (which also stores h1 | h3, pre, Y) returns the same
+    bits as the inference forward on the same path."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    B, S, d, E, h, C = 2, 128, 256, 8, 128, 2.0
+    inp = make_layer_inputs(47, B, S, d, E, h, mode=mode)
+    g = to_gpu(inp, mode)
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    bank = M.ExpertBank(g["w1"], g["w3"], g["w2"], g["sw1"], g["sw3"], g["sw2"])
+    with torch.no_grad():
+        y0 = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg, bank, g["w_r"])
+    xm = g["x_mod"].clone().requires_grad_(True)
+    y1 = M.moe_forward(xm, g["x_norm"], xm, g["t_emb"], cfg, bank, g["w_r"])
+    assert y1.requires_grad
+    assert torch.equal(y0, y1.detach())
+
+
+def test_router_weight_and_x_norm_receive_grad():
+    """test_moe.py:239-249 restated: loss = sum(out * out) gives w_r and x_norm
+    non-zero gradients (the gates stay on the tape)."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    from paper_2604_12163_b200 import tensor as nt
+    rng = np.random.default_rng(12)
+    B, S, d, E, C, h = 1, 6, 4, 3, 2.0, 4
+    f = lambda *s: torch.tensor(rng.normal(size=s), dtype=torch.float32, device="cuda")
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    bank = M.ExpertBank(f(E, h, d), f(E, h, d), f(E, d, h), f(h, d), f(h, d), f(d, h))
+    w_r, x, x_norm, x_mod, t_emb = f(2 * d, E), f(B, S, d), f(B, S, d), f(B, S, d), f(B, d)
+    w_r.requires_grad_(True)
+    x_norm.requires_grad_(True)
+    with nt.Tape() as tape:
+        out = M.moe_forward(x, x_norm, x_mod, t_emb, cfg, bank, w_r)
+        loss = (out * out).sum()
+    nt.backward(tape, loss)
+    assert w_r.grad is not None and bool(torch.any(w_r.grad != 0))
+    assert x_norm.grad is not None and bool(torch.any(x_norm.grad != 0))
+    # backward twice accumulates (tensor.py:64-70 behaviour)
+    g1 = w_r.grad.clone()
+    with nt.Tape() as tape:
+        out = M.moe_forward(x, x_norm, x_mod, t_emb, cfg, bank, w_r)
+        loss = (out * out).sum()
+    nt.backward(tape, loss)
+    torch.testing.assert_close(w_r.grad, 2 * g1)
