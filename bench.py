@@ -280,6 +280,9 @@ def run_single(args, c, peaks, peak_kind):
     # fused prologue + layer + gated residual in the combine epilogue
     block = run_block(args, c, inp, cfg, bank, ms)
 
+    # ---- training step: forward (keeping the pullback's inputs) + backward
+    train = None if args.no_train else run_train(args, c, inp, cfg, bank, tf_peak)
+
     # ---- e2e through the public API with host buffers
     e2e = run_e2e(args, c, inp, cfg, bank)
 
@@ -314,6 +317,7 @@ def run_single(args, c, peaks, peak_kind):
                      "algorithmic": f"4*d*h*(R_rows+T) = {wc['flops_g1']:.4g} FLOP per launch"},
         "stages": stage_detail,
         "block": block,
+        "train": train,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": 8 * args.steps,
@@ -424,6 +428,75 @@ def run_stack(args, peaks, peak_kind):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_train(args, c, inp, cfg, bank, tf_peak):
+    """Training step of the layer: nimg_moe_forward_train
+    + nimg_moe_backward on the same workload (MoETrainPlan; the autograd path of
+    moe_forward makes the same two calls). Backward stage events come from the
+    library (nimg_profile_events)."""
+    import ctypes as C
+    import torch
+    from paper_2604_12163_b200 import _lib
+    from paper_2604_12163_b200 import moe as M
+    wc = work_counts(c)
+    plan = M.MoETrainPlan(cfg, bank, c["B"], c["S"], torch.bfloat16)
+    g = torch.Generator(device="cuda").manual_seed(c["seed"] + 200)
+    g_out = torch.randn(c["B"], c["S"], c["d"], generator=g, device="cuda").to(torch.bfloat16)
+    args_in = (inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"])
+
+    def step():
+        plan.forward(*args_in)
+        plan.backward(g_out)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    fwd_ms = bwd_ms = 0.0
+    for _ in range(args.steps):
+        e0.record()
+        plan.forward(*args_in)
+        e1.record()
+        plan.backward(g_out)
+        e2.record()
+        torch.cuda.synchronize()
+        fwd_ms += e0.elapsed_time(e1) / args.steps
+        bwd_ms += e1.elapsed_time(e2) / args.steps
+    # backward stages: [0] start [1] combine+router pullbacks [2] dH [3] dW2 [4] dX [5] dW1|dW3 [6] g_x_mod
+    n_ev = 7
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    for row in evs:
+        for e in row:
+            e.record()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        plan.forward(*args_in)
+        arr = (C.c_void_p * n_ev)(*[e.cuda_event for e in evs[k]])
+        _lib.check(_lib.lib.nimg_profile_events(arr, n_ev))
+        plan.backward(g_out)
+        _lib.check(_lib.lib.nimg_profile_events(None, 0))
+    torch.cuda.synchronize()
+    names = ["combine_router_pullback", "dgrad2_swiglu", "wgrad2", "dgrad1", "wgrad1", "gather_pullback"]
+    st = {n: sum(evs[k][i].elapsed_time(evs[k][i + 1]) for k in range(args.steps)) / args.steps
+          for i, n in enumerate(names)}
+    rt = wc["R"] + wc["T"]
+    d, h = c["d"], c["h"]
+    fl = {"dgrad2_swiglu": 2.0 * d * h * rt, "wgrad2": 2.0 * d * h * rt,
+          "dgrad1": 4.0 * d * h * rt, "wgrad1": 4.0 * d * h * rt}
+    gemm_ms = sum(st[k] for k in fl)
+    bwd_tf = sum(fl.values()) / (gemm_ms * 1e-3) / 1e12
+    return {
+        "ms_per_step": fwd_ms + bwd_ms, "fwd_ms": fwd_ms, "bwd_ms": bwd_ms,
+        "tokens_per_s": wc["T"] / ((fwd_ms + bwd_ms) * 1e-3),
+        "bwd_stages_ms": st,
+        "bwd_gemm_tflops": {k: fl[k] / (st[k] * 1e-3) / 1e12 for k in fl},
+        "bwd_expert_gemm_tflops": bwd_tf,
+        "bwd_expert_gemm_frac_of_peak": bwd_tf / tf_peak,
+        "what": "one layer training step: forward keeping h1|h3, pre, Y (nimg_moe_forward_train) + "
+                "full backward to x_norm, x_mod, t_emb, W_r and all expert weights (nimg_moe_backward)",
+        "algorithmic": f"backward expert GEMMs 12*d*h*(R_rows+T) = {sum(fl.values()):.4g} FLOP",
+    }
 
 
 def run_block(args, c, inp, cfg, bank, layer_ms):
@@ -700,6 +773,7 @@ def main():
                     help="override the config's capacity factor C (cfg3 sweep: 8, 4, 2)")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the training-step leg")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-overlap", action="store_true", help="EP: plain all-to-alls")
     ap.add_argument("--ep-transport", default="ce", choices=["ce", "nccl"],

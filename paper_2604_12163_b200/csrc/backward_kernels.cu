@@ -70,8 +70,8 @@ combine_bwd_kernel(const TG* __restrict__ g_out, const TY* __restrict__ yr,
                    const float* __restrict__ gates, const float* __restrict__ gate_raw,
                    const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
                    const float* __restrict__ logits, TD* __restrict__ dyr, TD* __restrict__ dys,
-                   float* __restrict__ dlogits, int64_t T, int d, int E, int rows_per_expert,
-                   float eps32, float alpha32) {
+                   float* __restrict__ dlogits, bf16* __restrict__ dl16, int64_t T, int d, int E,
+                   int rows_per_expert, float eps32, float alpha32) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
@@ -86,34 +86,61 @@ combine_bwd_kernel(const TG* __restrict__ g_out, const TY* __restrict__ yr,
   for (int e = lane; e < E; e += 32) gsc[e] = 0.0;
   __syncwarp();
   const TG* g = g_out + t * d;
-  // dY rows (mul bwd: g * gate) and dgate = sum_c g * Y (mul + broadcast_to bwd)
-  for (int k = 0; k < cnt; ++k) {
-    const int64_t r = rows[k];
-    const float gate = __ldg(gates + r);
-    const TY* y = yr + r * d;
-    TD* o = dyr + r * d;
-    float dot = 0.f;
-    if constexpr (VEC8) {
+  // dY rows (mul bwd: g * gate) and dgate = sum_c g * Y (mul + broadcast_to bwd);
+  // NB rows at a time so their loads are in flight together
+  if constexpr (VEC8) {
+    constexpr int NB = 4;
+    for (int k0 = 0; k0 < cnt; k0 += NB) {
+      float gate[NB], dot[NB];
+      const TY* y[NB];
+      TD* o[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int64_t r = rows[k0 + q < cnt ? k0 + q : k0];
+        gate[q] = __ldg(gates + r);
+        y[q] = yr + r * d;
+        o[q] = dyr + r * d;
+        dot[q] = 0.f;
+      }
       for (int c = lane * 8; c < d; c += 256) {
         V8<TG> gv; gv.load(g + c);
-        V8<TY> yv; yv.load(y + c);
-        float res[8];
+        V8<TY> yv[NB];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          dot = fmaf(gv.at(i), yv.at(i), dot);
-          res[i] = gv.at(i) * gate;
+        for (int q = 0; q < NB; ++q)
+          if (k0 + q < cnt) yv[q].load(y[q] + c);
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+          if (k0 + q >= cnt) continue;
+          float res[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            dot[q] = fmaf(gv.at(i), yv[q].at(i), dot[q]);
+            res[i] = gv.at(i) * gate[q];
+          }
+          store8(o[q] + c, res);
         }
-        store8(o + c, res);
       }
-    } else {
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const float v = warp_sum_f(dot[q]);
+        if (lane == 0 && k0 + q < cnt) dg[k0 + q] = v;
+      }
+    }
+  } else {
+    for (int k = 0; k < cnt; ++k) {
+      const int64_t r = rows[k];
+      const float gate = __ldg(gates + r);
+      const TY* y = yr + r * d;
+      TD* o = dyr + r * d;
+      float dot = 0.f;
       for (int c = lane; c < d; c += 32) {
         const float gvv = to_f32(g[c]);
         dot = fmaf(gvv, to_f32(y[c]), dot);
         o[c] = from_f32<TD>(gvv * gate);
       }
+      dot = warp_sum_f(dot);
+      if (lane == 0) dg[k] = dot;
     }
-    dot = warp_sum_f(dot);
-    if (lane == 0) dg[k] = dot;
   }
   if (dys != nullptr) {   // shared-expert upstream gradient in the dY dtype
     TD* o = dys + t * d;
@@ -160,7 +187,9 @@ combine_bwd_kernel(const TG* __restrict__ g_out, const TY* __restrict__ yr,
   gs = warp_sum_d(gs);
   for (int e = lane; e < E; e += 32) {
     const double s = exp((double)__ldg(lg + e) - m) / se;
-    dlogits[t * E + e] = (float)(s * (gsc[e] - gs));
+    const float v = (float)(s * (gsc[e] - gs));
+    dlogits[t * E + e] = v;
+    if (dl16 != nullptr) dl16[t * E + e] = __float2bfloat16_rn(v);
   }
 }
 
@@ -435,9 +464,10 @@ cudaError_t launch_grouped_simt_bwd(int mode, bool b_bf16, const BwdParams& p, c
 cudaError_t launch_combine_bwd(bool g_bf16, bool y_bf16, bool dy_bf16, const void* g_out,
                                const void* yr, const float* gates, const float* gate_raw,
                                const int32_t* comb_rows, const int32_t* comb_cnt,
-                               const float* logits, void* dyr, void* dys, float* dlogits, int64_t T,
-                               int d, int E, int rows_per_expert, float eps32, float alpha32,
-                               cudaStream_t s) {
+                               const float* logits, void* dyr, void* dys, float* dlogits,
+                               bf16_raw* dl16_raw, int64_t T, int d, int E, int rows_per_expert,
+                               float eps32, float alpha32, cudaStream_t s) {
+  bf16* dl16 = reinterpret_cast<bf16*>(dl16_raw);
   if (T <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)((T + CBB_WARPS - 1) / CBB_WARPS);
   const size_t smem = (size_t)CBB_WARPS * E * 16;
@@ -445,11 +475,11 @@ cudaError_t launch_combine_bwd(bool g_bf16, bool y_bf16, bool dy_bf16, const voi
 #define NIMG_CBB(TG, TY, TD)                                                                       \
   return v8 ? launch_pdl(combine_bwd_kernel<TG, TY, TD, true>, dim3(grid), dim3(CBB_WARPS * 32),  \
                          smem, s, (const TG*)g_out, (const TY*)yr, gates, gate_raw, comb_rows,    \
-                         comb_cnt, logits, (TD*)dyr, (TD*)dys, dlogits, T, d, E,                  \
+                         comb_cnt, logits, (TD*)dyr, (TD*)dys, dlogits, dl16, T, d, E,                  \
                          rows_per_expert, eps32, alpha32)                                          \
             : launch_pdl(combine_bwd_kernel<TG, TY, TD, false>, dim3(grid), dim3(CBB_WARPS * 32), \
                          smem, s, (const TG*)g_out, (const TY*)yr, gates, gate_raw, comb_rows,    \
-                         comb_cnt, logits, (TD*)dyr, (TD*)dys, dlogits, T, d, E,                  \
+                         comb_cnt, logits, (TD*)dyr, (TD*)dys, dlogits, dl16, T, d, E,                  \
                          rows_per_expert, eps32, alpha32)
   // supported combos: tcgen05 path (all bf16); SIMT path (g act, y/dY fp32)
   if (g_bf16 && y_bf16 && dy_bf16) { NIMG_CBB(bf16, bf16, bf16); }
@@ -463,29 +493,46 @@ size_t router_bwd_part_bytes(int64_t T, int d, int E) {
   return (size_t)((T + RW_CHUNK - 1) / RW_CHUNK) * d * E * 4;
 }
 
-cudaError_t launch_router_bwd(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
-                              const float* dl, void* dx, float* g_wr, float* g_t, float* part,
-                              float* colsum, int B, int S, int d, int E, cudaStream_t s) {
-  const int64_t T = (int64_t)B * S;
+cudaError_t launch_router_bwd_simt(bool x_bf16, const void* x_norm, const float* w_r,
+                                   const float* dl, void* dx, float* part, int64_t T, int d, int E,
+                                   cudaStream_t s, int* nchunks) {
+  *nchunks = (int)((T + RW_CHUNK - 1) / RW_CHUNK);
   if (T <= 0) return cudaSuccess;
   const dim3 gdx((unsigned)((T + RB_T - 1) / RB_T), (unsigned)((d + RB_J - 1) / RB_J));
   cudaError_t err = x_bf16
       ? launch_pdl(router_bwd_dx_kernel<bf16>, gdx, dim3(256), 0, s, dl, w_r, (bf16*)dx, T, d, E)
       : launch_pdl(router_bwd_dx_kernel<float>, gdx, dim3(256), 0, s, dl, w_r, (float*)dx, T, d, E);
   if (err != cudaSuccess) return err;
-  const int nchunks = (int)((T + RW_CHUNK - 1) / RW_CHUNK);
-  const dim3 gdw((unsigned)((d + RB_J - 1) / RB_J), (unsigned)((E + RB_J - 1) / RB_J), (unsigned)nchunks);
-  err = x_bf16 ? launch_pdl(router_bwd_dw_partial_kernel<bf16>, gdw, dim3(256), 0, s,
-                            (const bf16*)x_norm, dl, part, T, d, E)
-               : launch_pdl(router_bwd_dw_partial_kernel<float>, gdw, dim3(256), 0, s,
-                            (const float*)x_norm, dl, part, T, d, E);
-  if (err != cudaSuccess) return err;
-  err = launch_pdl(router_bwd_colsum_kernel, dim3((unsigned)((E + 31) / 32), (unsigned)B), dim3(256),
-                   0, s, dl, colsum, S, E);
+  const dim3 gdw((unsigned)((d + RB_J - 1) / RB_J), (unsigned)((E + RB_J - 1) / RB_J), (unsigned)*nchunks);
+  return x_bf16 ? launch_pdl(router_bwd_dw_partial_kernel<bf16>, gdw, dim3(256), 0, s,
+                             (const bf16*)x_norm, dl, part, T, d, E)
+                : launch_pdl(router_bwd_dw_partial_kernel<float>, gdw, dim3(256), 0, s,
+                             (const float*)x_norm, dl, part, T, d, E);
+}
+
+cudaError_t launch_router_bwd_fold(const float* dl, const float* t_emb, const float* w_r,
+                                   const float* part, int nchunks, float* colsum, float* g_wr,
+                                   float* g_t, int B, int S, int d, int E, cudaStream_t s) {
+  if ((int64_t)B * S <= 0) return cudaSuccess;
+  cudaError_t err = launch_pdl(router_bwd_colsum_kernel, dim3((unsigned)((E + 31) / 32), (unsigned)B),
+                               dim3(256), 0, s, dl, colsum, S, E);
   if (err != cudaSuccess) return err;
   const int64_t n = (int64_t)d * E > (int64_t)B * d ? (int64_t)d * E : (int64_t)B * d;
   return launch_pdl(router_bwd_fold_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s,
-                    (const float*)part, nchunks, (const float*)colsum, t_emb, w_r, g_wr, g_t, B, d, E);
+                    part, nchunks, (const float*)colsum, t_emb, w_r, g_wr, g_t, B, d, E);
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+cudaError_t launch_f32_to_bf16(const float* src, bf16_raw* dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  return launch_pdl(f32_to_bf16_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, src,
+                    reinterpret_cast<bf16*>(dst), n);
 }
 
 }  // namespace nimg

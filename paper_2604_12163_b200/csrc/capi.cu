@@ -108,6 +108,22 @@ int map_3d(CUtensorMap* m, const void* base, uint64_t E, uint64_t N, uint64_t K,
   return NIMG_OK;
 }
 
+// fp32 [E, M, N] row-major output (weight gradients), box (32 x 32 x 1),
+// 128-B swizzle: the TMA-store target of the backward weight-gradient tiles.
+int map_3d_f32_out(CUtensorMap* m, void* base, uint64_t E, uint64_t M, uint64_t N) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return fail(NIMG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {N, M, E};
+  cuuint64_t strides[2] = {N * 4, M * N * 4};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NIMG_ERR_CUDA, "tensor map (f32 out) encode failed (%d)", (int)r);
+  return NIMG_OK;
+}
+
 // SMs the persistent GEMMs size their grid by. NIMG_GEMM_MAX_SMS caps it
 // (leaves SMs for concurrently running communication kernels).
 int device_sms(int* out) {
@@ -461,8 +477,11 @@ TrainState train_state_layout(const nimg_moe_desc* d, void* base) {
 struct BwdWs {
   void *dy_r, *dy_s, *dh_r, *dh_s, *dx_r, *dx_s;
   float *dlogits, *colsum, *part;
+  bf16_raw *dl16, *wr16;   // tcgen05 router pullback operands
   size_t bytes;
 };
+// Router pullback on tcgen05 (bf16 layer, TMA-aligned E)
+bool router_bwd_tc(const nimg_moe_desc* d) { return train_use_tc(d) && d->E % 8 == 0; }
 BwdWs bwd_ws_layout(const nimg_moe_desc* d, void* base) {
   BwdWs w{};
   const bool tc = train_use_tc(d);
@@ -479,7 +498,12 @@ BwdWs bwd_ws_layout(const nimg_moe_desc* d, void* base) {
   w.dx_s = take(T * d->d * ei);
   w.dlogits = static_cast<float*>(take(T * d->E * 4));
   w.colsum = static_cast<float*>(take((size_t)d->B * d->E * 4));
-  w.part = static_cast<float*>(take(router_bwd_part_bytes((int64_t)T, (int)d->d, (int)d->E)));
+  const size_t part_simt = router_bwd_part_bytes((int64_t)T, (int)d->d, (int)d->E);
+  const size_t part_tc = (size_t)d->B * d->d * d->E * 4;   // one partial per sample
+  w.part = static_cast<float*>(take(part_simt > part_tc ? part_simt : part_tc));
+  const bool rtc = router_bwd_tc(d);
+  w.dl16 = rtc ? static_cast<bf16_raw*>(take(T * d->E * 2)) : nullptr;
+  w.wr16 = rtc ? static_cast<bf16_raw*>(take((size_t)d->d * d->E * 2)) : nullptr;
   w.bytes = o;
   return w;
 }
@@ -749,9 +773,9 @@ int nimg_moe_backward_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   return NIMG_OK;
 }
 
-static int bwd_grouped(int mode, bool tc, bool b_bf16, BwdParams& P, const TmapSet& tm, int sms,
+static int bwd_grouped(int mode, bool tc, bool b_bf16, BwdParams& P, const TmapSetBwd& tm, int sms,
                        const nimg_moe_desc* d, cudaStream_t st) {
-  const int bm = tc ? 128 : simt_bwd_bm();
+  const int bm = tc ? tc_bwd_tile_rows(mode) : simt_bwd_bm();
   const int bn = tc ? tc_bwd_bn(mode) : simt_bwd_bn();
   NIMG_TRY(fill_bwd_segments(P, mode, d, bm, bn));
   if (tc) CUDA_TRY(launch_grouped_tc_bwd(mode, tm, P, sms, st));
@@ -790,15 +814,75 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
   NIMG_TRY(device_sms(&sms));
   mark(0, st);
   // 1. combine / gate / softmax pullback -> dY rows, dlogits
+  const bool rtc = router_bwd_tc(d);
   CUDA_TRY(launch_combine_bwd(bf, tc, tc, g->g_out, ts.y_r, ro.gates, ro.gate_raw, ro.comb_rows,
-                              ro.comb_cnt, ro.logits, w.dy_r, w.dy_s, w.dlogits, T, dd, E,
+                              ro.comb_cnt, ro.logits, w.dy_r, w.dy_s, w.dlogits, w.dl16, T, dd, E,
                               (int)rows_e, d->gate_eps, d->gate_scale, st));
   // 2. router pullback -> g_x_norm, g_t_emb, g_w_r
-  CUDA_TRY(launch_router_bwd(bf, p->x_norm, p->t_emb, p->w_r, w.dlogits, g->g_x_norm, g->g_w_r,
-                             g->g_t_emb, w.part, w.colsum, (int)d->B, (int)d->S, dd, E, st));
+  int nchunks = 0;
+  if (rtc && d->B > kMaxSeg) return fail(NIMG_ERR_CONFIG, "batch too large for one grouped launch");
+  if (rtc) {
+    // dx_norm = dl W_r[:d]^T: the forward's GEMM2 kernel (A = dl rows, K = E; B = W_r[:d] rows)
+    CUDA_TRY(launch_f32_to_bf16(p->w_r, w.wr16, dd * (int64_t)E, st));
+    {
+      const bool pair = use_pair_kernels();
+      const int bn = tc_bn_out(1), box = pair ? tc_b_box(1) / 2 : tc_b_box(1);
+      const int rows_tile = pair ? tc_pair_rows() : 128;
+      GroupedParams P;
+      memset(&P, 0, sizeof(P));
+      TmapSet tmf;
+      memset(&tmf, 0, sizeof(tmf));
+      NIMG_TRY(map_2d(&tmf.a[0], w.dl16, T, E, 128));
+      NIMG_TRY(map_3d(&tmf.b[0], w.wr16, 1, dd, E, box));
+      tmf.a[1] = tmf.a[0]; tmf.b[1] = tmf.b[0]; tmf.b3[0] = tmf.b[0]; tmf.b3[1] = tmf.b[0];
+      P.bank[0] = GBank{g->g_x_norm, dd, E, dd, (dd + bn - 1) / bn, 0, nullptr, nullptr, nullptr};
+      P.bank[1] = P.bank[0];
+      P.nseg0 = P.nseg = 1;
+      P.seg_row0[0] = 0;
+      P.seg_rows[0] = (int)T;
+      P.seg_expert[0] = 0;
+      P.seg_tile0[0] = 0;
+      P.total_tiles = P.seg_tile0[1] = (int)((T + rows_tile - 1) / rows_tile) * ((dd + bn - 1) / bn);
+      if (pair) CUDA_TRY(launch_grouped_tc_pair(1, tmf, P, sms, st));
+      else CUDA_TRY(launch_grouped_tc(1, tmf, P, sms, st));
+    }
+    // dW_r[:d] partials, one per sample: x_norm[b]^T dl[b] (both MN-major), TMA-stored
+    {
+      BwdParams P;
+      memset(&P, 0, sizeof(P));
+      TmapSetBwd tmr;
+      memset(&tmr, 0, sizeof(tmr));
+      P.bank[0] = BwdBank{p->x_norm, dd, w.dl16, nullptr, E, nullptr, w.part, nullptr, 0, dd, E, 0,
+                          1 << 30, (E + tc_bwd_bn(BWD_WR) - 1) / tc_bwd_bn(BWD_WR), (dd + 127) / 128};
+      P.bank[1] = P.bank[0];
+      int64_t tiles = 0;
+      for (int b = 0; b < (int)d->B; ++b) {
+        P.seg_row0[b] = (int)(b * d->S);
+        P.seg_rows[b] = (int)d->S;
+        P.seg_expert[b] = b;
+        P.seg_bank[b] = 0;
+        P.seg_tile0[b] = (int)tiles;
+        tiles += (int64_t)P.bank[0].ntm * P.bank[0].ntn;
+      }
+      P.nseg = (int)d->B;
+      P.seg_tile0[P.nseg] = P.total_tiles = (int)tiles;
+      NIMG_TRY(map_3d(&tmr.a[0], p->x_norm, d->B, d->S, dd, 64));
+      NIMG_TRY(map_3d(&tmr.b[0], w.dl16, d->B, d->S, E, 64));
+      NIMG_TRY(map_3d_f32_out(&tmr.o[0], w.part, d->B, dd, E));
+      tmr.a[1] = tmr.a[0]; tmr.b[1] = tmr.b[0]; tmr.b3[0] = tmr.b3[1] = tmr.b[0];
+      tmr.o3[0] = tmr.o[0]; tmr.o[1] = tmr.o3[1] = tmr.o[0];
+      CUDA_TRY(launch_grouped_tc_bwd(BWD_WR, tmr, P, sms, st));
+    }
+    nchunks = (int)d->B;
+  } else {
+    CUDA_TRY(launch_router_bwd_simt(bf, p->x_norm, p->w_r, w.dlogits, g->g_x_norm, w.part, T, dd, E,
+                                    st, &nchunks));
+  }
+  CUDA_TRY(launch_router_bwd_fold(w.dlogits, p->t_emb, p->w_r, w.part, nchunks, w.colsum, g->g_w_r,
+                                  g->g_t_emb, (int)d->B, (int)d->S, dd, E, st));
   mark(1, st);
   const void* dys = tc ? g->g_out : w.dy_s;
-  TmapSet tm;
+  TmapSetBwd tm;
   // 3. dH = SwiGLU'(dY W2)
   {
     BwdParams P;
@@ -829,6 +913,9 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
       NIMG_TRY(map_3d(&tm.a[1], dys, 1, T, dd, 64));
       NIMG_TRY(map_3d(&tm.b[1], ts.pre_s, 1, T, hs, 64));
       tm.b3[0] = tm.b[0]; tm.b3[1] = tm.b[1];
+      NIMG_TRY(map_3d_f32_out(&tm.o[0], g->g_w2, E, dd, h));
+      NIMG_TRY(map_3d_f32_out(&tm.o[1], g->g_sw2, 1, dd, hs));
+      tm.o3[0] = tm.o[0]; tm.o3[1] = tm.o[1];
     }
     NIMG_TRY(bwd_grouped(BWD_W2, tc, false, P, tm, sms, d, st));
   }
@@ -864,6 +951,10 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
       NIMG_TRY(map_3d(&tm.a[1], w.dh_s, 1, T, 2 * hs, 64));
       NIMG_TRY(map_3d(&tm.b[1], p->x_mod, 1, T, dd, 64));
       tm.b3[0] = tm.b[0]; tm.b3[1] = tm.b[1];
+      NIMG_TRY(map_3d_f32_out(&tm.o[0], g->g_w1, E, h, dd));
+      NIMG_TRY(map_3d_f32_out(&tm.o3[0], g->g_w3, E, h, dd));
+      NIMG_TRY(map_3d_f32_out(&tm.o[1], g->g_sw1, 1, hs, dd));
+      NIMG_TRY(map_3d_f32_out(&tm.o3[1], g->g_sw3, 1, hs, dd));
     }
     NIMG_TRY(bwd_grouped(BWD_W1, tc, bf, P, tm, sms, d, st));
   }

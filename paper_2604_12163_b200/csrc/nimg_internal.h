@@ -8,6 +8,7 @@
 
 namespace nimg {
 
+typedef uint16_t bf16_raw;   // bf16 storage in host-visible signatures
 constexpr int kMaxSeg = 264;  // routed segments + shared; EP: R * E/R + 1
 
 // One weight bank of a grouped launch: bank 0 = routed experts (3-D weights
@@ -65,7 +66,7 @@ struct SimtParams {
 
 // Backward grouped GEMMs (backward_kernels.cu SIMT, grouped_gemm_bwd_sm100.cu
 // tcgen05). Modes: see backward_kernels.cu.
-enum { BWD_D2 = 0, BWD_D1 = 1, BWD_W2 = 2, BWD_W1 = 3 };
+enum { BWD_D2 = 0, BWD_D1 = 1, BWD_W2 = 2, BWD_W1 = 3, BWD_WR = 4 };
 struct BwdBank {
   const void* a;     // D2: dY rows [rows, K=d]; D1: dH rows [rows, 2h]; W2: dY rows [rows, M=d];
                      // W1: dH rows [rows, M=2h]
@@ -95,18 +96,32 @@ cudaError_t launch_grouped_simt_bwd(int mode, bool b_bf16, const BwdParams& p, c
 // tcgen05 backward GEMMs (bf16 operands, MN-major where the pullback needs a
 // transposed operand): tile rows 128, N tile tc_bwd_bn(mode).
 int tc_bwd_bn(int mode);
-cudaError_t launch_grouped_tc_bwd(int mode, const TmapSet& tm, const BwdParams& p, int num_sms,
+int tc_bwd_tile_rows(int mode);   // 256 for the CTA-pair kernels, else 128
+// Backward tensor maps: operands as TmapSet, plus the weight-gradient outputs
+// (fp32 [E][M][N], stored by TMA from a swizzled staging tile).
+struct __align__(64) TmapSetBwd {
+  CUtensorMap a[2], b[2], b3[2];
+  CUtensorMap o[2], o3[2];   // W modes: dW2 / dW1, dW3 per bank
+};
+cudaError_t launch_grouped_tc_bwd(int mode, const TmapSetBwd& tm, const BwdParams& p, int num_sms,
                                   cudaStream_t stream);
+// dl16 != null: also a bf16 copy of dlogits (A / B operand of the tcgen05 router pullback)
 cudaError_t launch_combine_bwd(bool g_bf16, bool y_bf16, bool dy_bf16, const void* g_out,
                                const void* yr, const float* gates, const float* gate_raw,
                                const int32_t* comb_rows, const int32_t* comb_cnt,
-                               const float* logits, void* dyr, void* dys, float* dlogits, int64_t T,
-                               int d, int E, int rows_per_expert, float eps32, float alpha32,
-                               cudaStream_t s);
+                               const float* logits, void* dyr, void* dys, float* dlogits,
+                               bf16_raw* dl16, int64_t T, int d, int E, int rows_per_expert,
+                               float eps32, float alpha32, cudaStream_t s);
 size_t router_bwd_part_bytes(int64_t T, int d, int E);
-cudaError_t launch_router_bwd(bool x_bf16, const void* x_norm, const float* t_emb, const float* w_r,
-                              const float* dl, void* dx, float* g_wr, float* g_t, float* part,
-                              float* colsum, int B, int S, int d, int E, cudaStream_t s);
+// CUDA-core router pullback: dx_norm and the token-chunk partials of dW_r[:d]
+cudaError_t launch_router_bwd_simt(bool x_bf16, const void* x_norm, const float* w_r,
+                                   const float* dl, void* dx, float* part, int64_t T, int d, int E,
+                                   cudaStream_t s, int* nchunks);
+// sum_s dl -> colsum; fold the partials (fixed order) into g_w_r[:d]; g_w_r[d:], g_t_emb
+cudaError_t launch_router_bwd_fold(const float* dl, const float* t_emb, const float* w_r,
+                                   const float* part, int nchunks, float* colsum, float* g_wr,
+                                   float* g_t, int B, int S, int d, int E, cudaStream_t s);
+cudaError_t launch_f32_to_bf16(const float* src, bf16_raw* dst, int64_t n, cudaStream_t s);
 
 // Launch with programmatic stream serialization (PDL) unless NIMG_PDL=0. The
 // kernel must call pdl_wait() before touching global memory (common.cuh).

@@ -314,3 +314,67 @@ class MoEPlan:
 
     def routing(self, with_decisions: bool = False):
         return build_routing(self.r, self.B, self.S, self.cfg.n_experts, self.cap, with_decisions)
+
+
+class MoETrainPlan:
+    """Pre-planned training step of the layer for a fixed shape (benchmark /
+    trainer path): owns the training state, both workspaces, routing buffers
+    and gradient buffers, so forward() and backward() are one C-ABI call each
+    (nimg_moe_forward_train, nimg_moe_backward) with no allocation. Same
+    arithmetic as the autograd path of moe_forward."""
+
+    def __init__(self, cfg: RouterConfig, bank: ExpertBank, B: int, S: int,
+                 act: torch.dtype = torch.bfloat16):
+        self.cfg, self.B, self.S, self.act = cfg, B, S, act
+        d, E = cfg.d_model, cfg.n_experts
+        self.bank = bank_on_device(bank, act)
+        w = self.bank
+        _, self.h, self.hs = _check_bank_shapes(w.w1, w.w3, w.w2, w.shared_w1, w.shared_w3,
+                                                w.shared_w2, d)
+        self.cap = capacity_for(S, E, cfg.capacity_factor)
+        self.desc = make_desc(B, S, d, E, self.cap, self.h, self.hs, cfg, act)
+        self.ws = workspace(_sizeof(_lib.lib.nimg_moe_workspace_bytes, self.desc))
+        self.state = workspace(_sizeof(_lib.lib.nimg_moe_train_state_bytes, self.desc))
+        self.bws = workspace(_sizeof(_lib.lib.nimg_moe_backward_workspace_bytes, self.desc))
+        dev = self.ws.device
+        self.out = torch.empty((B, S, d), dtype=act, device=dev)
+        self.r = alloc_route_out(B, S, E, self.cap, dev)
+        f32 = torch.float32
+        self.grads = {"x_norm": torch.empty((B, S, d), dtype=act, device=dev),
+                      "x_mod": torch.empty((B, S, d), dtype=act, device=dev),
+                      "t_emb": torch.empty((B, d), dtype=f32, device=dev),
+                      "w_r": torch.empty((2 * d, E), dtype=f32, device=dev)}
+        for k, t in (("w1", w.w1), ("w3", w.w3), ("w2", w.w2), ("sw1", w.shared_w1),
+                     ("sw3", w.shared_w3), ("sw2", w.shared_w2)):
+            self.grads[k] = torch.empty(t.shape, dtype=f32, device=dev)
+        self._inputs = None
+
+    def _ptrs(self, x_norm, x_mod, t_emb, w_r, out):
+        w = self.bank
+        return _lib.MoePtrs(ptr(x_norm), ptr(x_mod), ptr(t_emb), ptr(w_r), ptr(w.w1), ptr(w.w3),
+                            ptr(w.w2), ptr(w.shared_w1), ptr(w.shared_w3), ptr(w.shared_w2),
+                            ptr(out), route_struct(self.r))
+
+    def forward(self, x_norm, x_mod, t_emb, w_r) -> torch.Tensor:
+        """Contiguous CUDA inputs of the plan's dtypes; returns the out buffer."""
+        self._inputs = (x_norm, x_mod, t_emb, w_r)
+        p = self._ptrs(x_norm, x_mod, t_emb, w_r, self.out)
+        _lib.check(_lib.lib.nimg_moe_forward_train(C.byref(self.desc), C.byref(p), ptr(self.state),
+                                                   self.state.numel(), ptr(self.ws),
+                                                   self.ws.numel(), stream_handle()))
+        return self.out
+
+    def backward(self, g_out) -> dict:
+        """Gradients of the last forward() for upstream gradient g_out (act
+        dtype, contiguous); returns the plan's gradient buffers."""
+        if self._inputs is None:
+            raise RuntimeError("backward() before forward()")
+        p = self._ptrs(*self._inputs, None)
+        g = self.grads
+        grads = _lib.MoeGrads(ptr(g_out), *(ptr(g[k]) for k in ("x_norm", "x_mod", "t_emb", "w_r",
+                                                                 "w1", "w3", "w2", "sw1", "sw3",
+                                                                 "sw2")))
+        _lib.check(_lib.lib.nimg_moe_backward(C.byref(self.desc), C.byref(p), ptr(self.state),
+                                              self.state.numel(), C.byref(grads), ptr(self.bws),
+                                              self.bws.numel(), stream_handle()))
+        return g
