@@ -12,6 +12,8 @@ import os
 from .errors import ConfigError, ShapeError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnimg_moe.so")
+# A/B experiments only (tools/): load another in-tree build of the same ABI
+LIB_PATH = os.environ.get("NIMG_LIB_PATH", LIB_PATH)
 
 NIMG_OK, NIMG_ERR_SHAPE, NIMG_ERR_CONFIG, NIMG_ERR_CUDA = 0, 1, 2, 3
 NIMG_F32, NIMG_BF16 = 0, 1

@@ -465,8 +465,9 @@ TrainState train_state_layout(const nimg_moe_desc* d, void* base) {
   size_t o = 0;
   auto take = [&](size_t bytes) { void* q = p ? p + o : nullptr; o += align_up(bytes); return q; };
   s.xg = take(R * d->d * ea);
-  s.h_r = take(R * 2 * d->h * ei);
-  s.h_s = take(T * 2 * d->h_shared * ei);
+  // tcgen05: row-blocked h1 | h3 (hblk_off, 128-row blocks); CUDA cores: row-major fp32
+  s.h_r = take(s.tc ? hblk_elems((int64_t)R, d->h) * 2 : R * 2 * d->h * ei);
+  s.h_s = take(s.tc ? hblk_elems((int64_t)T, d->h_shared) * 2 : T * 2 * d->h_shared * ei);
   s.pre_r = take(R * d->h * ei);
   s.pre_s = take(T * d->h_shared * ei);
   s.y_r = take(R * d->d * ei);

@@ -124,6 +124,18 @@ NIMG_DEV uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
   return r;
 }
+// Remote arrive with the default (CTA-scope release) semantics: for the
+// TMEM-buffer-free signal of the pair epilogues, which only orders the
+// preceding tcgen05 loads (tcgen05.fence::before_thread_sync) -- a
+// cluster-scope release would also wait for every outstanding global store
+// of the arriving thread (MEMBAR.ALL.GPU).
+NIMG_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
+#if defined(NIMG_ARRIVE_CLUSTER_RELEASE)
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#else
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+#endif
+}
 NIMG_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
@@ -280,6 +292,18 @@ __host__ __device__ constexpr uint32_t make_idesc_bf16(int M, int N) {
 // Same with per-operand major-ness (bit 15: A MN-major, bit 16: B MN-major).
 __host__ __device__ constexpr uint32_t make_idesc_bf16_major(int M, int N, bool a_mn, bool b_mn) {
   return make_idesc_bf16(M, N) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16);
+}
+
+// ---------------------------------------------------------------- saved h1 | h3 layout
+// The tcgen05 training forward keeps h1 = x W1^T and h3 = x W3^T for the
+// SwiGLU pullback in a row-blocked layout matched to the epilogues that write
+// (GEMM1) and read (dgrad of GEMM2) it: both hold one row per thread and 16
+// columns per step, so each (128-row block, 16-column chunk) is one contiguous
+// 4-KB block with a row's 16 values at row%128 * 32 B -- a warp's 32 rows are
+// 1 KB contiguous (coalesced), where a row-major [rows][2h] layout would be 32
+// separate lines. Chunks [0, nch) are h1, [nch, 2 nch) are h3 (nch = h / 16).
+NIMG_DEV int64_t hblk_off(int64_t row, int chunk, int nch) {
+  return (((row >> 7) * (2 * nch) + chunk) << 11) + ((row & 127) << 4);
 }
 
 // ---------------------------------------------------------------- numpy sum

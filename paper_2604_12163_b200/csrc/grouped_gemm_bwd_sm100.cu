@@ -238,14 +238,17 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
       const BwdBank& bk = p.bank[ti.bank];
       const int N = bk.N, h = bk.h;
       if (MODE == BWD_D2 && t + n_units < p.total_tiles) {
-        // warm L2 with the next tile's h1 | h3 rows (read by this thread after that tile's MMAs)
+        // warm L2 with the next tile's h1 | h3 (row-blocked: one 128-B line per
+        // 4 rows and chunk; lanes 0, 4, .. cover this warp's 32 rows)
         Tile nx; decode<MODE, PAIR>(p, t + n_units, nx);
-        if (rc + r < nx.rows_valid) {
+        if ((lane & 3) == 0 && rc + r < nx.rows_valid) {
           const BwdBank& nb = p.bank[nx.bank];
-          const bf16* hr = reinterpret_cast<const bf16*>(nb.aux) + (int64_t)(nx.row0 + rc + r) * (2 * nb.h);
-          for (int c = half * 64; c < BN && nx.n0 + c < nb.N; c += 128) {
-            prefetch_l2(hr + nx.n0 + c);
-            prefetch_l2(hr + nb.h + nx.n0 + c);
+          const int nch = nb.h >> 4;
+          const bf16* hb = reinterpret_cast<const bf16*>(nb.aux);
+          const int64_t row = nx.row0 + rc + r;
+          for (int c = half; c < BN / 16 && nx.n0 + 16 * c < nb.N; c += 2) {
+            prefetch_l2(hb + hblk_off(row, (nx.n0 >> 4) + c, nch));
+            prefetch_l2(hb + hblk_off(row, nch + (nx.n0 >> 4) + c, nch));
           }
         }
       }
@@ -258,7 +261,8 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
         // flight before the first use (the rows are strided: latency-bound otherwise)
         constexpr int G = 3, NCH = BN / 16;
         const int64_t row = ti.row0 + rc + r;
-        const bf16* hr = reinterpret_cast<const bf16*>(bk.aux) + row * (int64_t)(2 * h);
+        const int nch = h >> 4;
+        const bf16* hb = reinterpret_cast<const bf16*>(bk.aux);
         bf16* o = reinterpret_cast<bf16*>(bk.out) + row * (int64_t)(2 * h);
 #pragma unroll 1
         for (int c0 = half * G; c0 < NCH; c0 += 2 * G) {
@@ -267,10 +271,12 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
           for (int g = 0; g < G; ++g) {
             const int n = ti.n0 + (c0 + g) * 16;
             if (rv && c0 + g < NCH && n < N) {
-              hv[g][0] = __ldg(reinterpret_cast<const uint4*>(hr + n));
-              hv[g][1] = __ldg(reinterpret_cast<const uint4*>(hr + n) + 1);
-              hv[g][2] = __ldg(reinterpret_cast<const uint4*>(hr + h + n));
-              hv[g][3] = __ldg(reinterpret_cast<const uint4*>(hr + h + n) + 1);
+              const uint4* s1 = reinterpret_cast<const uint4*>(hb + hblk_off(row, n >> 4, nch));
+              const uint4* s3 = reinterpret_cast<const uint4*>(hb + hblk_off(row, nch + (n >> 4), nch));
+              hv[g][0] = __ldg(s1);
+              hv[g][1] = __ldg(s1 + 1);
+              hv[g][2] = __ldg(s3);
+              hv[g][3] = __ldg(s3 + 1);
             }
           }
           uint32_t a[G][16];
@@ -361,7 +367,7 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if (PAIR) mbar_arrive_cluster(acc ? te1 : te0);
+        if (PAIR) mbar_arrive_remote(acc ? te1 : te0);
         else mbar_arrive(&tempty[acc]);
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }

@@ -76,7 +76,8 @@ NIMG_DEV void decode_tile(const GroupedParams& p, int t, TileInfo& ti) {
 
 NIMG_DEV float silu_mul(float a, float g) { return a / (1.0f + __expf(-a)) * g; }
 
-// Training forward: h1 (16 columns at n) and h3 of one row -> h_out row (h1 | h3).
+// Training forward: h1 (16 columns at n) and h3 of one row -> the row-blocked
+// h1 | h3 buffer (hblk_off, common.cuh).
 NIMG_DEV void store_h1h3(const GBank& bk, int64_t row, int n, const uint32_t (&a)[16],
                          const uint32_t (&g)[16]) {
   uint32_t p1[8], p3[8];
@@ -85,9 +86,10 @@ NIMG_DEV void store_h1h3(const GBank& bk, int64_t row, int n, const uint32_t (&a
     p1[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
     p3[j] = pack_bf16x2(__uint_as_float(g[2 * j]), __uint_as_float(g[2 * j + 1]));
   }
-  bf16* hrow = reinterpret_cast<bf16*>(bk.h_out) + row * (int64_t)(2 * bk.N);
-  uint4* d1 = reinterpret_cast<uint4*>(hrow + n);
-  uint4* d3 = reinterpret_cast<uint4*>(hrow + bk.N + n);
+  const int nch = bk.N >> 4;
+  bf16* hb = reinterpret_cast<bf16*>(bk.h_out);
+  uint4* d1 = reinterpret_cast<uint4*>(hb + hblk_off(row, n >> 4, nch));
+  uint4* d3 = reinterpret_cast<uint4*>(hb + hblk_off(row, nch + (n >> 4), nch));
   d1[0] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
   d1[1] = make_uint4(p1[4], p1[5], p1[6], p1[7]);
   d3[0] = make_uint4(p3[0], p3[1], p3[2], p3[3]);
@@ -507,7 +509,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+      if (lane == 0) mbar_arrive_remote(acc ? tempty_leader1 : tempty_leader0);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   }

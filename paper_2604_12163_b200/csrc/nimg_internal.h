@@ -9,6 +9,9 @@
 namespace nimg {
 
 typedef uint16_t bf16_raw;   // bf16 storage in host-visible signatures
+// elements of the row-blocked h1 | h3 buffer (hblk_off in common.cuh)
+inline int64_t hblk_elems(int64_t rows, int64_t h) { return (rows + 127) / 128 * 128 * 2 * h; }
+
 constexpr int kMaxSeg = 264;  // routed segments + shared; EP: R * E/R + 1
 
 // One weight bank of a grouped launch: bank 0 = routed experts (3-D weights
