@@ -452,6 +452,8 @@ def run_train(args, c, inp, cfg, bank, tf_peak):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    clk = ClockSampler(0)
+    time.sleep(0.3)
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     fwd_ms = bwd_ms = 0.0
     for _ in range(args.steps):
@@ -463,6 +465,7 @@ def run_train(args, c, inp, cfg, bank, tf_peak):
         torch.cuda.synchronize()
         fwd_ms += e0.elapsed_time(e1) / args.steps
         bwd_ms += e1.elapsed_time(e2) / args.steps
+    clocks = clk.stop()
     # backward stages: [0] start [1] combine+router pullbacks [2] dH [3] dW2 [4] dX [5] dW1|dW3 [6] g_x_mod
     n_ev = 7
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
@@ -493,6 +496,7 @@ def run_train(args, c, inp, cfg, bank, tf_peak):
         "bwd_gemm_tflops": {k: fl[k] / (st[k] * 1e-3) / 1e12 for k in fl},
         "bwd_expert_gemm_tflops": bwd_tf,
         "bwd_expert_gemm_frac_of_peak": bwd_tf / tf_peak,
+        "clocks": clocks,
         "what": "one layer training step: forward keeping h1|h3, pre, Y (nimg_moe_forward_train) + "
                 "full backward to x_norm, x_mod, t_emb, W_r and all expert weights (nimg_moe_backward)",
         "algorithmic": f"backward expert GEMMs 12*d*h*(R_rows+T) = {sum(fl.values()):.4g} FLOP",

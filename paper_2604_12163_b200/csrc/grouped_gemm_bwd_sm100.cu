@@ -42,7 +42,10 @@ template <> struct Cfg<BWD_W2, false> { static constexpr int BN = 192, STAGES = 
 template <> struct Cfg<BWD_W1, false> { static constexpr int BN = 256, STAGES = 4; };
 // router weight gradient dW_r[:d] = x_norm^T dlogits per sample (N = E = 64)
 template <> struct Cfg<BWD_WR, false> { static constexpr int BN = 64, STAGES = 8; };
-template <> struct Cfg<BWD_D2, true> { static constexpr int BN = 224, STAGES = 6; };   // h = 6 x 224
+#ifndef NIMG_D2_BN
+#define NIMG_D2_BN 224
+#endif
+template <> struct Cfg<BWD_D2, true> { static constexpr int BN = NIMG_D2_BN, STAGES = 6; };   // h = 6 x 224
 template <> struct Cfg<BWD_D1, true> { static constexpr int BN = 256, STAGES = 6; };
 template <> struct Cfg<BWD_W2, true> { static constexpr int BN = 224, STAGES = 6; };
 template <> struct Cfg<BWD_W1, true> { static constexpr int BN = 256, STAGES = 6; };
