@@ -522,6 +522,29 @@ cudaError_t launch_router_bwd_fold(const float* dl, const float* t_emb, const fl
                     part, nchunks, (const float*)colsum, t_emb, w_r, g_wr, g_t, B, d, E);
 }
 
+// out[i] = sum_c part[c][i], c ascending (fixed order): fold of the shared
+// bank's row-chunk weight-gradient partials
+__global__ void sum_partials_kernel(const float4* __restrict__ part, int ks, int64_t n4,
+                                    float4* __restrict__ out) {
+  pdl_trigger();
+  pdl_wait();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n4) return;
+  float4 a = __ldg(part + i);
+  for (int c = 1; c < ks; ++c) {
+    const float4 b = __ldg(part + (int64_t)c * n4 + i);
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  }
+  out[i] = a;
+}
+
+cudaError_t launch_sum_partials(const float* part, int ks, int64_t n, float* out, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t n4 = n / 4;   // n % 4 == 0 (weight shapes are multiples of 64)
+  return launch_pdl(sum_partials_kernel, dim3((unsigned)((n4 + 255) / 256)), dim3(256), 0, s,
+                    reinterpret_cast<const float4*>(part), ks, n4, reinterpret_cast<float4*>(out));
+}
+
 __global__ void f32_to_bf16_kernel(const float* __restrict__ src, bf16* __restrict__ dst, int64_t n) {
   pdl_trigger();
   pdl_wait();

@@ -479,8 +479,21 @@ struct BwdWs {
   void *dy_r, *dy_s, *dh_r, *dh_s, *dx_r, *dx_s;
   float *dlogits, *colsum, *part;
   bf16_raw *dl16, *wr16;   // tcgen05 router pullback operands
+  float *sp1, *sp2, *sp3;  // shared-bank weight-gradient row-chunk partials
   size_t bytes;
 };
+// Shared-expert weight gradients reduce over all T rows (16x a routed
+// segment at cfg2): on the tcgen05 path they are split into ks row chunks
+// (own partial outputs, folded in fixed order) so the persistent grid's
+// round-robin stays balanced.
+int shared_wgrad_chunks(const nimg_moe_desc* d) {
+  if (!train_use_tc(d)) return 1;
+  const int64_t T = d->B * d->S, rows_e = d->B * d->cap;
+  int ks = (int)(T / (4 * rows_e));
+  ks = ks < 1 ? 1 : (ks > 4 ? 4 : ks);
+  while (ks > 1 && T % (64 * ks)) --ks;
+  return ks;
+}
 // Router pullback on tcgen05 (bf16 layer, TMA-aligned E)
 bool router_bwd_tc(const nimg_moe_desc* d) { return train_use_tc(d) && d->E % 8 == 0; }
 BwdWs bwd_ws_layout(const nimg_moe_desc* d, void* base) {
@@ -503,6 +516,10 @@ BwdWs bwd_ws_layout(const nimg_moe_desc* d, void* base) {
   const size_t part_tc = (size_t)d->B * d->d * d->E * 4;   // one partial per sample
   w.part = static_cast<float*>(take(part_simt > part_tc ? part_simt : part_tc));
   const bool rtc = router_bwd_tc(d);
+  const int ks = shared_wgrad_chunks(d);
+  w.sp2 = ks > 1 ? static_cast<float*>(take((size_t)ks * d->d * d->h_shared * 4)) : nullptr;
+  w.sp1 = ks > 1 ? static_cast<float*>(take((size_t)ks * d->h_shared * d->d * 4)) : nullptr;
+  w.sp3 = ks > 1 ? static_cast<float*>(take((size_t)ks * d->h_shared * d->d * 4)) : nullptr;
   w.dl16 = rtc ? static_cast<bf16_raw*>(take(T * d->E * 2)) : nullptr;
   w.wr16 = rtc ? static_cast<bf16_raw*>(take((size_t)d->d * d->E * 2)) : nullptr;
   w.bytes = o;
@@ -511,7 +528,8 @@ BwdWs bwd_ws_layout(const nimg_moe_desc* d, void* base) {
 
 // Segment table of one backward grouped launch. W modes put the shared bank
 // first (its tiles reduce over all T rows: longest first).
-int fill_bwd_segments(BwdParams& p, int mode, const nimg_moe_desc* d, int bm, int bn) {
+int fill_bwd_segments(BwdParams& p, int mode, const nimg_moe_desc* d, int bm, int bn,
+                      int ks_shared = 1) {
   const bool wm = mode == BWD_W2 || mode == BWD_W1;
   const int64_t rows_e = d->B * d->cap, T = d->B * d->S;
   int n = 0;
@@ -528,7 +546,10 @@ int fill_bwd_segments(BwdParams& p, int mode, const nimg_moe_desc* d, int bm, in
     tiles += wm ? (int64_t)bk.ntm * bk.ntn : (rows + bm - 1) / bm * bk.ntn;
     ++n;
   };
-  if (wm) add(1, 0, T, 0);
+  if (wm) {
+    const int ks = ks_shared;
+    for (int c = 0; c < ks; ++c) add(1, c * (T / ks), T / ks, c);
+  }
   for (int e = 0; e < d->E; ++e) add(0, e * rows_e, rows_e, e);
   if (!wm) add(1, 0, T, 0);
   p.nseg = n;
@@ -775,10 +796,10 @@ int nimg_moe_backward_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
 }
 
 static int bwd_grouped(int mode, bool tc, bool b_bf16, BwdParams& P, const TmapSetBwd& tm, int sms,
-                       const nimg_moe_desc* d, cudaStream_t st) {
+                       const nimg_moe_desc* d, cudaStream_t st, int ks_shared = 1) {
   const int bm = tc ? tc_bwd_tile_rows(mode) : simt_bwd_bm();
   const int bn = tc ? tc_bwd_bn(mode) : simt_bwd_bn();
-  NIMG_TRY(fill_bwd_segments(P, mode, d, bm, bn));
+  NIMG_TRY(fill_bwd_segments(P, mode, d, bm, bn, ks_shared));
   if (tc) CUDA_TRY(launch_grouped_tc_bwd(mode, tm, P, sms, st));
   else CUDA_TRY(launch_grouped_simt_bwd(mode, b_bf16, P, st));
   return NIMG_OK;
@@ -792,7 +813,7 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
   cudaStream_t st = (cudaStream_t)stream;
   NIMG_TRY(check_moe_desc(d));
   if (!p || !g) return fail(NIMG_ERR_SHAPE, "null pointers");
-  if (d->E + 2 > kMaxSeg) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
+  if (d->E + 5 > kMaxSeg) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
   const TrainState ts = train_state_layout(d, const_cast<void*>(state));
   if (!state || state_bytes < ts.bytes) return fail(NIMG_ERR_CONFIG, "training state too small");
   const BwdWs w = bwd_ws_layout(d, ws);
@@ -804,6 +825,7 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
   if (!ro.logits || !ro.gates || !ro.gate_raw || !ro.comb_rows || !ro.comb_cnt)
     return fail(NIMG_ERR_SHAPE, "null routing pointer");
   const bool tc = ts.tc, bf = d->act_dtype == NIMG_BF16;
+  const int ks = shared_wgrad_chunks(d);
   const int64_t T = d->B * d->S, R = d->E * d->B * d->cap, rows_e = d->B * d->cap;
   const int dd = (int)d->d, h = (int)d->h, hs = (int)d->h_shared, E = (int)d->E;
   if (tc) {
@@ -915,10 +937,12 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
       NIMG_TRY(map_3d(&tm.b[1], ts.pre_s, 1, T, hs, 64));
       tm.b3[0] = tm.b[0]; tm.b3[1] = tm.b[1];
       NIMG_TRY(map_3d_f32_out(&tm.o[0], g->g_w2, E, dd, h));
-      NIMG_TRY(map_3d_f32_out(&tm.o[1], g->g_sw2, 1, dd, hs));
+      if (ks > 1) NIMG_TRY(map_3d_f32_out(&tm.o[1], w.sp2, ks, dd, hs));
+      else NIMG_TRY(map_3d_f32_out(&tm.o[1], g->g_sw2, 1, dd, hs));
       tm.o3[0] = tm.o[0]; tm.o3[1] = tm.o[1];
     }
-    NIMG_TRY(bwd_grouped(BWD_W2, tc, false, P, tm, sms, d, st));
+    NIMG_TRY(bwd_grouped(BWD_W2, tc, false, P, tm, sms, d, st, ks));
+    if (ks > 1) CUDA_TRY(launch_sum_partials(w.sp2, ks, (int64_t)dd * hs, g->g_sw2, st));
   }
   mark(3, st);
   // 5. dX = dH [W1; W3]
@@ -954,10 +978,14 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
       tm.b3[0] = tm.b[0]; tm.b3[1] = tm.b[1];
       NIMG_TRY(map_3d_f32_out(&tm.o[0], g->g_w1, E, h, dd));
       NIMG_TRY(map_3d_f32_out(&tm.o3[0], g->g_w3, E, h, dd));
-      NIMG_TRY(map_3d_f32_out(&tm.o[1], g->g_sw1, 1, hs, dd));
-      NIMG_TRY(map_3d_f32_out(&tm.o3[1], g->g_sw3, 1, hs, dd));
+      NIMG_TRY(map_3d_f32_out(&tm.o[1], ks > 1 ? (void*)w.sp1 : (void*)g->g_sw1, ks, hs, dd));
+      NIMG_TRY(map_3d_f32_out(&tm.o3[1], ks > 1 ? (void*)w.sp3 : (void*)g->g_sw3, ks, hs, dd));
     }
-    NIMG_TRY(bwd_grouped(BWD_W1, tc, bf, P, tm, sms, d, st));
+    NIMG_TRY(bwd_grouped(BWD_W1, tc, bf, P, tm, sms, d, st, ks));
+    if (ks > 1) {
+      CUDA_TRY(launch_sum_partials(w.sp1, ks, (int64_t)hs * dd, g->g_sw1, st));
+      CUDA_TRY(launch_sum_partials(w.sp3, ks, (int64_t)hs * dd, g->g_sw3, st));
+    }
   }
   mark(5, st);
   // 7. gather pullback: g_x_mod[t] = dX_shared[t] + sum of its routed dX rows

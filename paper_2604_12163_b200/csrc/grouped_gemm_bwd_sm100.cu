@@ -173,17 +173,21 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
           uint8_t* sa = smem + stage * SB;
           uint8_t* sb = sa + BM * BK * 2;
           if (leader) mbar_arrive_expect_tx(&full[stage], (PAIR ? 2 : 1) * SB);
+          // W modes: routed segment e reads rows of z = e of the 3-D [E][rows_e][.]
+          // views; the shared bank (z = 0, all T rows) may be split into row
+          // chunks (segments with their own partial output z = chunk)
+          const int krow = kb * BK + (AMN && ti.bank ? ti.row0 : 0);
           if (AMN) {   // A^T: 2 boxes of 64 M-columns x 64 K-rows (3-D map [E][rows][M])
             const int z = ti.bank ? 0 : ti.expert;
             const int m = ti.m0 + (int)crank * BM;
-            load_3d<PAIR>(sa, &tm.a[ti.bank], &full[stage], m, kb * BK, z);
-            load_3d<PAIR>(sa + kChunk, &tm.a[ti.bank], &full[stage], m + 64, kb * BK, z);
+            load_3d<PAIR>(sa, &tm.a[ti.bank], &full[stage], m, krow, z);
+            load_3d<PAIR>(sa + kChunk, &tm.a[ti.bank], &full[stage], m + 64, krow, z);
           } else {     // A rows: one box {64 K, 128 rows}
             load_2d<PAIR>(sa, &tm.a[ti.bank], &full[stage], kb * BK, ti.row0 + (int)crank * BM);
           }
           // B: this CTA's columns, MN-major boxes {64 N, 64 K}
           const void* bm = &tm.b[ti.bank];
-          int kc = kb * BK, z = ti.expert;
+          int kc = AMN ? krow : kb * BK, z = ti.expert;
           if (MODE == BWD_D1 && kb >= ti.nk1) { bm = &tm.b3[ti.bank]; kc = (kb - ti.nk1) * BK; }
           if (AMN) z = ti.bank ? 0 : ti.expert;
           const int nb = ti.n0 + (int)crank * BNC;
@@ -239,7 +243,8 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
     for (int t = unit; t < p.total_tiles; t += n_units) {
       Tile ti; decode<MODE, PAIR>(p, t, ti);
       const BwdBank& bk = p.bank[ti.bank];
-      const int N = bk.N, h = bk.h;
+      const int N = ti.bank ? p.bank[1].N : p.bank[0].N;   // immediate-offset constant reads
+      const int h = ti.bank ? p.bank[1].h : p.bank[0].h;
       if (MODE == BWD_D2 && t + n_units < p.total_tiles) {
         // warm L2 with the next tile's h1 | h3 (row-blocked: one 128-B line per
         // 4 rows and chunk; lanes 0, 4, .. cover this warp's 32 rows)
@@ -319,6 +324,7 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
           }
         }
       } else if constexpr (MODE == BWD_D1) {
+        bf16* const orow = reinterpret_cast<bf16*>(bk.out) + (ti.row0 + rc + r) * bk.out_ld;
 #pragma unroll 1
         for (int c = 0; c < BN / 16; ++c) {
           uint32_t a[16];
@@ -329,7 +335,7 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
           uint32_t pk[8];
 #pragma unroll
           for (int j = 0; j < 8; ++j) pk[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
-          uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(bk.out) + (ti.row0 + rc + r) * bk.out_ld + n);
+          uint4* dst = reinterpret_cast<uint4*>(orow + n);
           dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }

@@ -78,7 +78,7 @@ NIMG_DEV float silu_mul(float a, float g) { return a / (1.0f + __expf(-a)) * g; 
 
 // Training forward: h1 (16 columns at n) and h3 of one row -> the row-blocked
 // h1 | h3 buffer (hblk_off, common.cuh).
-NIMG_DEV void store_h1h3(const GBank& bk, int64_t row, int n, const uint32_t (&a)[16],
+NIMG_DEV void store_h1h3(void* h_out, int N, int64_t row, int n, const uint32_t (&a)[16],
                          const uint32_t (&g)[16]) {
   uint32_t p1[8], p3[8];
 #pragma unroll
@@ -86,8 +86,8 @@ NIMG_DEV void store_h1h3(const GBank& bk, int64_t row, int n, const uint32_t (&a
     p1[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
     p3[j] = pack_bf16x2(__uint_as_float(g[2 * j]), __uint_as_float(g[2 * j + 1]));
   }
-  const int nch = bk.N >> 4;
-  bf16* hb = reinterpret_cast<bf16*>(bk.h_out);
+  const int nch = N >> 4;
+  bf16* hb = reinterpret_cast<bf16*>(h_out);
   uint4* d1 = reinterpret_cast<uint4*>(hb + hblk_off(row, n >> 4, nch));
   uint4* d3 = reinterpret_cast<uint4*>(hb + hblk_off(row, nch + (n >> 4), nch));
   d1[0] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
@@ -207,7 +207,11 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
     int acc = 0; uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x) {
       TileInfo ti; decode_tile<MODE>(p, t, ti);
+      // bank fields into registers once per tile (a runtime-indexed parameter
+      // read inside the chunk loop is an LDC on the critical path)
       const GBank& bk = p.bank[ti.bank];
+      const int Nb = ti.bank ? p.bank[1].N : p.bank[0].N;   // immediate-offset constant reads
+      void* const h_out = ti.bank ? p.bank[1].h_out : p.bank[0].h_out;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
@@ -220,7 +224,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
           tmem_ld16(tb + c * 16, a);
           tmem_ld16(tb + C::B_BOX + c * 16, g);
           tmem_ld_wait();
-          if (rv && ti.n0 + c * 16 < bk.N) {
+          if (rv && ti.n0 + c * 16 < Nb) {
             uint32_t pk[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -229,7 +233,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
             dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-            if (bk.h_out != nullptr) store_h1h3(bk, ti.a_row + r, ti.n0 + c * 16, a, g);
+            if (h_out != nullptr) store_h1h3(h_out, Nb, ti.a_row + r, ti.n0 + c * 16, a, g);
           }
         }
       } else {
@@ -238,7 +242,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
           uint32_t a[16];
           tmem_ld16(tb + c * 16, a);
           tmem_ld_wait();
-          if (rv && ti.n0 + c * 16 < bk.N) {
+          if (rv && ti.n0 + c * 16 < Nb) {
             uint32_t pk[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j)
@@ -475,6 +479,8 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
     for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
       TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
       const GBank& bk = p.bank[ti.bank];
+      const int Nb = ti.bank ? p.bank[1].N : p.bank[0].N;   // immediate-offset constant reads
+      void* const h_out = ti.bank ? p.bank[1].h_out : p.bank[0].h_out;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
@@ -499,12 +505,12 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
           for (int j = 0; j < 8; ++j)
             pk[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
         }
-        if (rv && ti.n0 + c * 16 < bk.N) {
+        if (rv && ti.n0 + c * 16 < Nb) {
           uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
           dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          if (MODE == 0 && bk.h_out != nullptr)   // training forward: keep h1 | h3
-            store_h1h3(bk, ti.a_row + row, ti.n0 + c * 16, a, g);
+          if (MODE == 0 && h_out != nullptr)   // training forward: keep h1 | h3
+            store_h1h3(h_out, Nb, ti.a_row + row, ti.n0 + c * 16, a, g);
         }
       }
       tc_fence_before();

@@ -125,6 +125,7 @@ cudaError_t launch_router_bwd_fold(const float* dl, const float* t_emb, const fl
                                    const float* part, int nchunks, float* colsum, float* g_wr,
                                    float* g_t, int B, int S, int d, int E, cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* src, bf16_raw* dst, int64_t n, cudaStream_t s);
+cudaError_t launch_sum_partials(const float* part, int ks, int64_t n, float* out, cudaStream_t s);
 
 // Launch with programmatic stream serialization (PDL) unless NIMG_PDL=0. The
 // kernel must call pdl_wait() before touching global memory (common.cuh).
