@@ -597,10 +597,15 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     torch.cuda.synchronize()
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    hts = []
+    ms0 = torch.cuda.memory_stats(dev)
     e0.record()
     h0 = time.perf_counter()
-    for _ in range(args.steps):
+    for i in range(args.steps):
         step()
+        per[i].record()
+        hts.append(time.perf_counter())
     host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # issue time per step
     e1.record()
     torch.cuda.synchronize()
@@ -608,6 +613,16 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     out = {"ms": float(t.item()), "host_issue_ms": round(host_ms, 4)}
+    if os.environ.get("NIMG_BENCH_DEBUG"):
+        dev_steps = [round(e0.elapsed_time(per[0]), 3)] + [
+            round(per[i - 1].elapsed_time(per[i]), 3) for i in range(1, args.steps)]
+        host_steps = [round((hts[0] - h0) * 1e3, 3)] + [
+            round((hts[i] - hts[i - 1]) * 1e3, 3) for i in range(1, args.steps)]
+        ms1 = torch.cuda.memory_stats(dev)
+        allocs = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("num_device_alloc", "num_device_free",
+                                                             "num_alloc_retries")}
+        print(f"[rank {rank}] {c['name']} device ms/step {dev_steps} host ms/step {host_steps} "
+              f"allocator {allocs}", file=sys.stderr, flush=True)
     if timeline:
         tl = []
         # two steps ahead of the recorded one keep the host ahead of the GPU,
@@ -727,7 +742,8 @@ def run_ep(args, c, peaks, peak_kind):
         wc4 = work_counts(CFG4)
         strong = {"workload": workload_name(CFG4), "ms_per_step": st["ms"],
                   "value": wc4["T"] / (st["ms"] * 1e-3), "unit": "tokens/s",
-                  "timeline_ms_rank0": st["timeline"], "nvlink_dispatch_rank0": st.get("dispatch")}
+                  "timeline_ms_rank0": st["timeline"], "nvlink_dispatch_rank0": st.get("dispatch"),
+                  "host_issue_ms_rank0": st.get("host_issue_ms")}
         if ms1 is not None:
             strong["same_config_1gpu"] = {"ms_per_step": ms1, "value": wc4["T"] / (ms1 * 1e-3)}
             strong["efficiency"] = ms1 / (world * st["ms"])
@@ -767,6 +783,13 @@ def run_ep(args, c, peaks, peak_kind):
 
 
 def main():
+    # The host path issues a layer per step from Python: a cyclic-GC pass
+    # (tens of ms, at the same step on every rank since they allocate alike)
+    # would starve the GPUs inside a timed region. Collect now, then keep the
+    # collector off for the run (refcounting still frees the per-step objects).
+    import gc
+    gc.collect()
+    gc.disable()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

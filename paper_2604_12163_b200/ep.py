@@ -245,6 +245,34 @@ class CETransport:
             b.close()
 
 
+class _Ring:
+    """Two persistent buffers of one shape, handed out alternately. Before a
+    slot is reused, the current stream waits for the side-stream readers of
+    its previous use (events the caller records with reader_done). Replaces
+    per-step allocations whose record_stream() deferred frees would keep the
+    caching allocator growing -- each new segment a cudaMalloc that must also
+    map into every IPC peer, stalling the host for tens of ms mid-run."""
+
+    def __init__(self, shape, dtype, device):
+        self.bufs = [torch.empty(shape, dtype=dtype, device=device) for _ in range(2)]
+        self.events = [[], []]
+        self.k = 0
+
+    def next(self):
+        s = self.k % 2
+        self.k += 1
+        cur = torch.cuda.current_stream()
+        for ev in self.events[s]:
+            cur.wait_event(ev)
+        self.events[s] = []
+        return s, self.bufs[s]
+
+    def reader_done(self, slot: int, stream) -> None:
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        self.events[slot].append(ev)
+
+
 class EPContext:
     """Process groups, streams and transport state of one expert-parallel layer."""
 
@@ -259,6 +287,14 @@ class EPContext:
         self._ce = None
         self._ret_group = None
         self._streams = None
+        self._rings = {}
+
+    def ring(self, name: str, shape, dtype, device) -> _Ring:
+        key = (name, tuple(shape), dtype, str(device))
+        r = self._rings.get(key)
+        if r is None:
+            r = self._rings[key] = _Ring(shape, dtype, device)
+        return r
 
     def ce(self, chunk_rows, d, act, ydt, device) -> CETransport:
         """The transport, grown (collectively: every rank makes the same calls)
@@ -336,7 +372,14 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
     _mark(timeline, "start")
     r = stages.route(x_norm, t_emb, w_r, cfg, cap)
     _mark(timeline, "routed")
-    xg = stages.gather(xm, r["token_flat"])                       # (E*B_l*cap, d)
+    xring = None
+    if ctx.overlap and ctx.transport == "ce":
+        # persistent double buffer (read by the dispatch copy streams)
+        xring = ctx.ring("xg", (E * B_l * cap, d), act, x_mod.device)
+        xslot, xg = xring.next()
+        stages.gather(xm, r["token_flat"], out=xg)
+    else:
+        xg = stages.gather(xm, r["token_flat"])                   # (E*B_l*cap, d)
     _mark(timeline, "gathered")
 
     if not ctx.overlap:
@@ -354,7 +397,7 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
         else:
             y_back.copy_(y_recv)
     elif ctx.transport == "ce":
-        y_back, y_sh = _ce_exchange(plan, ctx, stages, xg, xm, w, timeline)
+        y_back, y_sh = _ce_exchange(plan, ctx, stages, xg, xm, w, timeline, (xring, xslot))
     else:
         y_back, y_sh = _overlapped_exchange(plan, ctx, stages, xg, xm, w, timeline)
     _mark(timeline, "returned")
@@ -414,7 +457,7 @@ def _overlapped_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeli
     return y_back.view(R * n, -1), y_sh
 
 
-def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None):
+def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None, xring=None):
     """Copy-engine dispatch / return with per-step flags (see module doc).
 
     Flags in rank r's array: disp[src] (src's chunk for r has landed in r's
@@ -462,7 +505,10 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
             timeline.append((f"copy_start_q{q}", ev0))
             timeline.append((f"copy_end_q{q}", ev1))
         _lib.check(L.nimg_stream_write_u32(tp.flag(q, DISP, me), k, sh))
-        xg.record_stream(st)
+        if xring is not None and xring[0] is not None:
+            xring[0].reader_done(xring[1], st)
+        else:
+            xg.record_stream(st)
 
     # The rank's own chunk needs no exchange: its first half of experts runs
     # right after the shared expert (together they cover the dispatch copies),
@@ -484,7 +530,8 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
     _, y_sh = own_part(0, half, shared=True)
     _mark(timeline, "shared+own_a")
 
-    y_recv = torch.empty((R, n, d), dtype=ydt, device=dev)
+    yring = ctx.ring("y_recv", (R, n, d), ydt, dev)
+    yslot, y_recv = yring.next()
     recv_all = tp.recv_t.view(R * n, d)
     y_all = y_recv.view(R * n, d)
     for gi, grp in enumerate(plan.chunk_groups(_GROUP_ROWS)):
@@ -511,7 +558,7 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None)
                                          ybytes, sh))
             _lib.check(L.nimg_stream_write_u32(tp.flag(src, RET, me), k, sh))
     for st in tp.streams:
-        y_recv.record_stream(st)
+        yring.reader_done(yslot, st)
 
     own_part(half, El)
     _mark(timeline, "own_b")

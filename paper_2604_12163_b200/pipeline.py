@@ -56,7 +56,11 @@ class HostPipeline:
             self.d2h.wait_event(self.ev_out[k])
             self.host_out[k].copy_(y, non_blocking=True)
             self.ev_drained[k].record(self.d2h)
-        y.record_stream(self.d2h)
+        # no y.record_stream(d2h): y stays referenced in _outs[k] until step
+        # i + depth, whose compute is already ordered after ev_drained[k], so
+        # its block returns to the compute stream's pool only when the download
+        # is done -- without deferred frees growing the allocator (a cudaMalloc
+        # mid-run, mapped into every IPC peer under EP, stalls the host)
         self.i += 1
 
     def drain(self) -> None:

@@ -37,10 +37,12 @@ class CudaStages:
                                        C.byref(ro), ptr(ws), ws.numel(), stream_handle()))
         return r
 
-    def gather(self, src: torch.Tensor, idx_i32: torch.Tensor) -> torch.Tensor:
+    def gather(self, src: torch.Tensor, idx_i32: torch.Tensor, out: torch.Tensor | None = None
+               ) -> torch.Tensor:
         """tensor.py:348-363 gather_rows: src (N, d)[idx] -> (len(idx), d)."""
         n, d = src.shape
-        out = torch.empty((idx_i32.numel(), d), dtype=src.dtype, device=src.device)
+        if out is None:
+            out = torch.empty((idx_i32.numel(), d), dtype=src.dtype, device=src.device)
         _lib.check(_lib.lib.nimg_gather_rows(ptr(src), n, d * src.element_size(), ptr(idx_i32),
                                              idx_i32.numel(), ptr(out), stream_handle()))
         return out

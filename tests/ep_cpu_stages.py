@@ -33,8 +33,11 @@ class OracleStages:
                 "scores_bes": torch.from_numpy(np.ascontiguousarray(r["scores"].transpose(0, 2, 1))),
                 "comb_rows": torch.from_numpy(comb_rows), "comb_cnt": torch.from_numpy(comb_cnt)}
 
-    def gather(self, src, idx):
-        return src[idx.long()].clone()
+    def gather(self, src, idx, out=None):
+        if out is None:
+            return src[idx.long()].clone()
+        out.copy_(src[idx.long()])
+        return out
 
     def ffn_y_dtype(self, act, d, h, hs):
         return torch.float32
