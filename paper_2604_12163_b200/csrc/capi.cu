@@ -171,13 +171,14 @@ struct RouteWs {
   double* wd;
   int16_t* slot_of;
   unsigned* counters;
+  void* i8;   // INT8 router scratch (router_i8.cu)
 };
 size_t slot_bytes(const nimg_moe_desc* d) { return (size_t)d->E * d->B * d->S * 2; }
 size_t route_ws_bytes(const nimg_moe_desc* d) {
   return align_up((size_t)d->B * d->E * 8) +
          align_up(router_part_bytes((int)d->B, (int)d->d, (int)d->E)) +
          align_up(router_wd_bytes((int)d->d, (int)d->E)) + align_up(slot_bytes(d)) +
-         align_up((size_t)d->B * 4);
+         align_up((size_t)d->B * 4) + align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d));
 }
 RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
@@ -191,6 +192,8 @@ RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   r.slot_of = reinterpret_cast<int16_t*>(p);
   p += align_up(slot_bytes(d));
   r.counters = reinterpret_cast<unsigned*>(p);
+  p += align_up((size_t)d->B * 4);
+  r.i8 = p;
   return r;
 }
 
@@ -417,8 +420,11 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
   // caller-owned).
   if (!router_uses_dmma(E))
     CUDA_TRY(cudaMemsetAsync(w.counters, 0xFF, (size_t)B * 4, st));
-  CUDA_TRY(launch_router(d->act_dtype == NIMG_BF16, x_norm, t_emb, w_r, w.tb, w.part, w.counters,
-                         w.wd, o->logits, o->scores_bes, B, S, dd, E, st));
+  if (router_i8_eligible(d->act_dtype == NIMG_BF16, dd, E, x_norm))
+    CUDA_TRY(launch_router_i8(x_norm, t_emb, w_r, w.part, w.i8, o->logits, o->scores_bes, B, S, dd, st));
+  else
+    CUDA_TRY(launch_router(d->act_dtype == NIMG_BF16, x_norm, t_emb, w_r, w.tb, w.part, w.counters,
+                           w.wd, o->logits, o->scores_bes, B, S, dd, E, st));
   mark(6, st);   // router scores done (inside stage 0 -> 1)
   CUDA_TRY(launch_ec_select(o->scores_bes, o->token_flat, o->gate_raw, w.slot_of, B, S, E, cap, st));
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
@@ -708,8 +714,11 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   nimg_ffn_path(&f, &path, &ydt);
   // the gathered-row buffer exists only when the gather is not fused into GEMM1
   const size_t xg = use_fused_gather(path, d->d) ? 0 : align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
+  // the training forward (moe_forward_impl with a state blob) keeps the shared
+  // expert's outputs in fp32 on the CUDA-core training path: size for both
+  const size_t ys_elt = std::max<size_t>(elt(ydt), train_use_tc(d) ? 2 : 4);
   *bytes = route_ws_bytes(d) + xg + ffn_ws_bytes(&f) + align_up((size_t)f.n_rows * d->d * elt(ydt)) +
-           align_up((size_t)f.n_shared_rows * d->d * elt(ydt));
+           align_up((size_t)f.n_shared_rows * d->d * ys_elt);
   return NIMG_OK;
 }
 
@@ -727,6 +736,9 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   const nimg_ffn_desc f = layer_ffn_desc(d);
   int32_t path, ydt;
   nimg_ffn_path(&f, &path, &ydt);
+  // the workspace carve follows nimg_moe_workspace_bytes (inference dtypes);
+  // the training forward only re-types the outputs it writes
+  const int32_t ydt_ws = ydt;
   FfnTrain tr{};
   TrainState ts{};
   if (state) {
@@ -740,7 +752,7 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   void* route_ws = w;                 w += route_ws_bytes(d);
   void* xg = w;                       if (!fused_gather) w += align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
   void* ffn_ws = w;                   w += ffn_ws_bytes(&f);
-  void* yr = w;                       w += align_up((size_t)f.n_rows * d->d * elt(ydt));
+  void* yr = w;                       w += align_up((size_t)f.n_rows * d->d * elt(ydt_ws));
   void* ys = w;
   if (state) { xg = ts.xg; yr = ts.y_r; }
 

@@ -306,6 +306,95 @@ NIMG_DEV int64_t hblk_off(int64_t row, int chunk, int nch) {
   return (((row >> 7) * (2 * nch) + chunk) << 11) + ((row & 127) << 4);
 }
 
+// ---------------------------------------------------------------- int8 tcgen05 / bulk copy
+// D[tmem] (+)= A[smem] * B[smem]^T, signed int8 inputs, exact int32 accumulate.
+NIMG_DEV void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                      uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Instruction descriptor: kind::i8, A/B signed int8, D s32, K-major A and B.
+__host__ __device__ constexpr uint32_t make_idesc_s8(int M, int N) {
+  return (2u << 4)                       // D format s32
+         | (1u << 7)                     // A signed 8-bit
+         | (1u << 10)                    // B signed 8-bit
+         | ((uint32_t)(N >> 3) << 17)
+         | ((uint32_t)(M >> 4) << 24);
+}
+// 32 lanes x 32 bit, 8 consecutive columns -> 8 registers per thread.
+NIMG_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(taddr));
+}
+NIMG_DEV void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+}
+// Plain (non-tensor) bulk copy global -> shared, completion on an mbarrier.
+NIMG_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// ---------------------------------------------------------------- router t half
+// The t half of the router product [x_norm || t_emb] . W_r (router.py:120-122)
+// is per sample: part[b, ks, e] = sum over the ks-th k-range of t_emb[b, k] *
+// W_r[d + k, e] in f64, computed by a block of 256 threads (thread (e, q) sums
+// one of 4 sub-slices, folded in a fixed order), and folded per sample in ks
+// order by router_tbias (deterministic). Shared by the DMMA and int8 routers so
+// both add the identical f64 t-bias.
+__host__ __device__ inline int router_tpart_ks(int d) {
+  const int nkc = (d + 63) / 64;   // <= router_part_bytes' chunk count: the partials fit
+  return nkc < 8 ? nkc : 8;
+}
+NIMG_DEV void router_tpart_block(const float* __restrict__ t_emb, const float* __restrict__ w_r,
+                                 double* __restrict__ part, int b, int ks, int d, int E) {
+  __shared__ double sp[4][64];
+  const int KS = router_tpart_ks(d);
+  const int e = threadIdx.x & 63, q = threadIdx.x >> 6;
+  const int nsl = 4 * KS, sl = ks * 4 + q;
+  const int klen = (d + nsl - 1) / nsl, k0 = sl * klen, k1 = min(d, k0 + klen);
+  double acc = 0.0;
+  if (e < E) {
+    const float* t = t_emb + (int64_t)b * d;
+    const float* w = w_r + (int64_t)d * E + e;
+    int k = k0;
+    for (; k + 16 <= k1; k += 16) {   // loads batched ahead of the (sequential) f64 chain
+      float tv[16], wv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        tv[i] = __ldg(t + k + i);
+        wv[i] = __ldg(w + (int64_t)(k + i) * E);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc = fma((double)tv[i], (double)wv[i], acc);
+    }
+    for (; k < k1; ++k) acc = fma((double)__ldg(t + k), (double)__ldg(w + (int64_t)k * E), acc);
+  }
+  sp[q][e] = acc;
+  __syncthreads();
+  if (q == 0 && e < E)
+    part[((int64_t)b * KS + ks) * E + e] = ((sp[0][e] + sp[1][e]) + sp[2][e]) + sp[3][e];
+}
+NIMG_DEV double router_tbias(const double* __restrict__ part, int64_t b, int e, int d, int E) {
+  const int KS = router_tpart_ks(d);
+  const double* pp = part + (b * KS) * E + e;
+  double r = pp[0];
+  for (int ks = 1; ks < KS; ++ks) r += pp[(int64_t)ks * E];
+  return r;
+}
+
 // ---------------------------------------------------------------- numpy sum
 // Exact restatement of numpy's pairwise summation (float add.reduce over a
 // contiguous axis, e.g. `e.sum(axis=-1)` / `mean` in tensor.py:471, :527):

@@ -170,6 +170,13 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
                           double* tb, double* part, unsigned* counter, double* wd, float* logits,
                           float* scores_bes, int B, int S, int d, int E, cudaStream_t s);
 size_t router_wd_bytes(int d, int E);
+// Exact INT8 tensor-core router (router_i8.cu): bf16 x_norm, E == 64, d % 128 == 0.
+// NIMG_ROUTER=dmma forces the FP64 router.
+bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm);
+size_t router_i8_ws_bytes(int64_t T, int d);
+cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float* w_r, double* part,
+                             void* i8ws, float* logits, float* scores_bes, int B, int S, int d,
+                             cudaStream_t s);
 size_t router_part_bytes(int B, int d, int E);
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s);

@@ -320,11 +320,7 @@ constexpr int DM_TM = 64, DM_KC = 32, DM_XS = 36, DM_WS = 72, DM_EP = 64;
 // Blocks [B * KS, + RP2_CONV) write wd[k, e] = f64(W_r[k, e]) for the x half,
 // E padded to 64. Short dependent chains: the kernel is latency-bound.
 constexpr int RP2_CONV = 64;
-constexpr int RP2_KS_MAX = 8;
-__host__ __device__ inline int rp2_ks(int d) {
-  const int nkc = (d + 63) / 64;   // == router_part_bytes' chunk count: the partials fit
-  return nkc < RP2_KS_MAX ? nkc : RP2_KS_MAX;
-}
+__host__ __device__ inline int rp2_ks(int d) { return router_tpart_ks(d); }
 __global__ void __launch_bounds__(256)
 router_prep_dmma_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
                         double* __restrict__ part, double* __restrict__ wd, int B, int d, int E) {
@@ -340,22 +336,7 @@ router_prep_dmma_kernel(const float* __restrict__ t_emb, const float* __restrict
     }
     return;
   }
-  __shared__ double sp[4][64];
-  const int b = blockIdx.x / KS, ks = blockIdx.x % KS;
-  const int e = threadIdx.x & 63, q = threadIdx.x >> 6;
-  const int nsl = 4 * KS, sl = ks * 4 + q;
-  const int klen = (d + nsl - 1) / nsl, k0 = sl * klen, k1 = min(d, k0 + klen);
-  double acc = 0.0;
-  if (e < E) {
-    const float* t = t_emb + (int64_t)b * d;
-    const float* w = w_r + (int64_t)d * E + e;
-#pragma unroll 16
-    for (int k = k0; k < k1; ++k) acc = fma((double)__ldg(t + k), (double)__ldg(w + (int64_t)k * E), acc);
-  }
-  sp[q][e] = acc;
-  __syncthreads();
-  if (q == 0 && e < E)
-    part[((int64_t)b * KS + ks) * E + e] = ((sp[0][e] + sp[1][e]) + sp[2][e]) + sp[3][e];
+  router_tpart_block(t_emb, w_r, part, blockIdx.x / KS, blockIdx.x % KS, d, E);
 }
 
 __host__ __device__ inline size_t dmma_stage_bytes() {
@@ -502,13 +483,7 @@ router_scores_dmma_kernel(const TX* __restrict__ x, const double* __restrict__ w
   const int nb = (int)((t0 + rows - 1) / S - b_first + 1);
   double* tbs = reinterpret_cast<double*>(sm + dmma_tbs_offset(E));
   {
-    const int KS = rp2_ks(d);
-    for (int i = tid; i < nb * E; i += 128) {
-      const double* pp = part + ((b_first + i / E) * KS) * E + (i % E);
-      double r = pp[0];
-      for (int ks = 1; ks < KS; ++ks) r += pp[(int64_t)ks * E];
-      tbs[i] = r;
-    }
+    for (int i = tid; i < nb * E; i += 128) tbs[i] = router_tbias(part, b_first + i / E, i % E, d, E);
   }
   __syncthreads();
 

@@ -1,0 +1,684 @@
+// Router logits on the INT8 tensor cores, exact: the x half of
+// [x_norm || t_emb] . W_r (router.py:120-122, tensor.py:280-296) for bf16
+// x_norm and E == 64 experts.
+//
+// The reference sums the products in f64 and rounds once to fp32. A bf16 x has
+// an 8-bit significand and an fp32 W_r a 24-bit one, so the x half is an exact
+// sum of integers once both sides are written in fixed point:
+//
+//   x[t, k] = X[t, k] * 2^(emax_t - 154),  |X| < 2^28  (row scale, 4 signed
+//             7-bit digits X_0..X_3: X = sum_i X_i 2^(7 (3 - i)))
+//   w[k, e] = W[k, e] * 2^(ew_e - 161),    |W| < 2^35  (column scale, 5 digits)
+//
+// and sum_k X W = sum_{s=0..7} G_s 2^(7 (7 - s)), G_s = sum_{i+j=s} sum_k X_i W_j,
+// where every G_s is an int8 x int8 GEMM with int32 accumulation: EXACT, in any
+// order (tcgen05.mma kind::i8, 20 digit-pair MMAs per K step into 8 TMEM
+// accumulators of 64 columns = all 512 TMEM columns). Elements too small for the
+// row / column window are not lost: a W element below 2^-11 of its column max
+// becomes an exact f64 correction term (a short per-expert list), and a row
+// with an x element below 2^-20 of its row max (or a non-finite value) is
+// recomputed by the f64 fix-up kernel. The epilogue forms v = H 2^28 + L
+// exactly in int64 halves, scales by a power of two, adds the corrections and
+// the f64 t-bias, rounds to fp32 and PROVES the rounding: if the f64 value is
+// not farther than its error bound from an fp32 rounding boundary, the token is
+// recomputed by the fix-up kernel with a plain f64 dot (the DMMA router's
+// arithmetic). The fp32 logits therefore equal the correctly rounded f64 ones
+// -- the same bits the f64 routers produce -- at int8 tensor-core speed.
+//
+// Kernels: router_prep_i8 (t-half partials, W digit image in the UMMA smem
+// layout, correction lists, counter reset), router_scores_i8 (one CTA per 128
+// tokens: converter warps write the x digits into 128-B swizzled smem, a bulk
+// copy brings the W digits, one thread issues the MMAs, the same converter
+// warps run the epilogue and the numpy-order softmax), router_fix_i8 (flagged
+// tokens, f64).
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "nimg_internal.h"
+
+namespace nimg {
+namespace ri8 {
+
+constexpr int NE = 64;                       // experts = UMMA N
+constexpr int BM = 128;                      // tokens per CTA = UMMA M = TMEM lanes
+constexpr int KB = 128;                      // k per stage: one 128-B swizzle row of int8
+constexpr int LX = 4, LW = 5, NG = LX + LW - 1;
+constexpr int A_SLICE = BM * KB;             // 16 KB
+constexpr int W_SLICE = NE * KB;             // 8 KB
+constexpr int W_STAGE = LW * W_SLICE;        // 40 KB
+constexpr int STAGE = LX * A_SLICE + W_STAGE;   // 104 KB
+constexpr int NSTAGE = 2;
+constexpr int NCONV = 512;                   // converter / epilogue threads (warps 0-15)
+constexpr int THREADS = NCONV + 64;          // + MMA warp 16 + W producer warp 17
+constexpr int CORR_MAX = 32;                 // exact W corrections per expert
+constexpr int XC_MAX = 8;                    // exact x terms per row (more: f64 row)
+// control block after the stages: barriers, TMEM slot, per-row scale / flag /
+// x-term lists
+constexpr int C_EMAX = 256, C_RFLAG = C_EMAX + BM * 4, C_XCN = C_RFLAG + BM * 4;
+constexpr int C_XCK = C_XCN + BM * 4, C_XCV = C_XCK + BM * XC_MAX * 4;
+constexpr int CTRL = C_XCV + BM * XC_MAX * 4;
+constexpr size_t SMEM = (size_t)NSTAGE * STAGE + CTRL + 1024;
+// epilogue reuse of the (drained) stage buffers
+constexpr int LGS = NE + 1;                  // padded row strides (bank spread)
+constexpr size_t TBS_OFF = 0;                // folded t-bias, <= 130 samples x 64 f64
+constexpr size_t LG_OFF = 67584;             // fp32 logits [128][65]
+constexpr size_t EX_OFF = 101376;            // f64 exp [128][65]
+constexpr size_t WC_OFF = 167936;            // W corrections staged: k, dw, counts, scales
+constexpr size_t PM_OFF = 193536;            // per-row partial maxima [128][4] fp32
+static_assert(WC_OFF + (size_t)NE * CORR_MAX * 12 + NE * 8 <= (size_t)NSTAGE * STAGE, "epilogue smem");
+static_assert(EX_OFF + (size_t)BM * LGS * 8 <= WC_OFF, "epilogue smem");
+static_assert(LG_OFF + (size_t)BM * LGS * 4 <= EX_OFF, "epilogue smem");
+
+struct Ws {
+  uint8_t* wimg;      // [d/128][LW][64 rows x 128 B, swizzled]
+  int* ew;            // [64] column exponent (biased)
+  int* ccnt;          // [64] corrections per expert
+  int* ck;            // [64][CORR_MAX] k of each correction (ascending)
+  double* cdw;        // [64][CORR_MAX] w - w~ (exact)
+  int* bflag;         // [64] column needs the f64 path for every token
+  unsigned* counter;  // flagged-token count
+  int* list;          // [T] flagged tokens
+};
+inline size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+inline size_t ws_bytes(int64_t T, int d) {
+  return al((size_t)(d / KB) * W_STAGE) + al(NE * 4) * 2 + al((size_t)NE * CORR_MAX * 4) +
+         al((size_t)NE * CORR_MAX * 8) + al(NE * 4) + al(16) + al((size_t)T * 4);
+}
+inline Ws carve(void* base, int64_t T, int d) {
+  uint8_t* p = static_cast<uint8_t*>(base);
+  Ws w;
+  w.wimg = p;                                    p += al((size_t)(d / KB) * W_STAGE);
+  w.ew = reinterpret_cast<int*>(p);              p += al(NE * 4);
+  w.ccnt = reinterpret_cast<int*>(p);            p += al(NE * 4);
+  w.ck = reinterpret_cast<int*>(p);              p += al((size_t)NE * CORR_MAX * 4);
+  w.cdw = reinterpret_cast<double*>(p);          p += al((size_t)NE * CORR_MAX * 8);
+  w.bflag = reinterpret_cast<int*>(p);           p += al(NE * 4);
+  w.counter = reinterpret_cast<unsigned*>(p);    p += al(16);
+  w.list = reinterpret_cast<int*>(p);
+  (void)T;
+  return w;
+}
+
+NIMG_DEV double pow2(int e) {   // 2^e for -1022 <= e <= 1023
+  return __hiloint2double((e + 1023) << 20, 0);
+}
+// 28-bit magnitude -> four 7-bit digits, byte 3 = most significant
+NIMG_DEV uint32_t spread7(uint32_t X) {
+  return (X & 0x7Fu) | ((X << 1) & 0x7F00u) | ((X << 2) & 0x7F0000u) | ((X << 3) & 0x7F000000u);
+}
+// Signed 28-bit X -> its base-128 digits, one per byte: bytes 0-2 unsigned
+// 7-bit, byte 3 the signed top digit (X >> 21), so X = sum_i byte_i 128^i with
+// every byte a valid int8. Each step doubles the part above a digit boundary
+// (inserts the 8th bit), valid for negative X in two's complement too.
+NIMG_DEV uint32_t spread_signed(uint32_t X) {
+  X += X & ~0x7Fu;
+  X += X & ~0x7FFFu;
+  X += X & ~0x7FFFFFu;
+  return X;
+}
+// per-byte negation of digits in [0, 127]
+NIMG_DEV uint32_t neg_bytes(uint32_t Y) { return (0x80808080u - Y) ^ 0x80808080u; }
+NIMG_DEV void bar_conv() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+
+// ------------------------------------------------------------------ prep
+// blocks [0, B*KS): t-half partials (shared with the DMMA router).
+// blocks [B*KS, + 64): block e owns expert column e: the column's max exponent,
+// its five W digit planes written straight into the smem image the scores
+// kernel bulk-copies (K-major, 128-B swizzle), and the exact corrections of
+// the elements below the 35-bit column window, in ascending k.
+__global__ void __launch_bounds__(256)
+router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
+                      double* __restrict__ part, Ws ws, int B, int d) {
+  pdl_trigger();
+  const int KS = router_tpart_ks(d);
+  if ((int)blockIdx.x < B * KS) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *ws.counter = 0u;
+    router_tpart_block(t_emb, w_r, part, blockIdx.x / KS, blockIdx.x % KS, d, NE);
+    return;
+  }
+  __shared__ uint32_t red[8];
+  __shared__ int wsum[8];
+  __shared__ int sbad;
+  const int e = blockIdx.x - B * KS;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t* wu = reinterpret_cast<const uint32_t*>(w_r);
+  uint32_t mx = 0;
+  for (int k = tid; k < d; k += 256) mx = max(mx, __ldg(wu + (int64_t)k * NE + e) & 0x7FFFFFFFu);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if (lane == 0) red[warp] = mx;
+  if (tid == 0) sbad = 0;
+  __syncthreads();
+  mx = red[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = max(mx, red[i]);
+  const int ew = max((int)(mx >> 23), 1);
+  int nc = 0;   // corrections so far (block-uniform)
+  for (int k0 = 0; k0 < d; k0 += 1024) {
+    const int kq = k0 + 4 * tid;   // this thread's 4 consecutive k
+    const bool act = kq < d;
+    uint32_t dig[LW] = {0u, 0u, 0u, 0u, 0u};
+    double dw[4];
+    int has[4] = {0, 0, 0, 0};
+    if (act) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t u = __ldg(wu + (int64_t)(kq + q) * NE + e);
+        const uint32_t mag = u & 0x7FFFFFFFu;
+        const int e8 = (int)(mag >> 23);
+        const uint32_t M = (mag & 0x7FFFFFu) | (e8 ? 0x800000u : 0u);
+        const int ee = max(e8, 1);
+        const int sh = ee - ew + 11;
+        uint64_t Wi;
+        uint32_t res = 0;
+        if (sh >= 0) {
+          Wi = (uint64_t)M << sh;
+        } else {
+          const int r = min(-sh, 25);
+          Wi = r >= 25 ? 0 : (uint64_t)(M >> r);
+          res = M - (uint32_t)(Wi << r);
+        }
+        has[q] = res != 0u;
+        // w - w~ = sign * res * 2^(ee - 150): exact in f64
+        dw[q] = ((u >> 31) ? -1.0 : 1.0) * (double)res * pow2(ee - 150);
+#pragma unroll
+        for (int j = 0; j < LW; ++j) {
+          uint32_t dj = (uint32_t)(Wi >> (7 * (LW - 1 - j))) & 0x7Fu;
+          if (u >> 31) dj = (0x80u - dj) ^ 0x80u;
+          dig[j] |= (dj & 0xFFu) << (8 * q);
+        }
+      }
+      const int kb = kq / KB, kin = kq % KB;
+      const int off = e * KB + ((((kin >> 4) ^ (e & 7)) << 4) | (kin & 15));
+#pragma unroll
+      for (int j = 0; j < LW; ++j)
+        *reinterpret_cast<uint32_t*>(ws.wimg + (size_t)kb * W_STAGE + j * W_SLICE + off) = dig[j];
+    }
+    // block-ordered compaction of the corrections (k ascending)
+    const int cnt = has[0] + has[1] + has[2] + has[3];
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int before = nc, total = nc;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      if (w < warp) before += wsum[w];
+      total += wsum[w];
+    }
+    int pos = before + incl - cnt;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (has[q]) {
+        if (pos < CORR_MAX) {
+          ws.ck[e * CORR_MAX + pos] = kq + q;
+          ws.cdw[e * CORR_MAX + pos] = dw[q];
+        }
+        ++pos;
+      }
+    }
+    nc = total;
+    __syncthreads();   // wsum reuse
+  }
+  if (tid == 0) {
+    ws.ew[e] = ew;
+    ws.ccnt[e] = min(nc, CORR_MAX);
+    // inf / nan in the column, or too many corrections: f64 path for every token
+    ws.bflag[e] = (mx >= 0x7F800000u || nc > CORR_MAX) ? 1 : 0;
+  }
+}
+
+// ------------------------------------------------------------------ scores
+// One CTA per 128 tokens. Warps 0-15 convert x to digit planes (2 jobs of 16
+// elements per thread per stage) and run the epilogue; warp 16 issues the
+// MMAs; warp 17 bulk-copies the W digit planes.
+//
+// The row scale is guessed from the row's first 128 elements (two binades of
+// headroom above their max): any element outside the 21-binade window [emax-20,
+// emax] -- and any zero-exponent or non-finite one -- is left out of the
+// integer sum and added back exactly in f64 from a short per-row list.
+__global__ void __launch_bounds__(THREADS, 1)
+router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_r,
+                        const double* __restrict__ part, Ws ws, float* __restrict__ logits,
+                        float* __restrict__ scores_bes, int B, int S, int d) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ctrl = sm + (size_t)NSTAGE * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ctrl);
+  uint64_t* empty = full + NSTAGE;
+  uint64_t* tfull = empty + NSTAGE;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ctrl + 64);
+  int* emax_s = reinterpret_cast<int*>(ctrl + C_EMAX);
+  int* rflag_s = reinterpret_cast<int*>(ctrl + C_RFLAG);
+  int* xcn = reinterpret_cast<int*>(ctrl + C_XCN);
+  int* xck = reinterpret_cast<int*>(ctrl + C_XCK);
+  float* xcv = reinterpret_cast<float*>(ctrl + C_XCV);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t T = (int64_t)B * S;
+  const int64_t t0 = (int64_t)blockIdx.x * BM;
+  const int rows = (int)(T - t0 < BM ? T - t0 : BM);
+  const int nkb = d / KB;
+  pdl_trigger();
+
+  if (tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) { mbar_init(&full[s], NCONV + 1); mbar_init(&empty[s], 1); }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (tid < BM) { rflag_s[tid] = 0; xcn[tid] = 0; }
+  if (warp == NCONV / 32) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < NCONV / 32) {
+    // ---------------------------------------------- converters
+    // job = tid + 512 jj: tile row job / 8, 16-element chunk job % 8 of the stage
+    const bf16* src[2];
+    bool rv[2];
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const int job = tid + NCONV * jj, r = job >> 3, c = job & 7;
+      rv[jj] = r < rows;
+      src[jj] = x + (t0 + (rv[jj] ? r : 0)) * d + c * 16;
+    }
+    uint4 cur[4], nxt[4];
+    auto load = [&](int kb, uint4 (&buf)[4]) {
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        if (rv[jj]) {
+          const uint4* p = reinterpret_cast<const uint4*>(src[jj] + kb * KB);
+          buf[2 * jj] = __ldg(p);
+          buf[2 * jj + 1] = __ldg(p + 1);
+        } else {
+          buf[2 * jj] = buf[2 * jj + 1] = make_uint4(0u, 0u, 0u, 0u);
+        }
+      }
+    };
+    load(0, cur);
+    // row scale guess from the first stage: the 8 lanes of a row share it
+    int base[2];
+    uint32_t lo7[2], hi7[2];
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) {
+      const uint4 a = cur[2 * jj], b = cur[2 * jj + 1];
+      uint32_t m = __vmaxu2(__vmaxu2(__vmaxu2(a.x & 0x7FFF7FFFu, a.y & 0x7FFF7FFFu),
+                                     __vmaxu2(a.z & 0x7FFF7FFFu, a.w & 0x7FFF7FFFu)),
+                            __vmaxu2(__vmaxu2(b.x & 0x7FFF7FFFu, b.y & 0x7FFF7FFFu),
+                                     __vmaxu2(b.z & 0x7FFF7FFFu, b.w & 0x7FFF7FFFu)));
+      m = max(m & 0xFFFFu, m >> 16);
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
+      const int eg = min(max((int)(m >> 7), 1), 254) + 2;
+      base[jj] = 20 - eg;
+      lo7[jj] = (uint32_t)max(eg - 20, 1) << 7;
+      hi7[jj] = (uint32_t)min(eg, 254) << 7;
+      if ((tid & 7) == 0) emax_s[(tid + NCONV * jj) >> 3] = eg;
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      if (kb + 1 < nkb) load(kb + 1, nxt);
+      mbar_wait(&empty[stage], phase ^ 1);
+      uint8_t* sa = sm + (size_t)stage * STAGE;
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int job = tid + NCONV * jj, r = job >> 3, c = job & 7;
+        const uint32_t wv[8] = {cur[2 * jj].x,     cur[2 * jj].y,     cur[2 * jj].z,     cur[2 * jj].w,
+                                cur[2 * jj + 1].x, cur[2 * jj + 1].y, cur[2 * jj + 1].z, cur[2 * jj + 1].w};
+        // all 16 exponents inside [elo, ehi] (no zero / subnormal / inf / nan):
+        // the branch-free path; otherwise element by element
+        uint32_t mn = 0xFFFFFFFFu, mxe = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          mn = __vminu2(mn, wv[i] & 0x7F807F80u);
+          mxe = __vmaxu2(mxe, wv[i] & 0x7F807F80u);
+        }
+        const bool fast = min(mn & 0xFFFFu, mn >> 16) >= lo7[jj] && max(mxe & 0xFFFFu, mxe >> 16) <= hi7[jj];
+        uint32_t Y[16];
+        if (fast) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const uint32_t w = wv[i];
+            const int ml = (int)(w << 16) >> 31, mh = (int)w >> 31;
+            const uint32_t sl = ((((w & 0x7Fu) | 0x80u) ^ (uint32_t)ml) - (uint32_t)ml);
+            const uint32_t shv = ((((w >> 16) & 0x7Fu) | 0x80u) ^ (uint32_t)mh) - (uint32_t)mh;
+            Y[2 * i] = spread_signed(sl << (((w >> 7) & 0xFFu) + base[jj]));
+            Y[2 * i + 1] = spread_signed(shv << (((w >> 23) & 0xFFu) + base[jj]));
+          }
+        } else {
+#pragma unroll
+          for (int el = 0; el < 16; ++el) {
+            const uint32_t u = (wv[el >> 1] >> (16 * (el & 1))) & 0xFFFFu;
+            const int e8 = (int)((u >> 7) & 0xFFu);
+            const int sh = e8 + base[jj];
+            if (((unsigned)sh > 20u) | ((unsigned)(e8 - 1) > 253u)) {
+              Y[el] = 0u;
+              if (u & 0x7FFFu) {   // exact f64 term in the epilogue
+                const int slot = atomicAdd(&xcn[r], 1);
+                if (slot < XC_MAX) {
+                  xck[r * XC_MAX + slot] = kb * KB + c * 16 + el;
+                  xcv[r * XC_MAX + slot] = __uint_as_float(u << 16);
+                }
+              }
+            } else {
+              const uint32_t m = (u & 0x8000u) ? 0xFFFFFFFFu : 0u;
+              Y[el] = spread_signed(((((u & 0x7Fu) | 0x80u) ^ m) - m) << sh);
+            }
+          }
+        }
+        uint32_t out[LX][4];
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+          // 4x4 byte transpose: out[i] = digit i of elements 4g..4g+3 (byte 3 - i)
+          const uint32_t a0 = __byte_perm(Y[4 * g], Y[4 * g + 1], 0x5140);
+          const uint32_t a1 = __byte_perm(Y[4 * g + 2], Y[4 * g + 3], 0x5140);
+          const uint32_t a2 = __byte_perm(Y[4 * g], Y[4 * g + 1], 0x7362);
+          const uint32_t a3 = __byte_perm(Y[4 * g + 2], Y[4 * g + 3], 0x7362);
+          out[3][g] = __byte_perm(a0, a1, 0x5410);
+          out[2][g] = __byte_perm(a0, a1, 0x7632);
+          out[1][g] = __byte_perm(a2, a3, 0x5410);
+          out[0][g] = __byte_perm(a2, a3, 0x7632);
+        }
+        const int off = r * KB + ((c ^ (r & 7)) << 4);
+#pragma unroll
+        for (int i = 0; i < LX; ++i)
+          *reinterpret_cast<uint4*>(sa + i * A_SLICE + off) =
+              make_uint4(out[i][0], out[i][1], out[i][2], out[i][3]);
+      }
+      fence_proxy_async_smem();
+      mbar_arrive(&full[stage]);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
+      if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+    }
+
+    // ---------------------------------------------- epilogue
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    pdl_wait();   // prep outputs (t-bias partials, scales, corrections)
+    const int64_t b_first = t0 / S;
+    const int nb = (int)((t0 + rows - 1) / S - b_first + 1);
+    double* tbs = reinterpret_cast<double*>(sm + TBS_OFF);
+    float* lgs = reinterpret_cast<float*>(sm + LG_OFF);
+    double* exs = reinterpret_cast<double*>(sm + EX_OFF);
+    int* wck = reinterpret_cast<int*>(sm + WC_OFF);
+    double* wcd = reinterpret_cast<double*>(sm + WC_OFF + NE * CORR_MAX * 4);
+    int* wcn = reinterpret_cast<int*>(sm + WC_OFF + NE * CORR_MAX * 12);
+    int* wew = wcn + NE;
+    for (int i = tid; i < nb * NE; i += NCONV) tbs[i] = router_tbias(part, b_first + i / NE, i % NE, d, NE);
+    for (int i = tid; i < NE * CORR_MAX; i += NCONV) {
+      if (i % CORR_MAX < __ldg(ws.ccnt + i / CORR_MAX)) {
+        wck[i] = __ldg(ws.ck + i);
+        wcd[i] = __ldg(ws.cdw + i);
+      }
+    }
+    if (tid < NE) { wcn[tid] = __ldg(ws.ccnt + tid); wew[tid] = __ldg(ws.ew + tid); }
+    bar_conv();
+
+    const int q = warp & 3, p = warp >> 2;   // TMEM lane quadrant, 16-expert quarter
+    const int r = q * 32 + lane;
+    const bool valid = r < rows;
+    const int64_t t = t0 + (valid ? r : 0);
+    const int b = (int)t / S, srow = (int)t - b * S;   // T < 2^31 (capi check)
+    const double* tbr = tbs + (b - b_first) * NE;
+    const int er = emax_s[r];
+    const int nx = xcn[r];
+    const int nxu = min(nx, XC_MAX);
+    const bf16* xrow = x + t * d;
+    uint32_t fl = nx > XC_MAX;
+    float pm = -INFINITY;   // max of this thread's 16 logits (NaN ignored, as fmax)
+    float* pmx = reinterpret_cast<float*>(sm + PM_OFF);
+    const uint32_t tl = tmem_base + ((uint32_t)(q * 32) << 16);
+#pragma unroll 1
+    for (int ec = 0; ec < 4; ++ec) {
+      const int e0 = p * 16 + ec * 4;
+      uint32_t g[NG][4];
+#pragma unroll
+      for (int s = 0; s < NG; ++s) tmem_ld4(tl + s * NE + e0, g[s]);
+      tmem_ld_wait();
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int e = e0 + j;
+        const int64_t H = (int64_t)(int)g[0][j] * 2097152 + (int64_t)(int)g[1][j] * 16384 +
+                          (int64_t)(int)g[2][j] * 128 + (int64_t)(int)g[3][j];
+        const int64_t L = (int64_t)(int)g[4][j] * 2097152 + (int64_t)(int)g[5][j] * 16384 +
+                          (int64_t)(int)g[6][j] * 128 + (int64_t)(int)g[7][j];
+        const double v = fma((double)H, 268435456.0, (double)L) * pow2(er + wew[e] - 315);
+        double cs = 0.0, ca = 0.0;
+        const int ncw = wcn[e];
+        for (int c = 0; c < ncw; ++c) {   // x~ * (w - w~): x~ = 0 for the row's listed elements
+          const uint32_t u = __bfloat16_as_ushort(xrow[wck[e * CORR_MAX + c]]);
+          const int e8 = (int)((u >> 7) & 0xFFu), sh = e8 + 20 - er;
+          const bool special = ((unsigned)sh > 20u) | ((unsigned)(e8 - 1) > 253u);
+          const double pr = special ? 0.0 : (double)__uint_as_float(u << 16) * wcd[e * CORR_MAX + c];
+          cs += pr;
+          ca += fabs(pr);
+        }
+        for (int c = 0; c < nxu; ++c) {   // (x - x~) * w for the listed elements
+          const double pr = (double)xcv[r * XC_MAX + c] * (double)__ldg(w_r + (int64_t)xck[r * XC_MAX + c] * NE + e);
+          cs += pr;
+          ca += fabs(pr);
+        }
+        const double z = (v + cs) + tbr[e];
+        // rounding of v, of the correction sums and of the two adds
+        const double bound = (2.0 * fabs(v) + (ncw + nxu + 2) * ca + fabs(z)) * 0x1p-52;
+        const float rf = __double2float_rn(z);
+        // rf is the rounding of every value within `bound` of z iff that band
+        // stays strictly inside rf's rounding interval [|rf| - hd, |rf| + hu]
+        // (half the spacing above / below; below is halved at a power of two)
+        const uint32_t fb = __float_as_uint(rf) & 0x7FFFFFFFu;
+        const int ex = (int)(fb >> 23);
+        const double hu = pow2(max(ex, 1) - 151);
+        const double hd = ((fb & 0x7FFFFFu) == 0u && ex > 1) ? 0.5 * hu : hu;
+        const double dd = fabs(z) - (double)__uint_as_float(fb);
+        fl |= (ex == 255) | (fb == 0u) | !((dd - bound > -hd) && (dd + bound < hu));
+        lgs[r * LGS + e] = rf;
+        pm = fmaxf(pm, rf);
+      }
+    }
+    if (fl && valid) atomicOr(&rflag_s[r], 1);
+    pmx[r * 4 + p] = pm;
+    bar_conv();
+    // numpy-order softmax over the 64 experts (tensor.py:467-479): the four
+    // threads of a row compute the same max and sum; each writes its 16
+    const double mxv = (double)fmaxf(fmaxf(pmx[r * 4], pmx[r * 4 + 1]), fmaxf(pmx[r * 4 + 2], pmx[r * 4 + 3]));
+#pragma unroll 4
+    for (int e = p * 16; e < p * 16 + 16; ++e) exs[r * LGS + e] = exp((double)lgs[r * LGS + e] - mxv);
+    bar_conv();
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = exs[r * LGS + j];
+#pragma unroll
+    for (int i = 8; i < NE; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] += exs[r * LGS + i + j];
+    const double sum = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+    if (valid) {
+#pragma unroll 4
+      for (int e = p * 16; e < p * 16 + 16; ++e)
+        scores_bes[((int64_t)b * NE + e) * S + srow] = (float)(exs[r * LGS + e] / sum);
+      float4* lo = reinterpret_cast<float4*>(logits + t * NE + p * 16);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        lo[i] = make_float4(lgs[r * LGS + p * 16 + 4 * i], lgs[r * LGS + p * 16 + 4 * i + 1],
+                            lgs[r * LGS + p * 16 + 4 * i + 2], lgs[r * LGS + p * 16 + 4 * i + 3]);
+      if (p == 0 && rflag_s[r]) ws.list[atomicAdd(ws.counter, 1u)] = (int)t;
+    }
+  } else if (warp == NCONV / 32) {
+    // ---------------------------------------------- MMA issuer
+    if (lane == 0) {
+      // x digit i times [W_0 | W_1 | W_2 | W_3] (N = 256, the slices are
+      // contiguous rows of the stage) lands on the contiguous TMEM groups
+      // i..i+3; W_4 (N = 64) on group i+4.
+      constexpr uint32_t idesc256 = make_idesc_s8(BM, 4 * NE);
+      constexpr uint32_t idesc64 = make_idesc_s8(BM, NE);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(sm + (size_t)stage * STAGE);
+        const uint32_t sw = sa + LX * A_SLICE;
+        const uint64_t b03 = make_sdesc_k128(sw);
+        const uint64_t b4 = make_sdesc_k128(sw + 4 * W_SLICE);
+#pragma unroll
+        for (int kk = 0; kk < KB / 32; ++kk) {
+          const bool first = kb == 0 && kk == 0;
+#pragma unroll
+          for (int i = 0; i < LX; ++i) {
+            const uint64_t adesc = make_sdesc_k128(sa + i * A_SLICE) + 2 * kk;
+            umma_i8(tmem_base + i * NE, adesc, b03 + 2 * kk, idesc256, (first && i == 0) ? 0u : 1u);
+            umma_i8(tmem_base + (i + 4) * NE, adesc, b4 + 2 * kk, idesc64, first ? 0u : 1u);
+          }
+        }
+        umma_commit(&empty[stage]);
+        if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+      }
+      umma_commit(tfull);
+    }
+  } else {
+    // ---------------------------------------------- W digit producer
+    if (lane == 0) {
+      pdl_wait();   // the prep kernel wrote the digit image
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], W_STAGE);
+        bulk_load(sm + (size_t)stage * STAGE + LX * A_SLICE, ws.wimg + (size_t)kb * W_STAGE, W_STAGE,
+                  &full[stage]);
+        if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == NCONV / 32) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ------------------------------------------------------------------ fix-up
+// Flagged tokens (or all of them when W_r could not be written in fixed
+// point): the f64 dot, the t-bias, fp32 rounding and the softmax again.
+// Warp w sums the k-slice [w d/16, (w+1) d/16) for experts 2 lane, 2 lane + 1;
+// the 16 slice sums are folded in a fixed order.
+constexpr int FIX_THREADS = 512;
+__global__ void __launch_bounds__(FIX_THREADS)
+router_fix_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_r,
+                     const double* __restrict__ part, Ws ws, float* __restrict__ logits,
+                     float* __restrict__ scores_bes, int B, int S, int d) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ double red[FIX_THREADS / 32][NE];
+  __shared__ double ex[NE];
+  __shared__ float lg[NE];
+  __shared__ double tot;
+  int all = 0;
+  for (int i = 0; i < NE; ++i) all |= ws.bflag[i];
+  const int64_t T = (int64_t)B * S;
+  const int64_t n = all ? T : (int64_t)*ws.counter;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = FIX_THREADS / 32;
+  const int klen = d / NW, k0 = warp * klen;
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const int64_t t = all ? i : (int64_t)ws.list[i];
+    const int64_t b = t / S, srow = t % S;
+    const bf16* xr = x + t * d;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+    for (int k = k0; k < k0 + klen; ++k) {
+      const double xv = (double)__bfloat162float(xr[k]);
+      const float2 w2 = __ldg(reinterpret_cast<const float2*>(w_r + (int64_t)k * NE) + lane);
+      a0 = fma(xv, (double)w2.x, a0);
+      a1 = fma(xv, (double)w2.y, a1);
+    }
+    red[warp][2 * lane] = a0;
+    red[warp][2 * lane + 1] = a1;
+    __syncthreads();
+    if (threadIdx.x < NE) {
+      const int e = threadIdx.x;
+      double z = red[0][e];
+      for (int w = 1; w < NW; ++w) z += red[w][e];
+      lg[e] = (float)(z + router_tbias(part, b, e, d, NE));
+    }
+    __syncthreads();
+    if (threadIdx.x < NE) {
+      const int e = threadIdx.x;
+      double mxv = -INFINITY;
+      for (int j = 0; j < NE; ++j) mxv = fmax(mxv, (double)lg[j]);
+      ex[e] = exp((double)lg[e] - mxv);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tot = np_pairwise_sum(ex, NE);
+    __syncthreads();
+    if (threadIdx.x < NE) {
+      const int e = threadIdx.x;
+      logits[t * NE + e] = lg[e];
+      scores_bes[(b * NE + e) * S + srow] = (float)(ex[e] / tot);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace ri8
+
+bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm) {
+  // read per call (a getenv is ~100 ns) so tests can compare both routers in one process
+  const char* v = getenv("NIMG_ROUTER");
+  if (v && (!strcmp(v, "dmma") || !strcmp(v, "f64"))) return false;
+  return x_bf16 && E == ri8::NE && d % ri8::KB == 0 && d <= 32768 &&
+         (uintptr_t)x_norm % 16 == 0;
+}
+size_t router_i8_ws_bytes(int64_t T, int d) { return ri8::ws_bytes(T, d); }
+
+cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float* w_r, double* part,
+                             void* i8ws, float* logits, float* scores_bes, int B, int S, int d,
+                             cudaStream_t s) {
+  const int64_t T = (int64_t)B * S;
+  ri8::Ws ws = ri8::carve(i8ws, T, d);
+  // the first kernel of the chain: an ordinary launch (full stream order)
+  ri8::router_prep_i8_kernel<<<B * router_tpart_ks(d) + ri8::NE, 256, 0, s>>>(t_emb, w_r, part, ws,
+                                                                              B, d);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  static bool attr = false;
+  if (!attr) {
+    err = cudaFuncSetAttribute(ri8::router_scores_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)ri8::SMEM);
+    if (err != cudaSuccess) return err;
+    attr = true;
+  }
+  const bf16* x = reinterpret_cast<const bf16*>(x_norm);
+  err = launch_pdl(ri8::router_scores_i8_kernel, dim3((unsigned)((T + ri8::BM - 1) / ri8::BM)),
+                   dim3(ri8::THREADS), ri8::SMEM, s, x, w_r, (const double*)part, ws, logits, scores_bes,
+                   B, S, d);
+  if (err != cudaSuccess) return err;
+  if (const char* st = getenv("NIMG_ROUTER_I8_STATS")) {   // debugging only (synchronises)
+    if (st[0] == '1') {
+      unsigned cnt = 0;
+      int bf[ri8::NE];
+      cudaMemcpyAsync(&cnt, ws.counter, 4, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(bf, ws.bflag, sizeof(bf), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      int all = 0;
+      for (int i = 0; i < ri8::NE; ++i) all |= bf[i];
+      fprintf(stderr, "[router_i8] T=%lld flagged=%u all_fallback=%d\n", (long long)T, cnt, all);
+    }
+  }
+  const char* nofix = getenv("NIMG_ROUTER_I8_NOFIX");   // debugging only: leave flagged tokens
+  if (nofix && nofix[0] == '1') return cudaSuccess;
+  return launch_pdl(ri8::router_fix_i8_kernel, dim3(148), dim3(ri8::FIX_THREADS), 0, s, x, w_r, (const double*)part,
+                    ws, logits, scores_bes, B, S, d);
+}
+
+}  // namespace nimg
