@@ -64,11 +64,14 @@ block_prologue_bf16_kernel(const bf16* __restrict__ x, const bf16* __restrict__ 
       const uint4 rv = __ldg(reinterpret_cast<const uint4*>(rr + c0));
       const bf16* xe = reinterpret_cast<const bf16*>(&xv);
       const bf16* re = reinterpret_cast<const bf16*>(&rv);
+      float g[8];   // per-sample gate: two 16-B loads instead of eight scalar ones
+      *reinterpret_cast<float4*>(g) = __ldg(reinterpret_cast<const float4*>(ths + c0));
+      *reinterpret_cast<float4*>(g + 4) = __ldg(reinterpret_cast<const float4*>(ths + c0) + 1);
       bf16 hv[8];
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         hv[v] = __float2bfloat16_rn(__fadd_rn(__bfloat162float(xe[v]),
-                                              __fmul_rn(__ldg(ths + c0 + v), __bfloat162float(re[v]))));
+                                              __fmul_rn(g[v], __bfloat162float(re[v]))));
         hf[k][v] = __bfloat162float(hv[v]);
         ss = fmaf(hf[k][v], hf[k][v], ss);
       }
@@ -83,11 +86,14 @@ block_prologue_bf16_kernel(const bf16* __restrict__ x, const bf16* __restrict__ 
     const int c0 = (k * 32 + lane) * 8;
     if (c0 < d) {
       bf16 xn[8], xm[8];
+      float o1[8];
+      *reinterpret_cast<float4*>(o1) = __ldg(reinterpret_cast<const float4*>(op + c0));
+      *reinterpret_cast<float4*>(o1 + 4) = __ldg(reinterpret_cast<const float4*>(op + c0) + 1);
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const float xn0 = __bfloat162float(__float2bfloat16_rn(hf[k][v] * inv));
         xn[v] = __float2bfloat16_rn(xn0 * scale_t);
-        xm[v] = __float2bfloat16_rn(__bfloat162float(xn[v]) * __ldg(op + c0 + v));
+        xm[v] = __float2bfloat16_rn(__bfloat162float(xn[v]) * o1[v]);
       }
       *reinterpret_cast<uint4*>(xn_out + t * d + c0) = *reinterpret_cast<const uint4*>(xn);
       *reinterpret_cast<uint4*>(xm_out + t * d + c0) = *reinterpret_cast<const uint4*>(xm);

@@ -919,13 +919,17 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
         const ACC* tg = thg + (t / S) * d + c0 + u * STEP;
         VecIO<TO, VEC> hv;
         hv.load(hres + base);
+        VecIO<ACC, VEC> gv;   // the per-sample gate, vector loads
+        gv.load(tg);
 #pragma unroll
         for (int v = 0; v < VEC; ++v) {
           if constexpr (sizeof(ACC) == 8)   // reference chain: product and sum rounded apart
             res[v] = from_f32<TO>((float)__dadd_rn((double)hv.at(v),
-                                                   __dmul_rn(__ldg(tg + v), (double)to_f32(res[v]))));
+                                                   __dmul_rn(reinterpret_cast<const ACC*>(gv.v)[v],
+                                                             (double)to_f32(res[v]))));
           else
-            res[v] = from_f32<TO>(__fadd_rn(hv.at(v), __fmul_rn(__ldg(tg + v), to_f32(res[v]))));
+            res[v] = from_f32<TO>(__fadd_rn(hv.at(v), __fmul_rn(reinterpret_cast<const ACC*>(gv.v)[v],
+                                                                to_f32(res[v]))));
         }
       }
       TO* o = out + t * d + c0 + u * STEP;
