@@ -44,6 +44,18 @@ CONFIGS = {"cfg2": CFG2, "cfg3": CFG3, "cfg4": CFG4}
 FP64_PEAK_TFLOPS = 37.0
 
 
+def router_uses_i8(c) -> bool:
+    """Mirror of router_i8_eligible (csrc/router_i8.cu): bf16 x_norm, E = 64,
+    d % 128 == 0, unless NIMG_ROUTER=dmma."""
+    return (os.environ.get("NIMG_ROUTER") not in ("dmma", "f64") and c["E"] == 64
+            and c["d"] % 128 == 0)
+
+
+def router_impl(c) -> str:
+    return ("exact INT8 tensor-core digit GEMM (tcgen05 kind::i8) + f64 fix-up" if router_uses_i8(c)
+            else "FP64 tensor pipe (DMMA m8n8k4)")
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -266,11 +278,12 @@ def run_single(args, c, peaks, peak_kind):
         "gemm1_ms": stages["gemm1_swiglu"], "gemm2_ms": stages["gemm2"],
         "combine_ms": stages["combine"],
         "gemm1_tflops": g1_tf, "gemm2_tflops": g2_tf,
-        # router scores kernel (f64-accumulated [x_norm|t_emb] W_r + softmax) vs
-        # the measured FP64 pipe; the rest of route_ms is select + gates
+        # router scores ([x_norm|t_emb] W_r with f64 semantics + softmax); the
+        # rest of route_ms is select + gates
         "router_scores_ms": router_ms,
-        "router_f64_tflops": wc["flops_router"] / (router_ms * 1e-3) / 1e12,
-        "router_frac_of_fp64_peak": wc["flops_router"] / (router_ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+        "router_impl": router_impl(c),
+        # the f64 work the router stands for, per second of router time
+        "router_f64_equiv_tflops": wc["flops_router"] / (router_ms * 1e-3) / 1e12,
         "select_gates_ms": stages["route"] - router_ms,
         "gather_gbs": wc["bytes_gather"] / (stages["gather"] * 1e-3) / 1e9,
         "combine_gbs": wc["bytes_combine"] / (stages["combine"] * 1e-3) / 1e9,
@@ -320,9 +333,15 @@ def run_single(args, c, peaks, peak_kind):
         "train": train,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": (9 if router_uses_i8(c) else 8) * args.steps,
         "clocks": clocks,
     }
+    if router_uses_i8(c):
+        # int8 digit-pair MACs (4 x 5 digit planes of T x d x E) on the tensor pipe
+        macs = 20 * wc["T"] * c["d"] * c["E"]
+        stage_detail["router_int8_tops"] = 2 * macs / (router_ms * 1e-3) / 1e12
+    else:
+        stage_detail["router_frac_of_fp64_peak"] = stage_detail["router_f64_equiv_tflops"] / FP64_PEAK_TFLOPS
     print(json.dumps(line), flush=True)
 
 
