@@ -6,17 +6,21 @@
 // an 8-bit significand and an fp32 W_r a 24-bit one, so the x half is an exact
 // sum of integers once both sides are written in fixed point:
 //
-//   x[t, k] = X[t, k] * 2^(emax_t - 154),  |X| < 2^28  (row scale, 4 signed
-//             7-bit digits X_0..X_3: X = sum_i X_i 2^(7 (3 - i)))
-//   w[k, e] = W[k, e] * 2^(ew_e - 161),    |W| < 2^35  (column scale, 5 digits)
+//   x[t, k] = X[t, k] * 2^(e_t - 134 - XW), |X| < 2^(XW+8)  (row scale;
+//             base-128 digits (LX = 4) X_i: X = sum_i X_i 128^(LX-1-i), the top digit
+//             signed, the others unsigned 7-bit)
+//   w[k, e] = W[k, e] * 2^(ew_e - 161),     |W| < 2^35       (column scale, 5
+//             sign-magnitude digits)
 //
-// and sum_k X W = sum_{s=0..7} G_s 2^(7 (7 - s)), G_s = sum_{i+j=s} sum_k X_i W_j,
+// and sum_k X W = sum_s G_s 128^(NG-1-s), G_s = sum_{i+j=s} sum_k X_i W_j,
 // where every G_s is an int8 x int8 GEMM with int32 accumulation: EXACT, in any
-// order (tcgen05.mma kind::i8, 20 digit-pair MMAs per K step into 8 TMEM
-// accumulators of 64 columns = all 512 TMEM columns). Elements too small for the
-// row / column window are not lost: a W element below 2^-11 of its column max
-// becomes an exact f64 correction term (a short per-expert list), and a row
-// with an x element below 2^-20 of its row max (or a non-finite value) is
+// order (tcgen05.mma kind::i8: per K step, digit i x [W_0|W_1|W_2|W_3] (N = 256)
+// lands on TMEM groups i..i+3 and digit i x W_4 (N = 64) on group i+4).
+// Elements outside the fixed-point windows are not lost: a W element below
+// 2^-11 of its column max becomes an exact f64 correction term (a short
+// per-expert list), and an x element outside its row's XW-binade window (the
+// scale is guessed from the row's first 128 elements, XH binades of headroom)
+// becomes an exact f64 term in a per-row list; a row whose list overflows is
 // recomputed by the f64 fix-up kernel. The epilogue forms v = H 2^28 + L
 // exactly in int64 halves, scales by a power of two, adds the corrections and
 // the f64 t-bias, rounds to fp32 and PROVES the rounding: if the f64 value is
@@ -43,11 +47,19 @@ namespace ri8 {
 constexpr int NE = 64;                       // experts = UMMA N
 constexpr int BM = 128;                      // tokens per CTA = UMMA M = TMEM lanes
 constexpr int KB = 128;                      // k per stage: one 128-B swizzle row of int8
-constexpr int LX = 4, LW = 5, NG = LX + LW - 1;
+// x digit planes: 4 (28-bit window, the default) or 3 (21-bit: measured slower,
+// its narrower window sends ~1 element per row to the exact f64 list); W_r always 5
+#ifndef NIMG_I8_LX
+#define NIMG_I8_LX 4
+#endif
+constexpr int LX = NIMG_I8_LX, LW = 5, NG = LX + LW - 1;
+constexpr int XW = 7 * LX - 8;               // binades of the x window: 13 or 20
+constexpr int XH = LX == 3 ? 1 : 2;          // headroom over the first-stage max
+static_assert(LX == 3 || LX == 4, "x digit planes");
 constexpr int A_SLICE = BM * KB;             // 16 KB
 constexpr int W_SLICE = NE * KB;             // 8 KB
 constexpr int W_STAGE = LW * W_SLICE;        // 40 KB
-constexpr int STAGE = LX * A_SLICE + W_STAGE;   // 104 KB
+constexpr int STAGE = LX * A_SLICE + W_STAGE;   // 88 / 104 KB
 constexpr int NSTAGE = 2;
 constexpr int NCONV = 512;                   // converter / epilogue threads (warps 0-15)
 constexpr int THREADS = NCONV + 64;          // + MMA warp 16 + W producer warp 17
@@ -58,7 +70,10 @@ constexpr int XC_MAX = 8;                    // exact x terms per row (more: f64
 constexpr int C_EMAX = 256, C_RFLAG = C_EMAX + BM * 4, C_XCN = C_RFLAG + BM * 4;
 constexpr int C_XCK = C_XCN + BM * 4, C_XCV = C_XCK + BM * XC_MAX * 4;
 constexpr int CTRL = C_XCV + BM * XC_MAX * 4;
-constexpr size_t SMEM = (size_t)NSTAGE * STAGE + CTRL + 1024;
+constexpr size_t EPI_END = 195584;           // end of the epilogue buffers (below)
+// the stage ring, reused by the epilogue once the MMAs have drained it
+constexpr size_t BUF = (size_t)NSTAGE * STAGE > EPI_END ? (size_t)NSTAGE * STAGE : EPI_END;
+constexpr size_t SMEM = BUF + CTRL + 1024;
 // epilogue reuse of the (drained) stage buffers
 constexpr int LGS = NE + 1;                  // padded row strides (bank spread)
 constexpr size_t TBS_OFF = 0;                // folded t-bias, <= 130 samples x 64 f64
@@ -66,7 +81,8 @@ constexpr size_t LG_OFF = 67584;             // fp32 logits [128][65]
 constexpr size_t EX_OFF = 101376;            // f64 exp [128][65]
 constexpr size_t WC_OFF = 167936;            // W corrections staged: k, dw, counts, scales
 constexpr size_t PM_OFF = 193536;            // per-row partial maxima [128][4] fp32
-static_assert(WC_OFF + (size_t)NE * CORR_MAX * 12 + NE * 8 <= (size_t)NSTAGE * STAGE, "epilogue smem");
+static_assert(WC_OFF + (size_t)NE * CORR_MAX * 12 + NE * 8 <= PM_OFF, "epilogue smem");
+static_assert(PM_OFF + (size_t)BM * 4 * 4 <= EPI_END, "epilogue smem");
 static_assert(EX_OFF + (size_t)BM * LGS * 8 <= WC_OFF, "epilogue smem");
 static_assert(LG_OFF + (size_t)BM * LGS * 4 <= EX_OFF, "epilogue smem");
 
@@ -114,7 +130,7 @@ NIMG_DEV uint32_t spread7(uint32_t X) {
 NIMG_DEV uint32_t spread_signed(uint32_t X) {
   X += X & ~0x7Fu;
   X += X & ~0x7FFFu;
-  X += X & ~0x7FFFFFu;
+  if (LX == 4) X += X & ~0x7FFFFFu;
   return X;
 }
 // per-byte negation of digits in [0, 127]
@@ -247,7 +263,7 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
                         float* __restrict__ scores_bes, int B, int S, int d) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* ctrl = sm + (size_t)NSTAGE * STAGE;
+  uint8_t* ctrl = sm + BUF;
   uint64_t* full = reinterpret_cast<uint64_t*>(ctrl);
   uint64_t* empty = full + NSTAGE;
   uint64_t* tfull = empty + NSTAGE;
@@ -316,9 +332,9 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
       m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
-      const int eg = min(max((int)(m >> 7), 1), 254) + 2;
-      base[jj] = 20 - eg;
-      lo7[jj] = (uint32_t)max(eg - 20, 1) << 7;
+      const int eg = min(max((int)(m >> 7), 1), 254) + XH;
+      base[jj] = XW - eg;
+      lo7[jj] = (uint32_t)max(eg - XW, 1) << 7;
       hi7[jj] = (uint32_t)min(eg, 254) << 7;
       if ((tid & 7) == 0) emax_s[(tid + NCONV * jj) >> 3] = eg;
     }
@@ -359,7 +375,7 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
             const uint32_t u = (wv[el >> 1] >> (16 * (el & 1))) & 0xFFFFu;
             const int e8 = (int)((u >> 7) & 0xFFu);
             const int sh = e8 + base[jj];
-            if (((unsigned)sh > 20u) | ((unsigned)(e8 - 1) > 253u)) {
+            if (((unsigned)sh > (unsigned)XW) | ((unsigned)(e8 - 1) > 253u)) {
               Y[el] = 0u;
               if (u & 0x7FFFu) {   // exact f64 term in the epilogue
                 const int slot = atomicAdd(&xcn[r], 1);
@@ -382,10 +398,10 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
           const uint32_t a1 = __byte_perm(Y[4 * g + 2], Y[4 * g + 3], 0x5140);
           const uint32_t a2 = __byte_perm(Y[4 * g], Y[4 * g + 1], 0x7362);
           const uint32_t a3 = __byte_perm(Y[4 * g + 2], Y[4 * g + 3], 0x7362);
-          out[3][g] = __byte_perm(a0, a1, 0x5410);
-          out[2][g] = __byte_perm(a0, a1, 0x7632);
-          out[1][g] = __byte_perm(a2, a3, 0x5410);
-          out[0][g] = __byte_perm(a2, a3, 0x7632);
+          out[LX - 1][g] = __byte_perm(a0, a1, 0x5410);
+          out[LX - 2][g] = __byte_perm(a0, a1, 0x7632);
+          out[LX - 3][g] = __byte_perm(a2, a3, 0x5410);
+          if (LX == 4) out[0][g] = __byte_perm(a2, a3, 0x7632);
         }
         const int off = r * KB + ((c ^ (r & 7)) << 4);
 #pragma unroll
@@ -447,17 +463,19 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int e = e0 + j;
-        const int64_t H = (int64_t)(int)g[0][j] * 2097152 + (int64_t)(int)g[1][j] * 16384 +
-                          (int64_t)(int)g[2][j] * 128 + (int64_t)(int)g[3][j];
-        const int64_t L = (int64_t)(int)g[4][j] * 2097152 + (int64_t)(int)g[5][j] * 16384 +
-                          (int64_t)(int)g[6][j] * 128 + (int64_t)(int)g[7][j];
-        const double v = fma((double)H, 268435456.0, (double)L) * pow2(er + wew[e] - 315);
+        // v = sum_s G_s 128^(NG-1-s) = H 2^28 + L, H and L exact in int64
+        int64_t H = 0;
+#pragma unroll
+        for (int s = 0; s < NG - 4; ++s) H = H * 128 + (int64_t)(int)g[s][j];
+        const int64_t L = (int64_t)(int)g[NG - 4][j] * 2097152 + (int64_t)(int)g[NG - 3][j] * 16384 +
+                          (int64_t)(int)g[NG - 2][j] * 128 + (int64_t)(int)g[NG - 1][j];
+        const double v = fma((double)H, 268435456.0, (double)L) * pow2(er + wew[e] - 295 - XW);
         double cs = 0.0, ca = 0.0;
         const int ncw = wcn[e];
         for (int c = 0; c < ncw; ++c) {   // x~ * (w - w~): x~ = 0 for the row's listed elements
           const uint32_t u = __bfloat16_as_ushort(xrow[wck[e * CORR_MAX + c]]);
-          const int e8 = (int)((u >> 7) & 0xFFu), sh = e8 + 20 - er;
-          const bool special = ((unsigned)sh > 20u) | ((unsigned)(e8 - 1) > 253u);
+          const int e8 = (int)((u >> 7) & 0xFFu), sh = e8 + XW - er;
+          const bool special = ((unsigned)sh > (unsigned)XW) | ((unsigned)(e8 - 1) > 253u);
           const double pr = special ? 0.0 : (double)__uint_as_float(u << 16) * wcd[e * CORR_MAX + c];
           cs += pr;
           ca += fabs(pr);
