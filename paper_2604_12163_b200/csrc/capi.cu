@@ -171,14 +171,17 @@ struct RouteWs {
   double* wd;
   int16_t* slot_of;
   unsigned* counters;
-  void* i8;   // INT8 router scratch (router_i8.cu)
+  void* i8;        // INT8 router scratch (router_i8.cu)
+  int* bg_flags;   // GEMM1 background-gather flags, one per 32 routed rows
 };
+int64_t bg_flag_count(const nimg_moe_desc* d) { return (d->E * d->B * d->cap + 31) / 32; }
 size_t slot_bytes(const nimg_moe_desc* d) { return (size_t)d->E * d->B * d->S * 2; }
 size_t route_ws_bytes(const nimg_moe_desc* d) {
   return align_up((size_t)d->B * d->E * 8) +
          align_up(router_part_bytes((int)d->B, (int)d->d, (int)d->E)) +
          align_up(router_wd_bytes((int)d->d, (int)d->E)) + align_up(slot_bytes(d)) +
-         align_up((size_t)d->B * 4) + align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d));
+         align_up((size_t)d->B * 4) + align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d)) +
+         align_up((size_t)bg_flag_count(d) * 4);
 }
 RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
@@ -194,6 +197,8 @@ RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   r.counters = reinterpret_cast<unsigned*>(p);
   p += align_up((size_t)d->B * 4);
   r.i8 = p;
+  p += align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d));
+  r.bg_flags = reinterpret_cast<int*>(p);
   return r;
 }
 
@@ -294,7 +299,7 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
                     const void* xs, const void* sw1, const void* sw3, const void* sw2, void* ys,
                     void* ws, size_t ws_bytes, cudaStream_t st,
                     const int32_t* gather_idx = nullptr, int64_t gather_src_rows = 0,
-                    const FfnTrain* tr = nullptr) {
+                    const FfnTrain* tr = nullptr, const BgGather* bg = nullptr) {
   NIMG_TRY(check_ffn(f, off, ex));
   if (!tr && ws_bytes < ffn_ws_bytes(f)) return fail(NIMG_ERR_CONFIG, "workspace too small");
   const bool has_r = f->n_rows > 0, has_s = f->n_shared_rows > 0;
@@ -347,6 +352,7 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       if (!has_s) { tm.a[1] = tm.a[rb]; tm.b[1] = tm.b[rb]; tm.b3[1] = tm.b3[rb]; }
       p.bank[0] = GBank{pre_r, h, d, h, (h + bn - 1) / bn, 0, gather_idx, gather_idx ? xr : nullptr, h_r};
       p.bank[1] = GBank{pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, nullptr, nullptr, h_s};
+      if (bg && pair && has_r && has_s && !gather_idx) p.bg = *bg;
       if (pair) CUDA_TRY(launch_grouped_tc_pair(0, tm, p, sms, st));
       else CUDA_TRY(launch_grouped_tc(0, tm, p, sms, st));
       mark(3, st);
@@ -429,7 +435,8 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
   CUDA_TRY(launch_ec_select(o->scores_bes, o->token_flat, o->gate_raw, w.slot_of, B, S, E, cap, st));
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
   CUDA_TRY(launch_gate_norm(o->scores_bes, w.slot_of, o->gates, o->comb_rows, o->comb_cnt, B, S,
-                            E, cap, d->gate_eps, d->gate_scale, st));
+                            E, cap, d->gate_eps, d->gate_scale, st, w.bg_flags,
+                            (int)bg_flag_count(d)));
   return NIMG_OK;
 }
 
@@ -441,6 +448,13 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, c
 // LDGSTS sustains ~8 B/cycle/SM and gather4 issues at ~45 cycles per 512 B,
 // against the ~36 B/cycle/SM of A operand the UMMA consumes (GEMM1 1.51 ms /
 // 1.83 ms fused vs 0.63 ms + 0.064 ms separate gather at cfg2).
+bool use_bg_gather() {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_BG_GATHER");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 bool use_fused_gather(int32_t path, int64_t d) {
   static const bool on = [] {
     const char* e = getenv("NIMG_FUSED_GATHER");
@@ -756,10 +770,19 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   void* ys = w;
   if (state) { xg = ts.xg; yr = ts.y_r; }
 
+  // the routed-row gather runs inside GEMM1 (background warps) on the tcgen05
+  // pair path; NIMG_BG_GATHER=0 keeps the separate gather kernel
+  const bool bg_gather = !fused_gather && path == NIMG_PATH_TCGEN05 && use_pair_kernels() &&
+                         use_bg_gather() && f.n_rows > 0 && f.n_shared_rows > 0 &&
+                         (d->d * elt(d->act_dtype)) % 16 == 0;
+  BgGather bg{};
+  if (bg_gather)
+    bg = BgGather{p->x_mod, p->route.token_flat, xg, carve_route(d, route_ws).bg_flags,
+                  (int)f.n_rows, (int)(d->d * elt(d->act_dtype))};
   mark(0, st);
   NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st));
   mark(1, st);
-  if (!fused_gather)
+  if (!fused_gather && !bg_gather)
     CUDA_TRY(launch_gather_rows(p->x_mod, d->d * (int64_t)elt(d->act_dtype), p->route.token_flat,
                                 f.n_rows, xg, st));
   mark(2, st);
@@ -770,7 +793,7 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   NIMG_TRY(expert_ffn_impl(&f, off, nullptr, fused_gather ? p->x_mod : xg, p->w1, p->w3, p->w2, yr,
                            p->x_mod, p->sw1, p->sw3, p->sw2, ys, ffn_ws, ffn_ws_bytes(&f), st,
                            fused_gather ? p->route.token_flat : nullptr, d->B * d->S,
-                           state ? &tr : nullptr));
+                           state ? &tr : nullptr, bg_gather ? &bg : nullptr));
   mark(4, st);
   CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys, p->route.gates,
                           p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,

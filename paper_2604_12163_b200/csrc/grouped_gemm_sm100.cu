@@ -322,8 +322,33 @@ NIMG_DEV void decode_pair_tile(const GroupedParams& p, int t, TileInfo& ti) {
 // tiles the gather threads arrive without copying.
 constexpr int kGatherWarps = 2;
 
-template <int MODE, bool GATHER, int STAGES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (GATHER ? 32 * (kGatherWarps + 1) : 0), 1)
+// BG (GEMM1, 1-GPU layer): kBgWarps (2: measured best of 2/4/8 -- more copy
+// warps slow the power-capped GEMM more than they gain) extra warps (6..) per CTA run the routed-
+// row gather (moe.py:152-153) in the background: global -> global copies of
+// 32-row sub-blocks, each published with a release flag. The tile order is
+// rotated so the shared expert's tiles (no gathered operand) run first; the
+// TMA producer of a routed tile acquires the flags of its rows and fences the
+// async proxy before loading them. All CTAs are resident (persistent grid),
+// and the copies depend on nothing but the routing, so the waits cannot
+// deadlock. The gather's HBM traffic overlaps the shared tiles' tensor work.
+#ifndef NIMG_BG_WARPS
+#define NIMG_BG_WARPS 2
+#endif
+constexpr int kBgWarps = NIMG_BG_WARPS;
+constexpr int kBgRows = 32;
+
+NIMG_DEV int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+NIMG_DEV void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+NIMG_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+template <int MODE, bool GATHER, int STAGES, bool BG = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads + (GATHER ? 32 * (kGatherWarps + 1) : 0) + (BG ? 32 * kBgWarps : 0), 1)
 grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constant__ GroupedParams p) {
   using C = PairCfg<MODE>;
   constexpr int SB = pair_stage_bytes<MODE>();
@@ -365,14 +390,26 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   pdl_wait();   // setup above overlapped the previous kernel; inputs are ready now
+  // BG: visit the shared bank's tiles (the tail of the tile list) first
+  const int rot = BG ? p.seg_tile0[p.nseg0] : 0;
+  auto tile_at = [&](int t) { return BG ? (t + rot < p.total_tiles ? t + rot : t + rot - p.total_tiles) : t; };
 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer (both CTAs)
       int stage = 0; uint32_t phase = 0;
       for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
-        TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+        TileInfo ti; decode_pair_tile<MODE>(p, tile_at(t), ti);
         const int a_row = ti.a_row + (int)crank * BM;
+        if (BG && ti.bank == 0) {
+          // acquire the background-gathered rows of this CTA's half tile
+          const int r1 = min(ti.rows_valid, ((int)crank + 1) * BM) - (int)crank * BM;
+          if (r1 > 0) {
+            for (int j = a_row / kBgRows; j <= (a_row + r1 - 1) / kBgRows; ++j)
+              while (ld_acquire_gpu(p.bg.flags + j) == 0) { }
+            fence_proxy_async_global();
+          }
+        }
         for (int kb = 0; kb < ti.nk; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * SB;
@@ -398,7 +435,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
       for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
-        TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+        TileInfo ti; decode_pair_tile<MODE>(p, tile_at(t), ti);
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
@@ -425,7 +462,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
     const uint32_t sbase = smem_u32(smem);
     int stage = 0; uint32_t phase = 0;
     for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
-      TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+      TileInfo ti; decode_pair_tile<MODE>(p, tile_at(t), ti);
       const GBank& bk = p.bank[ti.bank];
       const int32_t* idx = bk.a_idx;
       // this lane's 16 rows of the CTA's 128 (row = gl/8 + 8j) and its 16-B column chunk
@@ -461,13 +498,54 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
     if (lane == 0) {
       int stage = 0; uint32_t phase = 0;
       for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
-        TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+        TileInfo ti; decode_pair_tile<MODE>(p, tile_at(t), ti);
         for (int kb = 0; kb < ti.nk; ++kb) {
           mbar_wait(&gfull[stage], phase);
           mbar_arrive_cluster(mapa_shared(smem_u32(&full[stage]), 0));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
+    }
+  } else if (BG && warp >= 6) {
+    // ------------------------------------------------ background gather (warps 6.., both CTAs)
+    const int gw = (int)blockIdx.x * kBgWarps + (warp - 6);
+    const int ngw = (int)gridDim.x * kBgWarps;
+    const int nsub = (p.bg.rows + kBgRows - 1) / kBgRows;
+    const int nv = p.bg.row_bytes >> 4;   // 16-B vectors per row
+    const uint4* src = reinterpret_cast<const uint4*>(p.bg.src);
+    uint4* dst = reinterpret_cast<uint4*>(p.bg.dst);
+    for (int j = gw; j < nsub; j += ngw) {
+      const int r0 = j * kBgRows;
+      const int nr = min(kBgRows, p.bg.rows - r0);
+      const int my_src = lane < nr ? __ldg(p.bg.idx + r0 + lane) : 0;
+#pragma unroll 1
+      for (int r = 0; r < nr; r += 2) {   // two rows (16 x 16 B per lane) in flight
+        const int s0 = __shfl_sync(0xffffffffu, my_src, r);
+        const int s1 = __shfl_sync(0xffffffffu, my_src, min(r + 1, nr - 1));
+        const uint4* a0 = src + (int64_t)s0 * nv;
+        const uint4* a1 = src + (int64_t)s1 * nv;
+        uint4* d0 = dst + (int64_t)(r0 + r) * nv;
+#pragma unroll 1
+        for (int cb = 0; cb < nv; cb += 256) {
+          uint4 v0[8], v1[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = cb + lane + 32 * i;
+            if (c < nv) { v0[i] = __ldg(a0 + c); v1[i] = __ldg(a1 + c); }
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = cb + lane + 32 * i;
+            if (c < nv) {
+              d0[c] = v0[i];
+              if (r + 1 < nr) d0[nv + c] = v1[i];
+            }
+          }
+        }
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu(p.bg.flags + j, 1);
     }
   } else if (warp >= 2 && warp < 6) {
     // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
@@ -477,7 +555,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
     const uint32_t tempty_leader1 = mapa_shared(smem_u32(&tempty[1]), 0);
     int acc = 0; uint32_t acc_phase = 0;
     for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
-      TileInfo ti; decode_pair_tile<MODE>(p, t, ti);
+      TileInfo ti; decode_pair_tile<MODE>(p, tile_at(t), ti);
       const GBank& bk = p.bank[ti.bank];
       const int Nb = ti.bank ? p.bank[1].N : p.bank[0].N;   // immediate-offset constant reads
       void* const h_out = ti.bank ? p.bank[1].h_out : p.bank[0].h_out;
@@ -534,18 +612,18 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
 int tc_bn_out(int mode) { return mode == 0 ? tc::Cfg<0>::BN_OUT : tc::Cfg<1>::BN_OUT; }
 int tc_pair_rows() { return tc::PBM; }
 
-template <int MODE, bool GATHER, int STAGES>
+template <int MODE, bool GATHER, int STAGES, bool BG = false>
 static cudaError_t launch_pair(const TmapSet& tm, const GroupedParams& p, int grid, cudaStream_t stream) {
   constexpr int smem = tc::pair_smem_bytes<MODE, STAGES>();
-  constexpr int threads = tc::kThreads + (GATHER ? 32 * (tc::kGatherWarps + 1) : 0);
+  constexpr int threads = tc::kThreads + (GATHER ? 32 * (tc::kGatherWarps + 1) : 0) + (BG ? 32 * tc::kBgWarps : 0);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES>,
+    cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES, BG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_pdl(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES>, dim3(grid), dim3(threads),
+  return launch_pdl(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES, BG>, dim3(grid), dim3(threads),
                     (size_t)smem, stream, tm, p);
 }
 
@@ -568,6 +646,7 @@ cudaError_t launch_grouped_tc_pair(int mode, const TmapSet& tm, const GroupedPar
   const bool shallow = pair_stages() == 4;
   if (mode == 0) {
     if (gather) return launch_pair<0, true, 6>(tm, p, grid, stream);
+    if (p.bg.src != nullptr) return launch_pair<0, false, 6, true>(tm, p, grid, stream);
     return shallow ? launch_pair<0, false, 4>(tm, p, grid, stream) : launch_pair<0, false, 6>(tm, p, grid, stream);
   }
   return shallow ? launch_pair<1, false, 4>(tm, p, grid, stream) : launch_pair<1, false, 6>(tm, p, grid, stream);

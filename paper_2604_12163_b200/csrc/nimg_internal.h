@@ -31,8 +31,20 @@ struct GBank {
 // Segments [0, nseg0) use bank 0, [nseg0, nseg) bank 1. Segment i covers rows
 // [seg_row0[i], seg_row0[i] + seg_rows[i]) of its bank's A / out tensors and
 // multiplies them by expert seg_expert[i] of that bank.
+// Background gather (GEMM1, 1-GPU layer): extra warps of the GEMM copy the
+// routed rows bg_dst[r] = bg_src[bg_idx[r]] in 32-row sub-blocks while the
+// shared expert's tiles (scheduled first) run, and publish bg_flags[sub] = 1;
+// a routed tile's TMA producer waits for the flags of its rows.
+struct BgGather {
+  const void* src;       // x_mod rows
+  const int32_t* idx;    // token_flat
+  void* dst;             // gathered rows (the routed bank's A operand)
+  int* flags;            // one per 32-row sub-block, zeroed by gate_norm
+  int rows, row_bytes;   // null src: off
+};
 struct GroupedParams {
   GBank bank[2];
+  BgGather bg;
   int nseg0, nseg, total_tiles, pad_;
   int seg_tile0[kMaxSeg + 1];
   int seg_row0[kMaxSeg];
@@ -182,7 +194,8 @@ cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s);
 cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,
                              int32_t* comb_rows, int32_t* comb_cnt, int B, int S, int E, int cap,
-                             float gate_eps, float gate_scale, cudaStream_t s);
+                             float gate_eps, float gate_scale, cudaStream_t s, int* bg_flags = nullptr,
+                             int n_bg_flags = 0);
 cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
                                int64_t n_idx, void* dst, cudaStream_t s);
 // out[t] = fp32(fp32(sum_k fp32(Y[rows[k][t]] * gate)) + shared[t]) -- see combine kernel.

@@ -760,13 +760,17 @@ __global__ void __launch_bounds__(GN_WARPS * 32)
 gate_norm_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict__ slot_of,
                  float* __restrict__ gates, int32_t* __restrict__ comb_rows,
                  int32_t* __restrict__ comb_cnt, int B, int S, int E, int cap, float eps32,
-                 float alpha32) {
+                 float alpha32, int* __restrict__ bg_flags, int n_bg_flags) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float* raw_l = reinterpret_cast<float*>(sm) + (size_t)warp * E;
   int32_t* row_l = reinterpret_cast<int32_t*>(sm + (size_t)GN_WARPS * E * 4) + (size_t)warp * E;
   pdl_trigger();
   pdl_wait();
+  // arm the next GEMM1's background-gather flags (it waits on this kernel)
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bg_flags;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bg_flags[i] = 0;
   const int64_t T = (int64_t)B * S;
   const int64_t t = (int64_t)blockIdx.x * GN_WARPS + warp;
   if (t >= T) return;
@@ -1044,12 +1048,14 @@ cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float
 
 cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,
                              int32_t* comb_rows, int32_t* comb_cnt, int B, int S, int E, int cap,
-                             float gate_eps, float gate_scale, cudaStream_t s) {
+                             float gate_eps, float gate_scale, cudaStream_t s, int* bg_flags,
+                             int n_bg_flags) {
   const int64_t T = (int64_t)B * S;
   const int grid = (int)((T + GN_WARPS - 1) / GN_WARPS);
   const size_t smem = (size_t)GN_WARPS * E * 8;
   return launch_pdl(gate_norm_kernel, dim3(grid), dim3(GN_WARPS * 32), smem, s, scores_bes, slot_of,
-                    gates, comb_rows, comb_cnt, B, S, E, cap, gate_eps, gate_scale);
+                    gates, comb_rows, comb_cnt, B, S, E, cap, gate_eps, gate_scale, bg_flags,
+                    n_bg_flags);
 }
 
 cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
