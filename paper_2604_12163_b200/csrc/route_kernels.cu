@@ -839,7 +839,10 @@ __global__ void gather_rows_byte_kernel(const uint8_t* __restrict__ src, int64_t
 // token: the token's row list and gates are staged in smem, then each lane
 // issues the loads of up to CB_BATCH rows before consuming any of them.
 constexpr int CB_WARPS = 8;
-constexpr int CB_BATCH = 8;
+#ifndef NIMG_CB_BATCH
+#define NIMG_CB_BATCH 8
+#endif
+constexpr int CB_BATCH = NIMG_CB_BATCH;
 
 template <typename T, int VEC> struct VecIO {
   static_assert(VEC * sizeof(T) % 16 == 0 || VEC == 1, "vector width");
