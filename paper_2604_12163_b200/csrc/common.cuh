@@ -108,6 +108,10 @@ template <int N> NIMG_DEV void bulk_wait_read() {
 }
 template <int N> NIMG_DEV void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
 NIMG_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// Bulk L2 prefetch of `bytes` (multiple of 16) starting at a 16-B aligned address.
+NIMG_DEV void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // ---------------------------------------------------------------- clusters
 NIMG_DEV uint32_t cluster_ctarank() {

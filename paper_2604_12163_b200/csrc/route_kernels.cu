@@ -876,9 +876,18 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
   const int64_t t = (int64_t)blockIdx.x * CB_WARPS + warp;
   if (t >= T) return;
   const int cnt = comb_cnt[t];
+  const uint32_t row_bytes = (uint32_t)((int64_t)d * sizeof(TY));
+#ifndef NIMG_CB_NO_PREFETCH
+  // whole-row L2 prefetches (one bulk instruction per row) as soon as the
+  // row list is known: the column loop's loads then hit L2
+  if (lane == 0 && row_bytes % 16 == 0) bulk_prefetch_l2(ys + t * d, row_bytes);
+#endif
   for (int k = lane; k < cnt; k += 32) {
     const int32_t r = comb_rows[t * E + k];
     rows[k] = r;
+#ifndef NIMG_CB_NO_PREFETCH
+    if (row_bytes % 16 == 0) bulk_prefetch_l2(yr + (int64_t)r * d, row_bytes);
+#endif
     gl[k] = gates != nullptr ? gates[r] : 1.0f;   // null: unit gates (gather pullback)
   }
   __syncwarp();
