@@ -122,6 +122,14 @@ def test_ep_two_gpus_bitwise():
         assert res[r] == {"plain": True, "nccl": True, "ce": True}, res
 
 
+def test_ep_four_gpus_bitwise():
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    res = _run(4, (4, 1024, 2048, 64, 1344, 4.0), modes=("ce",))
+    for r in range(4):
+        assert res[r] == {"ce": True}, res
+
+
 @pytest.mark.parametrize("world", [4, 8])
 def test_ep_oversubscribed_ce_bitwise(world):
     """R ranks on fewer GPUs (rank % n_gpus): exercises the R-peer copy-engine
