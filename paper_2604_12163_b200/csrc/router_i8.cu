@@ -63,7 +63,8 @@ constexpr int STAGE = LX * A_SLICE + W_STAGE;   // 88 / 104 KB
 constexpr int NSTAGE = 2;
 constexpr int NCONV = 512;                   // converter / epilogue threads (warps 0-15)
 constexpr int THREADS = NCONV + 64;          // + MMA warp 16 + W producer warp 17
-constexpr int CORR_MAX = 32;                 // exact W corrections per expert
+constexpr int CORR_MAX = 256;                // exact W corrections per expert (more: f64 path)
+constexpr int CORR_SM = 32;                  // of them staged in smem for the epilogue
 constexpr int XC_MAX = 8;                    // exact x terms per row (more: f64 row)
 // control block after the stages: barriers, TMEM slot, per-row scale / flag /
 // x-term lists
@@ -81,7 +82,7 @@ constexpr size_t LG_OFF = 67584;             // fp32 logits [128][65]
 constexpr size_t EX_OFF = 101376;            // f64 exp [128][65]
 constexpr size_t WC_OFF = 167936;            // W corrections staged: k, dw, counts, scales
 constexpr size_t PM_OFF = 193536;            // per-row partial maxima [128][4] fp32
-static_assert(WC_OFF + (size_t)NE * CORR_MAX * 12 + NE * 8 <= PM_OFF, "epilogue smem");
+static_assert(WC_OFF + (size_t)NE * CORR_SM * 12 + NE * 8 <= PM_OFF, "epilogue smem");
 static_assert(PM_OFF + (size_t)BM * 4 * 4 <= EPI_END, "epilogue smem");
 static_assert(EX_OFF + (size_t)BM * LGS * 8 <= WC_OFF, "epilogue smem");
 static_assert(LG_OFF + (size_t)BM * LGS * 4 <= EX_OFF, "epilogue smem");
@@ -426,14 +427,15 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
     float* lgs = reinterpret_cast<float*>(sm + LG_OFF);
     double* exs = reinterpret_cast<double*>(sm + EX_OFF);
     int* wck = reinterpret_cast<int*>(sm + WC_OFF);
-    double* wcd = reinterpret_cast<double*>(sm + WC_OFF + NE * CORR_MAX * 4);
-    int* wcn = reinterpret_cast<int*>(sm + WC_OFF + NE * CORR_MAX * 12);
+    double* wcd = reinterpret_cast<double*>(sm + WC_OFF + NE * CORR_SM * 4);
+    int* wcn = reinterpret_cast<int*>(sm + WC_OFF + NE * CORR_SM * 12);
     int* wew = wcn + NE;
     for (int i = tid; i < nb * NE; i += NCONV) tbs[i] = router_tbias(part, b_first + i / NE, i % NE, d, NE);
-    for (int i = tid; i < NE * CORR_MAX; i += NCONV) {
-      if (i % CORR_MAX < __ldg(ws.ccnt + i / CORR_MAX)) {
-        wck[i] = __ldg(ws.ck + i);
-        wcd[i] = __ldg(ws.cdw + i);
+    for (int i = tid; i < NE * CORR_SM; i += NCONV) {
+      const int ee = i / CORR_SM, c = i % CORR_SM;
+      if (c < __ldg(ws.ccnt + ee)) {
+        wck[i] = __ldg(ws.ck + ee * CORR_MAX + c);
+        wcd[i] = __ldg(ws.cdw + ee * CORR_MAX + c);
       }
     }
     if (tid < NE) { wcn[tid] = __ldg(ws.ccnt + tid); wew[tid] = __ldg(ws.ew + tid); }
@@ -473,10 +475,13 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
         double cs = 0.0, ca = 0.0;
         const int ncw = wcn[e];
         for (int c = 0; c < ncw; ++c) {   // x~ * (w - w~): x~ = 0 for the row's listed elements
-          const uint32_t u = __bfloat16_as_ushort(xrow[wck[e * CORR_MAX + c]]);
+          const bool in_sm = c < CORR_SM;
+          const int kc = in_sm ? wck[e * CORR_SM + c] : __ldg(ws.ck + e * CORR_MAX + c);
+          const double dwc = in_sm ? wcd[e * CORR_SM + c] : __ldg(ws.cdw + e * CORR_MAX + c);
+          const uint32_t u = __bfloat16_as_ushort(xrow[kc]);
           const int e8 = (int)((u >> 7) & 0xFFu), sh = e8 + XW - er;
           const bool special = ((unsigned)sh > (unsigned)XW) | ((unsigned)(e8 - 1) > 253u);
-          const double pr = special ? 0.0 : (double)__uint_as_float(u << 16) * wcd[e * CORR_MAX + c];
+          const double pr = special ? 0.0 : (double)__uint_as_float(u << 16) * dwc;
           cs += pr;
           ca += fabs(pr);
         }

@@ -99,11 +99,19 @@ def test_i8_router_window_escapes():
     _check(inp, 2.0)
 
 
+def test_i8_router_many_corrections():
+    """A heavy-tailed column: 200 elements far below its max stay on the int8
+    path as exact corrections (list of up to 256 per expert), bit-exact."""
+    inp = make_router_inputs(8, 2, 256, 1024, 64, mode="bf16")
+    inp["w_r"][:200, 13] = np.float32(1e-10)
+    _check(inp, 4.0)
+
+
 def test_i8_router_all_tokens_fallback():
     """More tiny W_r elements in one column than the correction list holds:
     every token takes the f64 path, still bit-exact."""
     inp = make_router_inputs(8, 2, 256, 1024, 64, mode="bf16")
-    inp["w_r"][:100, 13] = np.float32(1e-10)
+    inp["w_r"][:300, 13] = np.float32(1e-10)
     _check(inp, 4.0)
 
 
