@@ -335,7 +335,9 @@ def run_single(args, c, peaks, peak_kind):
         "train": train,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": (9 if router_uses_i8(c) else 8) * args.steps,
+        # router (prep + scores [+ INT8 fix-up]) + select + gates [+ gather] + GEMM1 + GEMM2 + combine
+        "gpu_launches": ((3 if router_uses_i8(c) else 2) + 2
+                         + (0 if os.environ.get("NIMG_BG_GATHER", "1") != "0" else 1) + 3) * args.steps,
         "clocks": clocks,
     }
     if router_uses_i8(c):
