@@ -686,8 +686,16 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
                    dim3(ri8::THREADS), ri8::SMEM, s, x, w_r, (const double*)part, ws, logits, scores_bes,
                    B, S, d);
   if (err != cudaSuccess) return err;
-  if (const char* st = getenv("NIMG_ROUTER_I8_STATS")) {   // debugging only (synchronises)
-    if (st[0] == '1') {
+  static const bool stats = [] {   // debugging only (synchronises)
+    const char* v = getenv("NIMG_ROUTER_I8_STATS");
+    return v && v[0] == '1';
+  }();
+  static const bool nofix = [] {   // debugging only: leave flagged tokens as they are
+    const char* v = getenv("NIMG_ROUTER_I8_NOFIX");
+    return v && v[0] == '1';
+  }();
+  {
+    if (stats) {
       unsigned cnt = 0;
       int bf[ri8::NE];
       cudaMemcpyAsync(&cnt, ws.counter, 4, cudaMemcpyDeviceToHost, s);
@@ -698,8 +706,7 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
       fprintf(stderr, "[router_i8] T=%lld flagged=%u all_fallback=%d\n", (long long)T, cnt, all);
     }
   }
-  const char* nofix = getenv("NIMG_ROUTER_I8_NOFIX");   // debugging only: leave flagged tokens
-  if (nofix && nofix[0] == '1') return cudaSuccess;
+  if (nofix) return cudaSuccess;
   return launch_pdl(ri8::router_fix_i8_kernel, dim3(148), dim3(ri8::FIX_THREADS), 0, s, x, w_r, (const double*)part,
                     ws, logits, scores_bes, B, S, d);
 }
