@@ -430,3 +430,22 @@ def test_block_full_width_bf16():
     want = hh[:1].astype(f64) + np.tanh(inp["ff_gate"][:1].astype(f64))[:, None, :] * moe
     err = rel_fro(np_of(out[:1]), want)
     assert err <= TOL_BF16, f"block bf16 rel-err {err:.3e}"
+
+
+@pytest.mark.parametrize("B,S,d,E,h,C", [(1, 40, 256, 8, 128, 1.0), (3, 56, 512, 8, 192, 2.0)])
+def test_ragged_routed_rows_tcgen05(B, S, d, E, h, C):
+    """tcgen05 shapes whose routed row count is not a multiple of the 32-row
+    background-gather sub-block or the 256-row pair tile (40 = 8 x 5 rows;
+    336 = 8 x 3 x 14): the gather inside GEMM1 and its flags at the edges."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    inp = make_layer_inputs(61, B, S, d, E, h, mode="bf16")
+    g = to_gpu(inp, "bf16")
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    out, _, routing = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg, bank_of(g),
+                                    g["w_r"], return_routing=True)
+    ref_out, ref = O.moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"], inp["w1"],
+                                 inp["w3"], inp["w2"], inp["sw1"], inp["sw3"], inp["sw2"],
+                                 capacity_factor=C, return_routing=True)
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), ref["token_flat"])
+    assert rel_fro(np_of(out), ref_out) <= TOL_BF16
