@@ -17,8 +17,8 @@
 // order (tcgen05.mma kind::i8: per K step, digit i x [W_0|W_1|W_2|W_3] (N = 256)
 // lands on TMEM groups i..i+3 and digit i x W_4 (N = 64) on group i+4).
 // Elements outside the fixed-point windows are not lost: a W element below
-// 2^-11 of its column max becomes an exact f64 correction term (a short
-// per-expert list), and an x element outside its row's XW-binade window (the
+// 2^-11 of its column max becomes an exact f64 correction term (a per-expert
+// list of up to CORR_MAX, ascending k), and an x element outside its row's XW-binade window (the
 // scale is guessed from the row's first 128 elements, XH binades of headroom)
 // becomes an exact f64 term in a per-row list; a row whose list overflows is
 // recomputed by the f64 fix-up kernel. The epilogue forms v = H 2^28 + L
@@ -31,10 +31,11 @@
 //
 // Kernels: router_prep_i8 (t-half partials, W digit image in the UMMA smem
 // layout, correction lists, counter reset), router_scores_i8 (one CTA per 128
-// tokens: converter warps write the x digits into 128-B swizzled smem, a bulk
-// copy brings the W digits, one thread issues the MMAs, the same converter
-// warps run the epilogue and the numpy-order softmax), router_fix_i8 (flagged
-// tokens, f64).
+// tokens, 18 warps: 16 converter warps write the x digits into 128-B swizzled
+// smem, a producer warp bulk-copies the W digits, one thread issues the MMAs,
+// and the 16 converter warps then run the epilogue and the numpy-order f64
+// softmax), router_fix_i8 (flagged tokens, f64). At cfg2 (T = 16384): 8.8 +
+// 68 + 3.5 us against 174 us for the FP64 DMMA router (profiles/r01b_*).
 #include <cstdio>
 #include <cstring>
 
