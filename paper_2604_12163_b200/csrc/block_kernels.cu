@@ -101,6 +101,66 @@ block_prologue_bf16_kernel(const bf16* __restrict__ x, const bf16* __restrict__ 
   }
 }
 
+// bf16, block per token: thread c owns the 8 elements [8c, 8c+8) (d / 8
+// threads, d <= 8192); the sum of squares is reduced lane-sequentially, over
+// the warp (xor tree) and over the warps in index order. No 64-float row in
+// registers, so many tokens are in flight per SM (the warp-per-token kernel
+// above keeps a whole row per warp).
+__global__ void block_prologue_bf16_blk_kernel(const bf16* __restrict__ x, const bf16* __restrict__ r_attn,
+                                               const float* __restrict__ th_sa, const float* __restrict__ onep,
+                                               bf16* __restrict__ h_out, bf16* __restrict__ xn_out,
+                                               bf16* __restrict__ xm_out, int S, int d, float scale_t) {
+  pdl_trigger();
+  pdl_wait();
+  __shared__ float red[32];
+  const int64_t t = blockIdx.x;
+  const int c = threadIdx.x, lane = c & 31, warp = c >> 5, nw = blockDim.x >> 5;
+  const int64_t b = t / S;
+  const int64_t o = t * d + (int64_t)c * 8;
+  const uint4 xv = __ldg(reinterpret_cast<const uint4*>(x + o));
+  const uint4 rv = __ldg(reinterpret_cast<const uint4*>(r_attn + o));
+  float g[8], o1[8];
+  *reinterpret_cast<float4*>(g) = __ldg(reinterpret_cast<const float4*>(th_sa + b * d + c * 8));
+  *reinterpret_cast<float4*>(g + 4) = __ldg(reinterpret_cast<const float4*>(th_sa + b * d + c * 8) + 1);
+  *reinterpret_cast<float4*>(o1) = __ldg(reinterpret_cast<const float4*>(onep + b * d + c * 8));
+  *reinterpret_cast<float4*>(o1 + 4) = __ldg(reinterpret_cast<const float4*>(onep + b * d + c * 8) + 1);
+  const bf16* xe = reinterpret_cast<const bf16*>(&xv);
+  const bf16* re = reinterpret_cast<const bf16*>(&rv);
+  bf16 hv[8];
+  float hf[8], ss = 0.f;
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    hv[v] = __float2bfloat16_rn(__fadd_rn(__bfloat162float(xe[v]), __fmul_rn(g[v], __bfloat162float(re[v]))));
+    hf[v] = __bfloat162float(hv[v]);
+    ss = fmaf(hf[v], hf[v], ss);
+  }
+  *reinterpret_cast<uint4*>(h_out + o) = *reinterpret_cast<const uint4*>(hv);
+#pragma unroll
+  for (int k = 16; k > 0; k >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, k);
+  if (lane == 0) red[warp] = ss;
+  __syncthreads();
+  float tot = red[0];
+  for (int w = 1; w < nw; ++w) tot += red[w];
+  const float inv = rsqrtf(tot / (float)d + 1e-6f);
+  bf16 xn[8], xm[8];
+#pragma unroll
+  for (int v = 0; v < 8; ++v) {
+    const float xn0 = __bfloat162float(__float2bfloat16_rn(hf[v] * inv));
+    xn[v] = __float2bfloat16_rn(xn0 * scale_t);
+    xm[v] = __float2bfloat16_rn(__bfloat162float(xn[v]) * o1[v]);
+  }
+  *reinterpret_cast<uint4*>(xn_out + o) = *reinterpret_cast<const uint4*>(xn);
+  *reinterpret_cast<uint4*>(xm_out + o) = *reinterpret_cast<const uint4*>(xm);
+}
+
+static bool bp_block() {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_BP_BLOCK");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 constexpr int BP_WARPS = 4;
 
 // squares staged per warp in leaf-padded smem: leaf l (128 elements) at
@@ -216,6 +276,10 @@ cudaError_t launch_block_prologue(bool bf, const void* x, const void* r_attn, co
                                   const float* th_sa_f, const float* onep, void* h, void* xn,
                                   void* xm, int64_t T, int S, int d, float scale_t, cudaStream_t s) {
   if (T <= 0) return cudaSuccess;
+  if (bf && bp_block() && d % 256 == 0 && d <= 8192)
+    return launch_pdl(block_prologue_bf16_blk_kernel, dim3((unsigned)T), dim3(d / 8), 0, s,
+                      (const bf16*)x, (const bf16*)r_attn, th_sa_f, onep, (bf16*)h, (bf16*)xn,
+                      (bf16*)xm, S, d, scale_t);
   if (bf && d % 256 == 0 && d <= 2048) {
     return launch_pdl(block_prologue_bf16_kernel, dim3((unsigned)((T + BPF_WARPS - 1) / BPF_WARPS)),
                       dim3(BPF_WARPS * 32), 0, s, (const bf16*)x, (const bf16*)r_attn, th_sa_f, onep,
