@@ -150,58 +150,79 @@ def make_inputs(c, dev, B=None):
 
 
 # ----------------------------------------------------------------- CPU baselines
-def cpu_layer_sample(c, budget_s: float, max_samples: int):
-    """Time the oracle port of the reference's moe_forward (moe.py:138-164)
-    one sample at a time (routing is per sample, router.py:127) on host cores."""
+REF_INSTALL = os.path.join(ROOT, "baseline", "_ref")
+
+
+def cpu_reference_step(c, B=None):
+    """(kind, step, tokens_per_step): one forward of the reference's CPU MoE
+    layer (moe.py:138-164) over the workload's whole batch, on the host cores.
+
+    kind "reference": the UNMODIFIED reference, imported from its offline pip
+    install under baseline/_ref, through its own public API (nimg.moe.
+    moe_forward on nimg Tensors, fp32 storage / f64 compute, under no_grad).
+    kind "port": the oracle restatement of the same function (oracle/), used
+    only when that install is absent. Inputs: the GPU arm's seeded bf16 values,
+    upcast to fp32 (the reference has no bf16)."""
     import numpy as np
     import torch
-    from oracle import nimg_oracle as O
-    inp = make_inputs(c, "cuda" if torch.cuda.is_available() else "cpu", B=max_samples)
-    a = {k: v.float().cpu().numpy() for k, v in inp.items()}
+    B = c["B"] if B is None else B
+    inp = make_inputs(c, "cuda" if torch.cuda.is_available() else "cpu", B=B)
+    a = {k: np.ascontiguousarray(v.float().cpu().numpy()) for k, v in inp.items()}
     del inp
-    times, tokens = [], 0
-    t_all = time.perf_counter()
-    for b in range(max_samples):
-        t0 = time.perf_counter()
-        O.moe_forward(a["x_norm"][b:b + 1], a["x_mod"][b:b + 1], a["t_emb"][b:b + 1], a["w_r"],
-                      a["w1"], a["w3"], a["w2"], a["sw1"], a["sw3"], a["sw2"],
-                      capacity_factor=c["C"])
-        times.append(time.perf_counter() - t0)
-        tokens += c["S"]
-        if time.perf_counter() - t_all > budget_s:
-            break
-    return tokens / sum(times), len(times), times
+    if os.path.isdir(os.path.join(REF_INSTALL, "nimg")):
+        if REF_INSTALL not in sys.path:
+            sys.path.insert(0, REF_INSTALL)
+        import nimg.moe as rm
+        import nimg.router as rr
+        import nimg.tensor as nt
+        T = lambda x: nt.Tensor(x, dtype=np.float32)      # no copy: already fp32 + contiguous
+        args = (T(a["x_mod"]), T(a["x_norm"]), T(a["x_mod"]), T(a["t_emb"]),
+                rr.RouterConfig(d_model=c["d"], n_experts=c["E"], capacity_factor=c["C"]),
+                rm.ExpertBank(*(T(a[k]) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2"))),
+                T(a["w_r"]))
+
+        def step():
+            with nt.no_grad():
+                rm.moe_forward(*args)
+        return "reference", step, B * c["S"]
+    from oracle import nimg_oracle as O
+
+    def step():
+        O.moe_forward(a["x_norm"], a["x_mod"], a["t_emb"], a["w_r"], a["w1"], a["w3"], a["w2"],
+                      a["sw1"], a["sw3"], a["sw2"], capacity_factor=c["C"])
+    return "port", step, B * c["S"]
+
+
+def _ref_sample(kind, c):
+    who = ("the reference's own nimg.moe.moe_forward (baseline/_ref install, fp32 Tensors, "
+           "f64 compute, no_grad)" if kind == "reference" else
+           "the oracle port of moe_forward (f64 compute)")
+    return (f"the full {c['name']} batch (B={c['B']} x S={c['S']} tokens) per step through {who}; "
+            f"numpy/OpenBLAS on all host threads")
 
 
 def run_reference_arm(args, c):
-    """--impl reference: the reference's CPU MoE path (oracle port; the
-    reference is pure Python and cannot be compiled) on all host threads."""
+    """--impl reference: the reference's CPU MoE layer on all host threads, on
+    the same config as our arm (whole batch per step). Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
-    import torch
-    from oracle import nimg_oracle as O
     cores = os.cpu_count()
-    inp = make_inputs(c, "cuda" if torch.cuda.is_available() else "cpu", B=1)
-    a = {k: v.float().cpu().numpy() for k, v in inp.items()}
-    step = lambda: O.moe_forward(a["x_norm"], a["x_mod"], a["t_emb"], a["w_r"], a["w1"], a["w3"],
-                                 a["w2"], a["sw1"], a["sw3"], a["sw2"], capacity_factor=c["C"])
+    kind, step, tokens = cpu_reference_step(c)
     for _ in range(args.warmup):
         step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step()
     dt = time.perf_counter() - t0
-    val = args.steps * c["S"] / dt
-    sample = f"1 sample (S={c['S']} tokens) of {c['name']} per step, fp32 oracle port (f64 compute)"
+    val = args.steps * tokens / dt
     line = {"metric": METRIC, "value": val, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": workload_name(c), "l2": "n/a (CPU)"},
-            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": "port",
-                             "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "tokens/s", "cores": cores, "kind": kind,
+                             "sample": _ref_sample(kind, c)},
             "e2e": {"value": val, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -299,13 +320,15 @@ def run_single(args, c, peaks, peak_kind):
     # ---- e2e through the public API with host buffers
     e2e = run_e2e(args, c, inp, cfg, bank)
 
-    # ---- CPU baseline (oracle port), bounded sample
+    # ---- CPU baseline: one whole-batch step of the reference's CPU layer
     cpu = None
     if not args.no_cpu_baseline:
-        val, n, _ = cpu_layer_sample(c, budget_s=args.cpu_budget, max_samples=4)
-        cpu = {"value": val, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{n} sample(s) x S={c['S']} tokens of {c['name']} through the oracle "
-                         f"port of moe_forward (f64 compute, OpenBLAS threads = all cores)"}
+        kind, cstep, tokens = cpu_reference_step(c)
+        t0 = time.perf_counter()
+        cstep()
+        val = tokens / (time.perf_counter() - t0)
+        cpu = {"value": val, "unit": "tokens/s", "cores": os.cpu_count(), "kind": kind,
+               "sample": "1 step: " + _ref_sample(kind, c)}
 
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": 1, "steps": args.steps,
@@ -824,7 +847,6 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the training-step leg")
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-overlap", action="store_true", help="EP: plain all-to-alls")
     ap.add_argument("--ep-transport", default="ce", choices=["ce", "nccl"],
                     help="EP exchange: copy engines over NVLink (default) or NCCL")
@@ -834,7 +856,19 @@ def main():
                     help="ncu dram bytes per GEMM1 launch, if captured")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` outside torchrun: relaunch as N ranks (one per GPU)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+               "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.config == "cfg5":
         if args.impl == "reference":
             if int(os.environ.get("RANK", "0")) == 0:

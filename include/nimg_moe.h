@@ -18,8 +18,16 @@
  *    thread-local message. Codes map to the reference's exceptions:
  *    NIMG_ERR_SHAPE -> nimg.tensor.ShapeError (tensor.py:19-20),
  *    NIMG_ERR_CONFIG -> nimg.router.ConfigError (router.py:22-23).
- *  - dtypes: NIMG_F32 = float32, NIMG_BF16 = bfloat16. The router weight and
- *    the timestep embedding are always float32 (routing stays bit-exact).
+ *  - dtypes: NIMG_F32 = float32, NIMG_BF16 = bfloat16, NIMG_F64 = float64.
+ *    In the fp32 / bf16 modes the router weight, the timestep embedding and
+ *    every routing output are float32 (routing stays bit-exact with the
+ *    reference's fp32 mode). NIMG_F64 is the reference's float64 storage mode
+ *    (tensor.py:39-47; the backbone runs its MoE on f64 inputs,
+ *    backbone.py:259-261): every input, weight, routing output and the layer
+ *    output are float64, and no intermediate is rounded to fp32.
+ *  - ABI version 2 (nimg_abi_version): nimg_moe_desc.router_dtype replaced the
+ *    v1 `reserved` field and the f64 gate parameters were appended; routing
+ *    value pointers became void* (their element type follows act_dtype).
  */
 #ifndef NIMG_MOE_H_
 #define NIMG_MOE_H_
@@ -38,6 +46,7 @@ extern "C" {
 
 #define NIMG_F32 0
 #define NIMG_BF16 1
+#define NIMG_F64 2
 
 #define NIMG_PATH_TCGEN05 0 /* bf16 tcgen05/TMEM/TMA grouped GEMM */
 #define NIMG_PATH_SIMT 1    /* fp32-accumulate CUDA-core grouped GEMM */
@@ -48,27 +57,34 @@ typedef struct nimg_moe_desc {
   int64_t B, S, d, E, cap, h, h_shared;
   float gate_scale; /* RouterConfig.gate_scale (alpha) */
   float gate_eps;   /* RouterConfig.gate_eps */
-  int32_t act_dtype; /* x_norm, x_mod, expert weights and out */
-  int32_t reserved;
+  int32_t act_dtype;    /* x_mod, expert weights and out */
+  int32_t router_dtype; /* x_norm (the router input). NIMG_F32 or NIMG_BF16 in the
+                           fp32 / bf16 modes -- routing is computed on x_norm's own
+                           values, as the reference does (router.py:120-122) --
+                           and NIMG_F64 iff act_dtype is NIMG_F64. The training
+                           entry points require router_dtype == act_dtype. */
+  double gate_scale_f64; /* RouterConfig.gate_scale / gate_eps as Python floats: */
+  double gate_eps_f64;   /* used (unrounded) in the NIMG_F64 mode             */
 } nimg_moe_desc;
 
 /* Routing results (router.py:104-162). Expert-major flat order (e, b, slot)
  * of length E*B*cap, as the reference's routing["token_flat"]. */
+/* "fp32" below is float64 in the NIMG_F64 mode. */
 typedef struct nimg_route_out {
-  float* logits;       /* (B,S,E) fp32        routing["logits"]              */
-  float* scores_bes;   /* (B,E,S) fp32        softmax scores, expert-major   */
+  void* logits;        /* (B,S,E) fp32        routing["logits"]              */
+  void* scores_bes;    /* (B,E,S) fp32        softmax scores, expert-major   */
   int32_t* token_flat; /* (E*B*cap) int32     routing["token_flat"]          */
-  float* gate_raw;     /* (E*B*cap) fp32      RouterDecision.affinity         */
-  float* gates;        /* (E*B*cap) fp32      routing["gates"]               */
+  void* gate_raw;      /* (E*B*cap) fp32      RouterDecision.affinity         */
+  void* gates;         /* (E*B*cap) fp32      routing["gates"]               */
   int32_t* comb_rows;  /* (B*S,E) int32       per token: routed rows, expert-ascending */
   int32_t* comb_cnt;   /* (B*S) int32         number of experts that picked the token */
 } nimg_route_out;
 
 typedef struct nimg_moe_ptrs {
-  const void* x_norm; /* (B,S,d) act: router input (unmodulated)  */
+  const void* x_norm; /* (B,S,d) router_dtype: router input (unmodulated) */
   const void* x_mod;  /* (B,S,d) act: expert input (modulated)     */
-  const float* t_emb; /* (B,d)   fp32                               */
-  const float* w_r;   /* (2d,E)  fp32                               */
+  const void* t_emb;  /* (B,d)   fp32 (f64 in the NIMG_F64 mode)    */
+  const void* w_r;    /* (2d,E)  fp32 (f64 in the NIMG_F64 mode)    */
   const void *w1, *w3, *w2;    /* (E,h,d), (E,h,d), (E,d,h) act     */
   const void *sw1, *sw3, *sw2; /* (hs,d), (hs,d), (d,hs) act        */
   void* out;          /* (B,S,d) act                                */
@@ -170,8 +186,8 @@ int nimg_moe_block_forward(const nimg_moe_desc* desc, const nimg_block_ptrs* ptr
 int nimg_route_workspace_bytes(const nimg_moe_desc* desc, size_t* bytes);
 /* router.py:104-162  route_full (logits, softmax, per-(b,e) top-cap,
  * expert-major token_flat, renormalised gates) + combine tables. */
-int nimg_route(const nimg_moe_desc* desc, const void* x_norm, const float* t_emb,
-               const float* w_r, const nimg_route_out* out, void* ws, size_t ws_bytes,
+int nimg_route(const nimg_moe_desc* desc, const void* x_norm, const void* t_emb,
+               const void* w_r, const nimg_route_out* out, void* ws, size_t ws_bytes,
                void* stream);
 
 /* tensor.py:348-363  gather_rows: dst[i,:] = src[idx[i],:] (row_bytes each) */
@@ -198,7 +214,7 @@ int nimg_expert_ffn(const nimg_ffn_desc* desc, const int64_t* seg_offsets,
  * fp32(y_routed[rows_k] * gates[rows_k]))) + f64(y_shared[t])), experts in
  * ascending order (deterministic; same bits for any expert-parallel split). */
 int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_dtype,
-                 const void* y_routed, const void* y_shared, const float* gates,
+                 const void* y_routed, const void* y_shared, const void* gates,
                  const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream);
 
 /* backbone.py:584-589 alone (the expert-parallel block runs the layer between

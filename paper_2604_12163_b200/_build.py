@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnimg_moe.so")
 SOURCES = ["capi.cu", "route_kernels.cu", "grouped_gemm_sm100.cu", "grouped_gemm_simt.cu",
            "block_kernels.cu", "stack_kernels.cu", "backward_kernels.cu",
-           "grouped_gemm_bwd_sm100.cu", "router_i8.cu"]
+           "grouped_gemm_bwd_sm100.cu", "router_i8.cu", "f64_kernels.cu"]
 HEADERS = ["common.cuh", "nimg_internal.h", os.path.join("..", "..", "include", "nimg_moe.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -58,8 +58,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
                 sys.stderr.write(r.stderr)
             objs.append(obj)
     tmp = lib + ".tmp"
+    # --no-undefined: an unresolved internal symbol fails the build, not the dlopen
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-           "-cudart", "static"]
+           "-cudart", "static", "-Xlinker", "--no-undefined"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

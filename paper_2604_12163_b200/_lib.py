@@ -16,7 +16,8 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libnimg_moe
 LIB_PATH = os.environ.get("NIMG_LIB_PATH", LIB_PATH)
 
 NIMG_OK, NIMG_ERR_SHAPE, NIMG_ERR_CONFIG, NIMG_ERR_CUDA = 0, 1, 2, 3
-NIMG_F32, NIMG_BF16 = 0, 1
+NIMG_F32, NIMG_BF16, NIMG_F64 = 0, 1, 2
+ABI_VERSION = 2
 NIMG_PATH_TCGEN05, NIMG_PATH_SIMT = 0, 1
 
 # Every entry point the header declares (checked by tests/test_abi.py).
@@ -38,7 +39,8 @@ class MoeDesc(C.Structure):
     _fields_ = [("B", C.c_int64), ("S", C.c_int64), ("d", C.c_int64), ("E", C.c_int64),
                 ("cap", C.c_int64), ("h", C.c_int64), ("h_shared", C.c_int64),
                 ("gate_scale", C.c_float), ("gate_eps", C.c_float),
-                ("act_dtype", C.c_int32), ("reserved", C.c_int32)]
+                ("act_dtype", C.c_int32), ("router_dtype", C.c_int32),
+                ("gate_scale_f64", C.c_double), ("gate_eps_f64", C.c_double)]
 
 
 class RouteOut(C.Structure):
@@ -129,6 +131,9 @@ def _load():
     for name in EXPORTS:
         fn = getattr(lib, name)
         fn.argtypes, fn.restype = sig[name]
+    if lib.nimg_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH} has ABI {lib.nimg_abi_version()}, this binding needs "
+                          f"{ABI_VERSION}: rebuild with `python -m paper_2604_12163_b200._build`")
     return lib
 
 

@@ -9,7 +9,9 @@ import torch
 
 from .errors import ConfigError
 
-KERNEL_DTYPES = (torch.float32, torch.bfloat16)
+# float64 is the reference's f64 storage mode (tensor.py:39-47), computed in
+# f64 end to end (csrc/f64_kernels.cu) -- never silently downcast.
+KERNEL_DTYPES = (torch.float32, torch.bfloat16, torch.float64)
 
 
 def device() -> torch.device:
@@ -21,15 +23,13 @@ def device() -> torch.device:
 
 def to_device(x, dtype: torch.dtype | None = None) -> torch.Tensor:
     """torch.Tensor, numpy array or reference Tensor (has a numpy `.data`)
-    -> contiguous CUDA tensor. float64 becomes float32 unless `dtype` says
-    otherwise (the kernels compute in fp32/bf16 with f64 only where the
-    reference's rounding chain needs it)."""
+    -> contiguous CUDA tensor of `dtype` (default: its own dtype)."""
     if not isinstance(x, torch.Tensor):
         arr = x.data if (hasattr(x, "data") and isinstance(getattr(x, "data"), np.ndarray)) else x
         x = torch.from_numpy(np.ascontiguousarray(np.asarray(arr)))
     dev = device()
     if dtype is None:
-        dtype = torch.float32 if x.dtype == torch.float64 else x.dtype
+        dtype = x.dtype
     if dtype not in KERNEL_DTYPES and dtype not in (torch.int64, torch.int32):
         raise ConfigError(f"unsupported dtype {x.dtype}")
     if x.device != dev or x.dtype != dtype:
@@ -38,12 +38,31 @@ def to_device(x, dtype: torch.dtype | None = None) -> torch.Tensor:
 
 
 def nimg_dtype(dt: torch.dtype) -> int:
-    from ._lib import NIMG_BF16, NIMG_F32
+    from ._lib import NIMG_BF16, NIMG_F32, NIMG_F64
     if dt == torch.bfloat16:
         return NIMG_BF16
     if dt == torch.float32:
         return NIMG_F32
+    if dt == torch.float64:
+        return NIMG_F64
     raise ConfigError(f"unsupported activation dtype {dt}")
+
+
+def dtype_of(x) -> torch.dtype | None:
+    """torch dtype of a torch tensor, numpy array or reference Tensor (None if
+    it has no dtype)."""
+    if isinstance(x, torch.Tensor):
+        return x.dtype
+    arr = x.data if (hasattr(x, "data") and isinstance(getattr(x, "data"), np.ndarray)) else x
+    if isinstance(arr, np.ndarray):
+        return torch.from_numpy(np.empty(0, dtype=arr.dtype)).dtype
+    return None
+
+
+def any_f64(*xs) -> bool:
+    """The reference promotes an op to f64 when any operand is f64
+    (np.result_type, tensor.py:203-204)."""
+    return any(dtype_of(x) == torch.float64 for x in xs if x is not None)
 
 
 def ptr(t: torch.Tensor | None) -> int | None:

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 
@@ -29,6 +30,24 @@ thread_local int g_nevents = 0;
 inline void mark(int i, cudaStream_t st) {
   if (i < g_nevents && g_events[i]) cudaEventRecord(g_events[i], st);
 }
+
+}  // namespace
+
+cudaError_t nimg::set_max_dyn_smem(const void* kernel, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;   // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  int& have = done[{kernel, dev}];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
+namespace {
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -55,7 +74,7 @@ int fail(int code, const char* fmt, ...) {
 
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
-inline size_t elt(int32_t dt) { return dt == NIMG_BF16 ? 2 : 4; }
+inline size_t elt(int32_t dt) { return dt == NIMG_BF16 ? 2 : (dt == NIMG_F64 ? 8 : 4); }
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // ------------------------------------------------------------- tensor maps
@@ -143,8 +162,14 @@ int device_sms(int* out) {
 // ------------------------------------------------------------- validation
 int check_moe_desc(const nimg_moe_desc* d) {
   if (!d) return fail(NIMG_ERR_CONFIG, "null descriptor");
-  if (d->act_dtype != NIMG_F32 && d->act_dtype != NIMG_BF16)
+  if (d->act_dtype != NIMG_F32 && d->act_dtype != NIMG_BF16 && d->act_dtype != NIMG_F64)
     return fail(NIMG_ERR_CONFIG, "unsupported act_dtype %d", d->act_dtype);
+  if (d->act_dtype == NIMG_F64 ? d->router_dtype != NIMG_F64
+                               : (d->router_dtype != NIMG_F32 && d->router_dtype != NIMG_BF16))
+    return fail(NIMG_ERR_CONFIG, "router_dtype %d incompatible with act_dtype %d", d->router_dtype,
+                d->act_dtype);
+  if (d->act_dtype == NIMG_F64 && !(d->gate_eps_f64 > 0.0))
+    return fail(NIMG_ERR_CONFIG, "gate_eps must be > 0");
   if (d->B < 1 || d->S < 1 || d->d < 1 || d->h < 1 || d->h_shared < 1)
     return fail(NIMG_ERR_SHAPE, "empty dimension B=%lld S=%lld d=%lld h=%lld hs=%lld",
                 (long long)d->B, (long long)d->S, (long long)d->d, (long long)d->h,
@@ -174,7 +199,8 @@ struct RouteWs {
   void* i8;        // INT8 router scratch (router_i8.cu)
   int* bg_flags;   // GEMM1 background-gather flags, one per 32 routed rows
 };
-int64_t bg_flag_count(const nimg_moe_desc* d) { return (d->E * d->B * d->cap + 31) / 32; }
+// one flag per 32 routed rows, plus the sub-block claim counter (flags[nsub])
+int64_t bg_flag_count(const nimg_moe_desc* d) { return (d->E * d->B * d->cap + 31) / 32 + 1; }
 size_t slot_bytes(const nimg_moe_desc* d) { return (size_t)d->E * d->B * d->S * 2; }
 size_t route_ws_bytes(const nimg_moe_desc* d) {
   return align_up((size_t)d->B * d->E * 8) +
@@ -209,7 +235,7 @@ bool ffn_use_tc(const nimg_ffn_desc* f) {
   return true;
 }
 size_t ffn_ws_bytes(const nimg_ffn_desc* f) {
-  const size_t e = ffn_use_tc(f) ? 2 : 4;
+  const size_t e = ffn_use_tc(f) ? 2 : (f->act_dtype == NIMG_F64 ? 8 : 4);
   return align_up((size_t)f->n_rows * f->h * e) + align_up((size_t)f->n_shared_rows * f->h_shared * e);
 }
 
@@ -246,7 +272,7 @@ int fill_segments(P& p, const nimg_ffn_desc* f, const int64_t* off, const int32_
 
 int check_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex) {
   if (!f) return fail(NIMG_ERR_CONFIG, "null descriptor");
-  if (f->act_dtype != NIMG_F32 && f->act_dtype != NIMG_BF16)
+  if (f->act_dtype != NIMG_F32 && f->act_dtype != NIMG_BF16 && f->act_dtype != NIMG_F64)
     return fail(NIMG_ERR_CONFIG, "unsupported act_dtype %d", f->act_dtype);
   if (f->nseg < 0 || f->nseg > kMaxSeg - 8)
     return fail(NIMG_ERR_CONFIG, "nseg %d outside [0, %d]", f->nseg, kMaxSeg - 8);
@@ -307,7 +333,9 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
   if ((has_r && (!xr || !w1 || !w3 || !w2 || !yr)) || (has_s && (!xs || !sw1 || !sw3 || !sw2 || !ys)))
     return fail(NIMG_ERR_SHAPE, "null tensor pointer");
   const bool tc = ffn_use_tc(f) && !(tr && tr->force_simt);
-  const size_t e = tc ? 2 : 4;
+  const bool f64 = f->act_dtype == NIMG_F64;
+  if (f64 && (tr || gather_idx || bg)) return fail(NIMG_ERR_CONFIG, "internal: f64 mode is forward-only");
+  const size_t e = tc ? 2 : (f64 ? 8 : 4);
   uint8_t* pre_r = static_cast<uint8_t*>(ws);
   uint8_t* pre_s = pre_r + align_up((size_t)f->n_rows * f->h * e);
   if (tr) {
@@ -385,7 +413,7 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
     return NIMG_OK;
   }
 
-  // SIMT path: fp32 pre / y
+  // SIMT path: fp32 pre / y (f64 in the f64 storage mode)
   if (gather_idx) return fail(NIMG_ERR_CONFIG, "internal: fused gather needs the tcgen05 path");
   const bool bf = f->act_dtype == NIMG_BF16;
   const int bm = simt_bm(), bn = simt_bn();
@@ -393,48 +421,64 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
     SimtParams p;
     memset(&p, 0, sizeof(p));
     NIMG_TRY(fill_segments(p, f, off, ex, bm, (h + bn - 1) / bn, (hs + bn - 1) / bn));
-    p.bank[0] = SimtBank{xr, d, w1, w3, reinterpret_cast<float*>(pre_r), h, d, h, (h + bn - 1) / bn, 0,
-                         static_cast<float*>(h_r)};
-    p.bank[1] = SimtBank{xs, d, sw1, sw3, reinterpret_cast<float*>(pre_s), hs, d, hs, (hs + bn - 1) / bn, 0,
-                         static_cast<float*>(h_s)};
-    CUDA_TRY(launch_grouped_simt(0, bf, p, st));
+    p.bank[0] = SimtBank{xr, d, w1, w3, pre_r, h, d, h, (h + bn - 1) / bn, 0, static_cast<float*>(h_r)};
+    p.bank[1] = SimtBank{xs, d, sw1, sw3, pre_s, hs, d, hs, (hs + bn - 1) / bn, 0, static_cast<float*>(h_s)};
+    CUDA_TRY(launch_grouped_simt(0, bf, p, st, f64));
     mark(3, st);
   }
   {
     SimtParams p;
     memset(&p, 0, sizeof(p));
     NIMG_TRY(fill_segments(p, f, off, ex, bm, (d + bn - 1) / bn, (d + bn - 1) / bn));
-    p.bank[0] = SimtBank{pre_r, h, w2, nullptr, reinterpret_cast<float*>(yr), d, h, d, (d + bn - 1) / bn, 0};
-    p.bank[1] = SimtBank{pre_s, hs, sw2, nullptr, reinterpret_cast<float*>(ys), d, hs, d, (d + bn - 1) / bn, 0};
-    CUDA_TRY(launch_grouped_simt(1, bf, p, st));
+    p.bank[0] = SimtBank{pre_r, h, w2, nullptr, yr, d, h, d, (d + bn - 1) / bn, 0};
+    p.bank[1] = SimtBank{pre_s, hs, sw2, nullptr, ys, d, hs, d, (d + bn - 1) / bn, 0};
+    CUDA_TRY(launch_grouped_simt(1, bf, p, st, f64));
   }
   return NIMG_OK;
 }
 
-int route_impl(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, const float* w_r,
+int route_impl(const nimg_moe_desc* d, const void* x_norm, const void* t_emb_v, const void* w_r_v,
                const nimg_route_out* o, void* ws, size_t ws_bytes, cudaStream_t st) {
   NIMG_TRY(check_moe_desc(d));
   if (!o || !o->logits || !o->scores_bes || !o->token_flat || !o->gate_raw || !o->gates ||
       !o->comb_rows || !o->comb_cnt)
     return fail(NIMG_ERR_SHAPE, "null routing output pointer");
-  if (!x_norm || !t_emb || !w_r) return fail(NIMG_ERR_SHAPE, "null input pointer");
+  if (!x_norm || !t_emb_v || !w_r_v) return fail(NIMG_ERR_SHAPE, "null input pointer");
   if (!ws || ws_bytes < route_ws_bytes(d)) return fail(NIMG_ERR_CONFIG, "workspace too small");
   const int B = (int)d->B, S = (int)d->S, dd = (int)d->d, E = (int)d->E, cap = (int)d->cap;
   RouteWs w = carve_route(d, ws);
+  if (d->act_dtype == NIMG_F64) {   // f64 storage mode: every routing value in f64
+    CUDA_TRY(launch_route_f64(static_cast<const double*>(x_norm), static_cast<const double*>(t_emb_v),
+                              static_cast<const double*>(w_r_v), static_cast<double*>(o->logits),
+                              static_cast<double*>(o->scores_bes), o->token_flat,
+                              static_cast<double*>(o->gate_raw), static_cast<double*>(o->gates),
+                              o->comb_rows, o->comb_cnt, w.slot_of, B, S, dd, E, cap, d->gate_eps_f64,
+                              d->gate_scale_f64, st));
+    mark(6, st);
+    return NIMG_OK;
+  }
+  const float* t_emb = static_cast<const float*>(t_emb_v);
+  const float* w_r = static_cast<const float*>(w_r_v);
+  float* logits = static_cast<float*>(o->logits);
+  float* scores_bes = static_cast<float*>(o->scores_bes);
+  // the router reads x_norm in its own dtype (router.py:120-122 routes on the
+  // caller's x_norm values, whatever x_mod's dtype)
+  const bool xn_bf16 = d->router_dtype == NIMG_BF16;
   // ec_select writes the whole slot table; only the DFMA router (E > 64) needs
   // its per-sample completion counters armed (0xFFFFFFFF; the workspace is
   // caller-owned).
   if (!router_uses_dmma(E))
     CUDA_TRY(cudaMemsetAsync(w.counters, 0xFF, (size_t)B * 4, st));
-  if (router_i8_eligible(d->act_dtype == NIMG_BF16, dd, E, x_norm))
-    CUDA_TRY(launch_router_i8(x_norm, t_emb, w_r, w.part, w.i8, o->logits, o->scores_bes, B, S, dd, st));
+  if (router_i8_eligible(xn_bf16, dd, E, x_norm))
+    CUDA_TRY(launch_router_i8(x_norm, t_emb, w_r, w.part, w.i8, logits, scores_bes, B, S, dd, st));
   else
-    CUDA_TRY(launch_router(d->act_dtype == NIMG_BF16, x_norm, t_emb, w_r, w.tb, w.part, w.counters,
-                           w.wd, o->logits, o->scores_bes, B, S, dd, E, st));
+    CUDA_TRY(launch_router(xn_bf16, x_norm, t_emb, w_r, w.tb, w.part, w.counters, w.wd, logits,
+                           scores_bes, B, S, dd, E, st));
   mark(6, st);   // router scores done (inside stage 0 -> 1)
-  CUDA_TRY(launch_ec_select(o->scores_bes, o->token_flat, o->gate_raw, w.slot_of, B, S, E, cap, st));
+  CUDA_TRY(launch_ec_select(scores_bes, o->token_flat, static_cast<float*>(o->gate_raw), w.slot_of, B,
+                            S, E, cap, st));
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
-  CUDA_TRY(launch_gate_norm(o->scores_bes, w.slot_of, o->gates, o->comb_rows, o->comb_cnt, B, S,
+  CUDA_TRY(launch_gate_norm(scores_bes, w.slot_of, static_cast<float*>(o->gates), o->comb_rows, o->comb_cnt, B, S,
                             E, cap, d->gate_eps, d->gate_scale, st, w.bg_flags,
                             (int)bg_flag_count(d)));
   return NIMG_OK;
@@ -599,7 +643,7 @@ nimg_ffn_desc layer_ffn_desc(const nimg_moe_desc* d) {
 extern "C" {
 
 const char* nimg_last_error(void) { return g_err.c_str(); }
-int nimg_abi_version(void) { return 1; }
+int nimg_abi_version(void) { return 2; }
 int nimg_device_sms(int* sms) {
   if (!sms) return fail(NIMG_ERR_CONFIG, "null output");
   return device_sms(sms);
@@ -622,7 +666,7 @@ int nimg_route_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   return NIMG_OK;
 }
 
-int nimg_route(const nimg_moe_desc* d, const void* x_norm, const float* t_emb, const float* w_r,
+int nimg_route(const nimg_moe_desc* d, const void* x_norm, const void* t_emb, const void* w_r,
                const nimg_route_out* out, void* ws, size_t ws_bytes, void* stream) {
   return route_impl(d, x_norm, t_emb, w_r, out, ws, ws_bytes, (cudaStream_t)stream);
 }
@@ -640,7 +684,7 @@ int nimg_ffn_path(const nimg_ffn_desc* f, int32_t* path, int32_t* y_dtype) {
   if (!f || !path || !y_dtype) return fail(NIMG_ERR_CONFIG, "null argument");
   const bool tc = ffn_use_tc(f);
   *path = tc ? NIMG_PATH_TCGEN05 : NIMG_PATH_SIMT;
-  *y_dtype = tc ? NIMG_BF16 : NIMG_F32;
+  *y_dtype = tc ? NIMG_BF16 : (f->act_dtype == NIMG_F64 ? NIMG_F64 : NIMG_F32);
   return NIMG_OK;
 }
 
@@ -659,12 +703,21 @@ int nimg_expert_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
 }
 
 int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_dtype,
-                 const void* y_routed, const void* y_shared, const float* gates,
+                 const void* y_routed, const void* y_shared, const void* gates_v,
                  const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream) {
   if (T < 0 || d < 1 || E < 1) return fail(NIMG_ERR_SHAPE, "bad combine shape");
   if (T == 0) return NIMG_OK;
-  if (!y_shared || !comb_cnt || !comb_rows || !out || !gates)
+  if (!y_shared || !comb_cnt || !comb_rows || !out || !gates_v)
     return fail(NIMG_ERR_SHAPE, "null pointer");
+  if ((y_dtype == NIMG_F64) != (out_dtype == NIMG_F64))
+    return fail(NIMG_ERR_CONFIG, "f64 combine needs f64 y and out");
+  if (y_dtype == NIMG_F64) {
+    CUDA_TRY(launch_combine_f64(static_cast<const double*>(y_routed), static_cast<const double*>(y_shared),
+                                static_cast<const double*>(gates_v), comb_rows, comb_cnt,
+                                static_cast<double*>(out), T, (int)d, (int)E, (cudaStream_t)stream));
+    return NIMG_OK;
+  }
+  const float* gates = static_cast<const float*>(gates_v);
   CUDA_TRY(launch_combine(y_dtype == NIMG_BF16, out_dtype == NIMG_BF16, y_routed, y_shared, gates,
                           comb_rows, comb_cnt, out, T, (int)d, (int)E, (cudaStream_t)stream));
   return NIMG_OK;
@@ -795,9 +848,16 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
                            fused_gather ? p->route.token_flat : nullptr, d->B * d->S,
                            state ? &tr : nullptr, bg_gather ? &bg : nullptr));
   mark(4, st);
-  CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys, p->route.gates,
-                          p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,
-                          (int)d->E, st, resid_h, th_ff, (int)d->S));
+  if (d->act_dtype == NIMG_F64)
+    CUDA_TRY(launch_combine_f64(static_cast<const double*>(yr), static_cast<const double*>(ys),
+                                static_cast<const double*>(p->route.gates), p->route.comb_rows,
+                                p->route.comb_cnt, static_cast<double*>(p->out), d->B * d->S,
+                                (int)d->d, (int)d->E, st));
+  else
+    CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys,
+                            static_cast<const float*>(p->route.gates), p->route.comb_rows,
+                            p->route.comb_cnt, p->out, d->B * d->S, (int)d->d, (int)d->E, st,
+                            resid_h, th_ff, (int)d->S));
   mark(5, st);
   return NIMG_OK;
 }
@@ -808,8 +868,21 @@ int nimg_moe_forward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* ws, s
 }
 
 // ------------------------------------------------------------------ training
-int nimg_moe_train_state_bytes(const nimg_moe_desc* d, size_t* bytes) {
+// Training entry points: fp32 / bf16 layers whose router input has the
+// activation dtype (the router pullback reads x_norm as an operand of the same
+// GEMM path as x_mod).
+static int check_train_desc(const nimg_moe_desc* d) {
   NIMG_TRY(check_moe_desc(d));
+  if (d->act_dtype == NIMG_F64)
+    return fail(NIMG_ERR_CONFIG, "the f64 storage mode is forward-only (no training path)");
+  if (d->router_dtype != d->act_dtype)
+    return fail(NIMG_ERR_CONFIG, "training needs x_norm in the activation dtype (router_dtype %d != "
+                "act_dtype %d)", d->router_dtype, d->act_dtype);
+  return NIMG_OK;
+}
+
+int nimg_moe_train_state_bytes(const nimg_moe_desc* d, size_t* bytes) {
+  NIMG_TRY(check_train_desc(d));
   if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");
   *bytes = train_state_layout(d, nullptr).bytes;
   return NIMG_OK;
@@ -817,14 +890,14 @@ int nimg_moe_train_state_bytes(const nimg_moe_desc* d, size_t* bytes) {
 
 int nimg_moe_forward_train(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void* state,
                            size_t state_bytes, void* ws, size_t ws_bytes, void* stream) {
-  NIMG_TRY(check_moe_desc(d));
+  NIMG_TRY(check_train_desc(d));
   if (!state || state_bytes < train_state_layout(d, nullptr).bytes)
     return fail(NIMG_ERR_CONFIG, "training state too small");
   return moe_forward_impl(d, p, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr, state);
 }
 
 int nimg_moe_backward_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
-  NIMG_TRY(check_moe_desc(d));
+  NIMG_TRY(check_train_desc(d));
   if (!bytes) return fail(NIMG_ERR_CONFIG, "null output");
   *bytes = bwd_ws_layout(d, nullptr).bytes;
   return NIMG_OK;
@@ -846,7 +919,7 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
                       size_t state_bytes, const nimg_moe_grads* g, void* ws, size_t ws_bytes,
                       void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  NIMG_TRY(check_moe_desc(d));
+  NIMG_TRY(check_train_desc(d));
   if (!p || !g) return fail(NIMG_ERR_SHAPE, "null pointers");
   if (d->E + 5 > kMaxSeg) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
   const TrainState ts = train_state_layout(d, const_cast<void*>(state));
@@ -856,7 +929,15 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
   if (!g->g_out || !g->g_x_norm || !g->g_x_mod || !g->g_t_emb || !g->g_w_r || !g->g_w1 || !g->g_w3 ||
       !g->g_w2 || !g->g_sw1 || !g->g_sw3 || !g->g_sw2)
     return fail(NIMG_ERR_SHAPE, "null gradient pointer");
-  const nimg_route_out& ro = p->route;
+  const nimg_route_out& rv = p->route;
+  // training is fp32 / bf16 only (check_train_desc): routing values are fp32
+  struct {
+    const float *logits, *gates, *gate_raw;
+    const int32_t *comb_rows, *comb_cnt, *token_flat;
+  } ro{static_cast<const float*>(rv.logits), static_cast<const float*>(rv.gates),
+       static_cast<const float*>(rv.gate_raw), rv.comb_rows, rv.comb_cnt, rv.token_flat};
+  const float* w_r = static_cast<const float*>(p->w_r);
+  const float* t_emb = static_cast<const float*>(p->t_emb);
   if (!ro.logits || !ro.gates || !ro.gate_raw || !ro.comb_rows || !ro.comb_cnt)
     return fail(NIMG_ERR_SHAPE, "null routing pointer");
   const bool tc = ts.tc, bf = d->act_dtype == NIMG_BF16;
@@ -881,7 +962,7 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
   if (rtc && d->B > kMaxSeg) return fail(NIMG_ERR_CONFIG, "batch too large for one grouped launch");
   if (rtc) {
     // dx_norm = dl W_r[:d]^T: the forward's GEMM2 kernel (A = dl rows, K = E; B = W_r[:d] rows)
-    CUDA_TRY(launch_f32_to_bf16(p->w_r, w.wr16, dd * (int64_t)E, st));
+    CUDA_TRY(launch_f32_to_bf16(w_r, w.wr16, dd * (int64_t)E, st));
     {
       const bool pair = use_pair_kernels();
       const int bn = tc_bn_out(1), box = pair ? tc_b_box(1) / 2 : tc_b_box(1);
@@ -933,10 +1014,10 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
     }
     nchunks = (int)d->B;
   } else {
-    CUDA_TRY(launch_router_bwd_simt(bf, p->x_norm, p->w_r, w.dlogits, g->g_x_norm, w.part, T, dd, E,
+    CUDA_TRY(launch_router_bwd_simt(bf, p->x_norm, w_r, w.dlogits, g->g_x_norm, w.part, T, dd, E,
                                     st, &nchunks));
   }
-  CUDA_TRY(launch_router_bwd_fold(w.dlogits, p->t_emb, p->w_r, w.part, nchunks, w.colsum, g->g_w_r,
+  CUDA_TRY(launch_router_bwd_fold(w.dlogits, t_emb, w_r, w.part, nchunks, w.colsum, g->g_w_r,
                                   g->g_t_emb, (int)d->B, (int)d->S, dd, E, st));
   mark(1, st);
   const void* dys = tc ? g->g_out : w.dy_s;
@@ -1040,10 +1121,23 @@ int nimg_moe_block_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   return NIMG_OK;
 }
 
-int nimg_moe_block_forward(const nimg_moe_desc* d, const nimg_block_ptrs* b, int32_t layer, void* ws,
+// The block computes x_norm itself, in the activation dtype: the router reads
+// it in that dtype whatever router_dtype says. fp32 / bf16 only.
+static int check_block_desc(const nimg_moe_desc* d, nimg_moe_desc* local) {
+  NIMG_TRY(check_moe_desc(d));
+  if (d->act_dtype == NIMG_F64)
+    return fail(NIMG_ERR_CONFIG, "the fused MoE block has no f64 path (use the layer entry points)");
+  *local = *d;
+  local->router_dtype = d->act_dtype;
+  return NIMG_OK;
+}
+
+int nimg_moe_block_forward(const nimg_moe_desc* d_in, const nimg_block_ptrs* b, int32_t layer, void* ws,
                            size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  NIMG_TRY(check_moe_desc(d));
+  nimg_moe_desc dl;
+  NIMG_TRY(check_block_desc(d_in, &dl));
+  const nimg_moe_desc* d = &dl;
   if (!b || !b->x || !b->r_attn || !b->sa_gate || !b->ff_scale || !b->ff_gate || !b->t_vec ||
       !b->h || !b->x_norm || !b->x_mod || !b->out)
     return fail(NIMG_ERR_SHAPE, "null block pointer");
@@ -1087,12 +1181,14 @@ int nimg_moe_block_prologue_workspace_bytes(const nimg_moe_desc* d, size_t* byte
   return NIMG_OK;
 }
 
-int nimg_moe_block_prologue(const nimg_moe_desc* d, const void* x, const void* r_attn,
+int nimg_moe_block_prologue(const nimg_moe_desc* d_in, const void* x, const void* r_attn,
                             const float* sa_gate, const float* ff_scale, const float* ff_gate,
                             int32_t layer, void* h, void* x_norm, void* x_mod, void* th_ff, void* ws,
                             size_t ws_bytes, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  NIMG_TRY(check_moe_desc(d));
+  nimg_moe_desc dl;
+  NIMG_TRY(check_block_desc(d_in, &dl));
+  const nimg_moe_desc* d = &dl;
   if (!x || !r_attn || !sa_gate || !ff_scale || !ff_gate || !h || !x_norm || !x_mod || !th_ff)
     return fail(NIMG_ERR_SHAPE, "null block pointer");
   if (layer < 0) return fail(NIMG_ERR_CONFIG, "layer must be >= 0");

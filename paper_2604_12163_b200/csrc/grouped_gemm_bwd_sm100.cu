@@ -419,13 +419,8 @@ int tc_bwd_tile_rows(int mode) { return tc_bwd_pair(mode) ? 2 * tcb::BM : tcb::B
 template <int MODE, bool PAIR>
 static cudaError_t launch_bwd(const TmapSetBwd& tm, const BwdParams& p, int num_sms, cudaStream_t s) {
   constexpr int smem = tcb::smem_bytes<MODE, PAIR>();
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tcb::grouped_gemm_bwd_sm100<MODE, PAIR>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_max_dyn_smem(tcb::grouped_gemm_bwd_sm100<MODE, PAIR>, smem);
+  if (e != cudaSuccess) return e;
   const int units = PAIR ? num_sms / 2 : num_sms;
   const int grid = (p.total_tiles < units ? p.total_tiles : units) * (PAIR ? 2 : 1);
   if (!PAIR)

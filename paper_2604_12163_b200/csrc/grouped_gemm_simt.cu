@@ -7,6 +7,9 @@
 // segment/bank tables as the tensor-core kernel.
 //   MODE 0: pre[r, n] = SiLU(x W1^T) * (x W3^T)  (fp32 out)
 //   MODE 1: y[r, n]   = pre W2^T                  (fp32 out; `pre` is fp32)
+// The f64 storage mode (f64_kernels.cu) instantiates the same kernel with f64
+// operands, accumulators and outputs (ACC = double), as the reference's
+// swiglu computes with an f64 `pre` that is never rounded (moe.py:42-51).
 #include "common.cuh"
 #include "nimg_internal.h"
 
@@ -15,11 +18,17 @@ namespace simt {
 
 constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
 
-template <int MODE, typename TA, typename TW>
+template <typename ACC, typename T> NIMG_DEV ACC to_acc(T v) { return (ACC)to_f32(v); }
+template <> NIMG_DEV double to_acc<double, double>(double v) { return v; }
+NIMG_DEV float silu_mul(float v, float g) { return v / (1.0f + expf(-v)) * g; }
+// moe.py:45-48: h1 * (1 / (1 + exp(-h1))) * h3 in f64
+NIMG_DEV double silu_mul(double v, double g) { return v * (1.0 / (1.0 + exp(-v))) * g; }
+
+template <int MODE, typename TA, typename TW, typename ACC = float>
 __global__ void __launch_bounds__(NT) grouped_simt_kernel(const __grid_constant__ SimtParams p) {
-  __shared__ float As[BK][BM + 4];
-  __shared__ float Bs[BK][BN + 4];
-  __shared__ float B3s[MODE == 0 ? BK : 1][BN + 4];
+  __shared__ ACC As[BK][BM + 4];
+  __shared__ ACC Bs[BK][BN + 4];
+  __shared__ ACC B3s[MODE == 0 ? BK : 1][BN + 4];
 
   const int t = blockIdx.x;
   int lo = 0, hi = p.nseg - 1;
@@ -40,26 +49,26 @@ __global__ void __launch_bounds__(NT) grouped_simt_kernel(const __grid_constant_
   const TW* W3 = MODE == 0 ? reinterpret_cast<const TW*>(bk.w3) + e * (int64_t)bk.N * bk.K : nullptr;
 
   const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-  float acc[4][4], acc3[4][4];
+  ACC acc[4][4], acc3[4][4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) { acc[i][j] = 0.f; acc3[i][j] = 0.f; }
+    for (int j = 0; j < 4; ++j) { acc[i][j] = ACC(0); acc3[i][j] = ACC(0); }
 
   for (int k0 = 0; k0 < bk.K; k0 += BK) {
     for (int i = threadIdx.x; i < BM * BK; i += NT) {
       const int r = i / BK, kk = i % BK;
-      float v = 0.f;
-      if (r < rows && k0 + kk < bk.K) v = to_f32(A[(int64_t)(row0 + r) * bk.a_ld + k0 + kk]);
+      ACC v = ACC(0);
+      if (r < rows && k0 + kk < bk.K) v = to_acc<ACC>(A[(int64_t)(row0 + r) * bk.a_ld + k0 + kk]);
       As[kk][r] = v;
     }
     for (int i = threadIdx.x; i < BN * BK; i += NT) {
       const int c = i / BK, kk = i % BK;
-      float v = 0.f, v3 = 0.f;
+      ACC v = ACC(0), v3 = ACC(0);
       if (n0 + c < bk.N && k0 + kk < bk.K) {
         const int64_t off = (int64_t)(n0 + c) * bk.K + k0 + kk;
-        v = to_f32(W[off]);
-        if (MODE == 0) v3 = to_f32(W3[off]);
+        v = to_acc<ACC>(W[off]);
+        if (MODE == 0) v3 = to_acc<ACC>(W3[off]);
       }
       Bs[kk][c] = v;
       if (MODE == 0) B3s[kk][c] = v3;
@@ -67,7 +76,7 @@ __global__ void __launch_bounds__(NT) grouped_simt_kernel(const __grid_constant_
     __syncthreads();
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
-      float a[4], b[4], b3[4];
+      ACC a[4], b[4], b3[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
 #pragma unroll
@@ -79,8 +88,8 @@ __global__ void __launch_bounds__(NT) grouped_simt_kernel(const __grid_constant_
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-          if (MODE == 0) acc3[i][j] = fmaf(a[i], b3[j], acc3[i][j]);
+          acc[i][j] = fma(a[i], b[j], acc[i][j]);
+          if (MODE == 0) acc3[i][j] = fma(a[i], b3[j], acc3[i][j]);
         }
     }
     __syncthreads();
@@ -90,19 +99,19 @@ __global__ void __launch_bounds__(NT) grouped_simt_kernel(const __grid_constant_
   for (int i = 0; i < 4; ++i) {
     const int r = ty * 4 + i;
     if (r >= rows) continue;
-    float* o = bk.out + (int64_t)(row0 + r) * bk.out_ld;
+    ACC* o = static_cast<ACC*>(bk.out) + (int64_t)(row0 + r) * bk.out_ld;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = n0 + tx * 4 + j;
       if (c >= bk.N) continue;
-      float v = acc[i][j];
+      ACC v = acc[i][j];
       if (MODE == 0) {
-        if (bk.h_out != nullptr) {   // training forward: keep h1 | h3 for the pullback
+        if (sizeof(ACC) == 4 && bk.h_out != nullptr) {   // training forward: keep h1 | h3
           float* hrow = bk.h_out + (int64_t)(row0 + r) * (2 * bk.N);
-          hrow[c] = v;
-          hrow[bk.N + c] = acc3[i][j];
+          hrow[c] = (float)v;
+          hrow[bk.N + c] = (float)acc3[i][j];
         }
-        v = v / (1.0f + expf(-v)) * acc3[i][j];
+        v = silu_mul(v, acc3[i][j]);
       }
       o[c] = v;
     }
@@ -114,9 +123,15 @@ __global__ void __launch_bounds__(NT) grouped_simt_kernel(const __grid_constant_
 int simt_bm() { return simt::BM; }
 int simt_bn() { return simt::BN; }
 
-cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream) {
+cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream,
+                                bool f64) {
   if (p.total_tiles <= 0) return cudaSuccess;
   const int grid = p.total_tiles;
+  if (f64) {
+    if (mode == 0) simt::grouped_simt_kernel<0, double, double, double><<<grid, simt::NT, 0, stream>>>(p);
+    else simt::grouped_simt_kernel<1, double, double, double><<<grid, simt::NT, 0, stream>>>(p);
+    return cudaGetLastError();
+  }
   if (mode == 0) {
     if (in_bf16) simt::grouped_simt_kernel<0, bf16, bf16><<<grid, simt::NT, 0, stream>>>(p);
     else simt::grouped_simt_kernel<0, float, float><<<grid, simt::NT, 0, stream>>>(p);

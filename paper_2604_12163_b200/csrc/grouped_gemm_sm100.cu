@@ -328,9 +328,15 @@ constexpr int kGatherWarps = 2;
 // 32-row sub-blocks, each published with a release flag. The tile order is
 // rotated so the shared expert's tiles (no gathered operand) run first; the
 // TMA producer of a routed tile acquires the flags of its rows and fences the
-// async proxy before loading them. All CTAs are resident (persistent grid),
-// and the copies depend on nothing but the routing, so the waits cannot
-// deadlock. The gather's HBM traffic overlaps the shared tiles' tensor work.
+// async proxy before loading them. The gather's HBM traffic overlaps the
+// shared tiles' tensor work.
+// Forward progress does not assume co-residency of the grid (a concurrent
+// kernel, a second layer in flight or an SM-limited context can leave CTAs
+// unscheduled): sub-blocks are CLAIMED from a global counter (flags[nsub],
+// zeroed with the flags) by whichever copy warps are running, never assigned
+// to a CTA. A flag a producer waits on is therefore either claimed -- by a
+// warp that is running and finishes the copy -- or unclaimed, and then the
+// copy warps of the waiting CTA itself are still claiming and will take it.
 #ifndef NIMG_BG_WARPS
 #define NIMG_BG_WARPS 2
 #endif
@@ -508,13 +514,16 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
     }
   } else if (BG && warp >= 6) {
     // ------------------------------------------------ background gather (warps 6.., both CTAs)
-    const int gw = (int)blockIdx.x * kBgWarps + (warp - 6);
-    const int ngw = (int)gridDim.x * kBgWarps;
     const int nsub = (p.bg.rows + kBgRows - 1) / kBgRows;
     const int nv = p.bg.row_bytes >> 4;   // 16-B vectors per row
     const uint4* src = reinterpret_cast<const uint4*>(p.bg.src);
     uint4* dst = reinterpret_cast<uint4*>(p.bg.dst);
-    for (int j = gw; j < nsub; j += ngw) {
+    int* claim = p.bg.flags + nsub;
+    for (;;) {
+      int j = 0;
+      if (lane == 0) j = atomicAdd(claim, 1);
+      j = __shfl_sync(0xffffffffu, j, 0);
+      if (j >= nsub) break;
       const int r0 = j * kBgRows;
       const int nr = min(kBgRows, p.bg.rows - r0);
       const int my_src = lane < nr ? __ldg(p.bg.idx + r0 + lane) : 0;
@@ -616,13 +625,8 @@ template <int MODE, bool GATHER, int STAGES, bool BG = false>
 static cudaError_t launch_pair(const TmapSet& tm, const GroupedParams& p, int grid, cudaStream_t stream) {
   constexpr int smem = tc::pair_smem_bytes<MODE, STAGES>();
   constexpr int threads = tc::kThreads + (GATHER ? 32 * (tc::kGatherWarps + 1) : 0) + (BG ? 32 * tc::kBgWarps : 0);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES, BG>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  cudaError_t e = set_max_dyn_smem(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES, BG>, smem);
+  if (e != cudaSuccess) return e;
   return launch_pdl(tc::grouped_gemm_sm100_pair<MODE, GATHER, STAGES, BG>, dim3(grid), dim3(threads),
                     (size_t)smem, stream, tm, p);
 }
@@ -659,24 +663,14 @@ cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& 
   const int grid = p.total_tiles < num_sms ? p.total_tiles : num_sms;
   if (mode == 0) {
     constexpr int smem = tc::smem_bytes<0>();
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100<0>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    cudaError_t e = set_max_dyn_smem(tc::grouped_gemm_sm100<0>, smem);
+    if (e != cudaSuccess) return e;
     return launch_pdl(tc::grouped_gemm_sm100<0>, dim3(grid), dim3(tc::kThreads), (size_t)smem,
                       stream, tm, p);
   } else {
     constexpr int smem = tc::smem_bytes<1>();
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(tc::grouped_gemm_sm100<1>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
+    cudaError_t e = set_max_dyn_smem(tc::grouped_gemm_sm100<1>, smem);
+    if (e != cudaSuccess) return e;
     return launch_pdl(tc::grouped_gemm_sm100<1>, dim3(grid), dim3(tc::kThreads), (size_t)smem,
                       stream, tm, p);
   }

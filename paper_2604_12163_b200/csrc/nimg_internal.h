@@ -8,6 +8,14 @@
 
 namespace nimg {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is per device and per
+// kernel: a process that drives several GPUs must set it on each of them.
+cudaError_t set_max_dyn_smem(const void* kernel, int bytes);
+template <typename K>
+inline cudaError_t set_max_dyn_smem(K* kernel, int bytes) {
+  return set_max_dyn_smem(reinterpret_cast<const void*>(kernel), bytes);
+}
+
 typedef uint16_t bf16_raw;   // bf16 storage in host-visible signatures
 // elements of the row-blocked h1 | h3 buffer (hblk_off in common.cuh)
 inline int64_t hblk_elems(int64_t rows, int64_t h) { return (rows + 127) / 128 * 128 * 2 * h; }
@@ -39,7 +47,7 @@ struct BgGather {
   const void* src;       // x_mod rows
   const int32_t* idx;    // token_flat
   void* dst;             // gathered rows (the routed bank's A operand)
-  int* flags;            // one per 32-row sub-block, zeroed by gate_norm
+  int* flags;            // one per 32-row sub-block + the claim counter, zeroed by gate_norm
   int rows, row_bytes;   // null src: off
 };
 struct GroupedParams {
@@ -65,7 +73,7 @@ struct SimtBank {
   int64_t a_ld;
   const void* w;     // [E, N, K]   (W1 or W2)
   const void* w3;    // [E, N, K]   (W3, GEMM1 only)
-  float* out;        // [rows, N] fp32
+  void* out;         // [rows, N] fp32 (f64 in the f64 storage mode)
   int64_t out_ld;
   int K, N, ntn, pad_;
   float* h_out;      // GEMM1, training forward: h1 | h3 rows (2N fp32 per row) or null
@@ -169,7 +177,18 @@ cudaError_t launch_grouped_tc(int mode, const TmapSet& tm, const GroupedParams& 
 // in_bf16: activations/weights dtype (bf16 vs fp32); GEMM2 reads fp32 `pre`.
 int simt_bm();
 int simt_bn();
-cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream);
+cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream,
+                                bool f64 = false);
+
+// f64 storage mode (f64_kernels.cu): routing and combine with every value in f64
+cudaError_t launch_route_f64(const double* x_norm, const double* t_emb, const double* w_r,
+                             double* logits, double* scores_bes, int32_t* token_flat,
+                             double* gate_raw, double* gates, int32_t* comb_rows,
+                             int32_t* comb_cnt, int16_t* slot_of, int B, int S, int d, int E,
+                             int cap, double eps, double alpha, cudaStream_t st);
+cudaError_t launch_combine_f64(const double* yr, const double* ys, const double* gates,
+                               const int32_t* comb_rows, const int32_t* comb_cnt, double* out,
+                               int64_t T, int d, int E, cudaStream_t st);
 
 // routing / data-movement kernels (route_kernels.cu)
 // router prep (t-half bias + f64 copy of W_r[:d]) and FP64 scores kernel.

@@ -14,6 +14,7 @@
 //   combine        deterministic expert-ascending weighted sum + shared expert
 //                  (moe.py:156-161, tensor.py:366-378).
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 
 #include "common.cuh"
@@ -749,6 +750,147 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
   for (int i = tid; i < S; i += SEL_THREADS) scol[i] = (int16_t)(int32_t)keys[i];
 }
 
+// ------------------------------------------------------------------ select, warp per column
+// One warp per (b, e) column with the keys in registers (lane l holds tokens
+// l + 32 j): no block barriers. The cap-th largest key is found MSB-first, one
+// bit per step (thr grows while count(key >= thr | bit) >= cap, one redux.sync
+// per step); the winners are every key > thr plus the first (cap - #gt) keys
+// == thr in token order (ballot prefix in index order), then a warp bitonic
+// sort in shared memory orders them by (score desc, index asc) -- the order
+// of argsort(-x, kind="stable")[:cap] (router.py:98-101), as ec_select_kernel.
+// Padding keys are 0 (= NaN's key) with indices >= S, so they rank after
+// every real element and are never taken (cap <= S).
+constexpr int WS_WARPS = 4;
+template <int KPL>
+__global__ void __launch_bounds__(WS_WARPS * 32)
+ec_select_warp_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
+                      float* __restrict__ gate_raw, int16_t* __restrict__ slot_of, int B, int S,
+                      int E, int cap, int P) {
+  extern __shared__ __align__(16) uint64_t wsel[];   // [WS_WARPS][P]
+  pdl_trigger();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = blockIdx.x * WS_WARPS + warp;      // b * E + e: scores_bes is (B, E, S)
+  if (col >= B * E) return;
+  const int b = col / E, e = col - b * E;
+  const float* c = scores_bes + (int64_t)col * S;
+  uint32_t key[KPL];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const int i = lane + 32 * j;
+    key[j] = i < S ? score_key(__ldg(c + i)) : 0u;
+  }
+  uint32_t thr = 0u;
+#pragma unroll 1
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t cand = thr | (1u << bit);
+    int n = 0;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) n += key[j] >= cand ? 1 : 0;
+    if ((int)__reduce_add_sync(0xffffffffu, (unsigned)n) >= cap) thr = cand;
+  }
+  int n_gt = 0;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) n_gt += key[j] > thr ? 1 : 0;
+  const int need_eq = cap - (int)__reduce_add_sync(0xffffffffu, (unsigned)n_gt);
+  uint64_t* win = wsel + (size_t)warp * P;
+  const unsigned lt = (1u << lane) - 1u;
+  int n_eq = 0, n_w = 0;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const bool eq = key[j] == thr;
+    const unsigned me = __ballot_sync(0xffffffffu, eq);
+    const bool take = key[j] > thr || (eq && n_eq + __popc(me & lt) < need_eq);
+    const unsigned mt = __ballot_sync(0xffffffffu, take);
+    if (take)
+      win[n_w + __popc(mt & lt)] = ((uint64_t)key[j] << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(lane + 32 * j));
+    n_w += __popc(mt);
+    n_eq += __popc(me);
+  }
+  for (int i = cap + lane; i < P; i += 32) win[i] = 0ull;
+  // the column of the slot table: -1, then the winners' slots (after the sort)
+  int16_t* scol = slot_of + (int64_t)col * S;
+  for (int i = lane; i < S; i += 32) scol[i] = (int16_t)-1;
+  __syncwarp();
+  // bitonic sort of P composite keys, descending
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = lane; i < P / 2; i += 32) {
+        const int a = 2 * i - (i & (stride - 1));
+        const int cc = a + stride;
+        const bool desc = (a & size) == 0;
+        const uint64_t va = win[a], vc = win[cc];
+        if ((va < vc) == desc) { win[a] = vc; win[cc] = va; }
+      }
+      __syncwarp();
+    }
+  }
+  for (int j = lane; j < cap; j += 32) {
+    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(win[j] & 0xFFFFFFFFull);
+    const int64_t o = ((int64_t)e * B + b) * cap + j;
+    token_flat[o] = (int32_t)((int64_t)b * S + idx);
+    gate_raw[o] = c[idx];
+    scol[idx] = (int16_t)j;
+  }
+}
+
+// ------------------------------------------------------------------ gates, tile of 32 tokens
+// One block per 32 consecutive tokens of one sample (router.py:137-143): the
+// (B, E, S) slot table and scores are read coalesced (32 tokens of one expert
+// per warp load) and transposed through shared memory; then thread per token,
+// experts in ascending order: totals = fp32(sequential f64 sum -- the
+// np.add.at order), den = fp32(f64(tot) + f64(fp32 eps)), gate =
+// fp32(f64(fp32(f64(raw) / f64(den))) * f64(fp32 alpha)); the per-token
+// combine list. Same arithmetic as gate_norm_kernel.
+constexpr int GT_TOK = 32, GT_THREADS = 256;
+__global__ void __launch_bounds__(GT_THREADS)
+gate_tile_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict__ slot_of,
+                 float* __restrict__ gates, int32_t* __restrict__ comb_rows,
+                 int32_t* __restrict__ comb_cnt, int B, int S, int E, int cap, float eps32,
+                 float alpha32, int* __restrict__ bg_flags, int n_bg_flags) {
+  extern __shared__ __align__(16) uint8_t gsm[];
+  int16_t* sl = reinterpret_cast<int16_t*>(gsm);                               // [E][32]
+  float* raw = reinterpret_cast<float*>(gsm + (((size_t)E * GT_TOK * 2 + 15) & ~size_t(15)));  // [E][32]
+  pdl_trigger();
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bg_flags;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bg_flags[i] = 0;
+  const int tiles_per_b = (S + GT_TOK - 1) / GT_TOK;
+  const int b = blockIdx.x / tiles_per_b;
+  const int s0 = (blockIdx.x - b * tiles_per_b) * GT_TOK;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool in = s0 + lane < S;
+  for (int e = warp; e < E; e += GT_THREADS / 32) {
+    const int64_t o = ((int64_t)b * E + e) * S + s0 + lane;
+    const int16_t j = in ? slot_of[o] : (int16_t)-1;
+    sl[e * GT_TOK + lane] = j;
+    raw[e * GT_TOK + lane] = (in && j >= 0) ? scores_bes[o] : 0.f;
+  }
+  __syncthreads();
+  if (threadIdx.x >= GT_TOK || !in) return;
+  const int tok = threadIdx.x;
+  const int64_t t = (int64_t)b * S + s0 + tok;
+  double tot = 0.0;
+  int cnt = 0;
+  int32_t* cr = comb_rows + t * E;
+  for (int e = 0; e < E; ++e) {
+    const int j = sl[e * GT_TOK + tok];
+    if (j < 0) continue;
+    tot += (double)raw[e * GT_TOK + tok];
+    cr[cnt++] = (int32_t)(((int64_t)e * B + b) * cap + j);
+  }
+  comb_cnt[t] = cnt;
+  const float den = (float)((double)(float)tot + (double)eps32);
+  for (int k = 0, e = 0; k < cnt; ++e) {
+    const int j = sl[e * GT_TOK + tok];
+    if (j < 0) continue;
+    const float q = (float)((double)raw[e * GT_TOK + tok] / (double)den);
+    gates[cr[k]] = (float)((double)q * (double)alpha32);
+    ++k;
+  }
+}
+
 // ------------------------------------------------------------------ gates
 // Warp per token (router.py:137-143): the experts that picked the token, in
 // ascending order (ballot + prefix), totals = fp32(sequential f64 sum in that
@@ -1048,8 +1190,39 @@ size_t router_part_bytes(int B, int d, int E) {
 }
 size_t router_wd_bytes(int d, int E) { return (size_t)d * (E <= DM_EP ? DM_EP : router_geom(E).EP) * 8; }
 
+// NIMG_SELECT=cta: the block-per-column radix-select kernel for every S
+static bool select_warp_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_SELECT");
+    return !(e && strcmp(e, "cta") == 0);
+  }();
+  return on;
+}
+
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s) {
+  static const bool wide = [] {   // warp kernel up to S = 4096 (A/B: NIMG_SELECT_WIDE=1)
+    const char* e = getenv("NIMG_SELECT_WIDE");
+    return e && e[0] == '1';
+  }();
+  if (select_warp_enabled() && (S <= 1024 || (wide && S <= 4096))) {
+    const int P = next_pow2(cap);
+    const size_t wsmem = (size_t)WS_WARPS * P * 8;
+    const dim3 grid((unsigned)((B * E + WS_WARPS - 1) / WS_WARPS));
+#define NIMG_WSEL(K)                                                                            \
+    do {                                                                                        \
+      cudaError_t e2 = set_max_dyn_smem(ec_select_warp_kernel<K>, (int)wsmem);                  \
+      if (e2 != cudaSuccess) return e2;                                                         \
+      return launch_pdl(ec_select_warp_kernel<K>, grid, dim3(WS_WARPS * 32), wsmem, s,          \
+                        scores_bes, token_flat, gate_raw, slot_of, B, S, E, cap, P);           \
+    } while (0)
+    if (S <= 256) NIMG_WSEL(8);
+    if (S <= 512) NIMG_WSEL(16);
+    if (S <= 1024) NIMG_WSEL(32);
+    if (S <= 2048) NIMG_WSEL(64);
+    NIMG_WSEL(128);
+#undef NIMG_WSEL
+  }
   const size_t smem = select_smem(S, cap);
   cudaError_t err = cudaFuncSetAttribute(ec_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
@@ -1063,6 +1236,15 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
                              float gate_eps, float gate_scale, cudaStream_t s, int* bg_flags,
                              int n_bg_flags) {
   const int64_t T = (int64_t)B * S;
+  if (select_warp_enabled()) {
+    const size_t smem = (((size_t)E * GT_TOK * 2 + 15) & ~size_t(15)) + (size_t)E * GT_TOK * 4;
+    cudaError_t err = set_max_dyn_smem(gate_tile_kernel, (int)smem);
+    if (err != cudaSuccess) return err;
+    const int grid = B * ((S + GT_TOK - 1) / GT_TOK);
+    return launch_pdl(gate_tile_kernel, dim3(grid), dim3(GT_THREADS), smem, s, scores_bes, slot_of,
+                      gates, comb_rows, comb_cnt, B, S, E, cap, gate_eps, gate_scale, bg_flags,
+                      n_bg_flags);
+  }
   const int grid = (int)((T + GN_WARPS - 1) / GN_WARPS);
   const size_t smem = (size_t)GN_WARPS * E * 8;
   return launch_pdl(gate_norm_kernel, dim3(grid), dim3(GN_WARPS * 32), smem, s, scores_bes, slot_of,

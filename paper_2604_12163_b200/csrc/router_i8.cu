@@ -675,13 +675,8 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
                                                                               B, d);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
-  static bool attr = false;
-  if (!attr) {
-    err = cudaFuncSetAttribute(ri8::router_scores_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)ri8::SMEM);
-    if (err != cudaSuccess) return err;
-    attr = true;
-  }
+  err = set_max_dyn_smem(ri8::router_scores_i8_kernel, (int)ri8::SMEM);
+  if (err != cudaSuccess) return err;
   const bf16* x = reinterpret_cast<const bf16*>(x_norm);
   err = launch_pdl(ri8::router_scores_i8_kernel, dim3((unsigned)((T + ri8::BM - 1) / ri8::BM)),
                    dim3(ri8::THREADS), ri8::SMEM, s, x, w_r, (const double*)part, ws, logits, scores_bes,

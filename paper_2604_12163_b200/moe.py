@@ -16,7 +16,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._tensors import nimg_dtype, ptr, stream_handle, to_device, workspace
+from ._tensors import any_f64, nimg_dtype, ptr, stream_handle, to_device, workspace
 from .errors import ConfigError, ShapeError
 from .router import (RouterConfig, alloc_route_out, build_routing, capacity_for, make_desc,
                      route_full, route_struct)
@@ -92,8 +92,9 @@ def _ffn(x, offsets, experts, w1, w3, w2, out_dtype):
                         act_dtype=nimg_dtype(x.dtype), nseg=nseg)
     path, ydt = C.c_int32(), C.c_int32()
     _lib.check(_lib.lib.nimg_ffn_path(C.byref(desc), C.byref(path), C.byref(ydt)))
-    y = torch.empty((n, d), dtype=torch.bfloat16 if ydt.value == _lib.NIMG_BF16 else torch.float32,
-                    device=x.device)
+    ytype = {_lib.NIMG_BF16: torch.bfloat16, _lib.NIMG_F32: torch.float32,
+             _lib.NIMG_F64: torch.float64}[ydt.value]
+    y = torch.empty((n, d), dtype=ytype, device=x.device)
     nbytes = C.c_size_t()
     _lib.check(_lib.lib.nimg_ffn_workspace_bytes(C.byref(desc), C.byref(nbytes)))
     ws = workspace(nbytes.value)
@@ -106,8 +107,9 @@ def _ffn(x, offsets, experts, w1, w3, w2, out_dtype):
 
 
 def swiglu(x, w1, w3, w2):
-    """moe.py:31-64 -- (SiLU(x W1^T) * (x W3^T)) W2^T on the GPU."""
-    xt = to_device(x)
+    """moe.py:31-64 -- (SiLU(x W1^T) * (x W3^T)) W2^T on the GPU. Any float64
+    operand runs the f64 mode (f64 internals and output, moe.py:42-51)."""
+    xt = to_device(x, torch.float64 if any_f64(x, w1, w3, w2) else None)
     act = xt.dtype
     w1t, w3t, w2t = (to_device(w, act) for w in (w1, w3, w2))
     n, d = xt.shape[-2], xt.shape[-1]
@@ -136,7 +138,8 @@ def grouped_forward(batch: GroupedBatch, bank: ExpertBank):
     E = bank.n_experts
     if len(batch.offsets) != E + 1:
         raise ShapeError(f"offsets length {len(batch.offsets)} != E+1 ({E + 1})")
-    x = to_device(batch.tokens)
+    x = to_device(batch.tokens,
+                  torch.float64 if any_f64(batch.tokens, bank.w1, bank.w3, bank.w2) else None)
     act = x.dtype
     w1, w3, w2 = (to_device(w, act) for w in (bank.w1, bank.w3, bank.w2))
     E_, h, d = w1.shape
@@ -152,20 +155,26 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
     """moe.py:138-164 -- route on x_norm + t_emb, experts on x_mod.
 
     Returns (B, S, d) in the activation dtype of x_mod (fp32 or bf16); with
-    return_routing, (out, decisions, routing) like the reference. When grad
-    mode is on and any input or expert weight requires grad, the layer is
-    recorded on the autograd tape (training forward + nimg_moe_backward), the
-    way the reference's moe_forward records tape nodes.
+    return_routing, (out, decisions, routing) like the reference. Routing
+    reads x_norm in its own dtype (router.py:120-122). If any input or weight
+    is float64 the whole layer runs in the reference's f64 mode (f64 routing,
+    experts, combine and output; np.result_type promotion, tensor.py:203-204).
+    When grad mode is on and any input or expert weight requires grad, the
+    layer is recorded on the autograd tape (training forward +
+    nimg_moe_backward), the way the reference's moe_forward records tape nodes.
     """
     B, S, d = x.shape
     cfg.validate_weight(w_r)
-    xm = to_device(x_mod)
+    f64 = any_f64(x_norm, x_mod, t_emb, w_r, bank.w1, bank.w3, bank.w2, bank.shared_w1,
+                  bank.shared_w3, bank.shared_w2)
+    xm = to_device(x_mod, torch.float64 if f64 else None)
     act = xm.dtype
-    xn = to_device(x_norm, act)
+    xn = to_device(x_norm, act if f64 else None)
     if tuple(xm.shape) != (B, S, d) or tuple(xn.shape) != (B, S, d):
         raise ShapeError(f"x_norm {tuple(xn.shape)} / x_mod {tuple(xm.shape)} != {(B, S, d)}")
-    te = to_device(t_emb, torch.float32)
-    wr = to_device(w_r, torch.float32)
+    vdt = torch.float64 if f64 else torch.float32
+    te = to_device(t_emb, vdt)
+    wr = to_device(w_r, vdt)
     if tuple(te.shape) != (B, d):
         raise ConfigError(f"t_emb shape {tuple(te.shape)}, expected {(B, d)}")
     E = cfg.n_experts
@@ -177,8 +186,12 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
     w = bank_on_device(bank, act)
     _, h, hs = _check_bank_shapes(w.w1, w.w3, w.w2, w.shared_w1, w.shared_w3, w.shared_w2, d)
 
-    desc = make_desc(B, S, d, E, cap, h, hs, cfg, act)
+    desc = make_desc(B, S, d, E, cap, h, hs, cfg, act, xn.dtype)
     if _wants_grad(xn, xm, te, wr, w.w1, w.w3, w.w2, w.shared_w1, w.shared_w3, w.shared_w2):
+        if f64:
+            raise ConfigError("the f64 mode is forward-only: no training path in float64")
+        if xn.dtype != act:
+            raise ConfigError(f"training needs x_norm in x_mod's dtype ({xn.dtype} != {act})")
         meta = {"desc": desc, "shape": (B, S, d, E, cap, h, hs)}
         out = _MoELayerFn.apply(meta, xn, xm, te, wr, w.w1, w.w3, w.w2, w.shared_w1,
                                 w.shared_w3, w.shared_w2)
@@ -190,7 +203,7 @@ def moe_forward(x, x_norm, x_mod, t_emb, cfg: RouterConfig, bank: ExpertBank, w_
     _lib.check(_lib.lib.nimg_moe_workspace_bytes(C.byref(desc), C.byref(nbytes)))
     ws = workspace(nbytes.value)
     out = torch.empty((B, S, d), dtype=act, device=xm.device)
-    r = alloc_route_out(B, S, E, cap, xm.device)
+    r = alloc_route_out(B, S, E, cap, xm.device, vdt)
     ptrs = _lib.MoePtrs(ptr(xn), ptr(xm), ptr(te), ptr(wr), ptr(w.w1), ptr(w.w3), ptr(w.w2),
                         ptr(w.shared_w1), ptr(w.shared_w3), ptr(w.shared_w2), ptr(out),
                         route_struct(r))

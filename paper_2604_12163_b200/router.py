@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._tensors import nimg_dtype, ptr, stream_handle, to_device, workspace
+from ._tensors import any_f64, nimg_dtype, ptr, stream_handle, to_device, workspace
 from .errors import ConfigError
 
 __all__ = ["ConfigError", "StageId", "DENSE", "RouterConfig", "RouterDecision",
@@ -91,15 +91,20 @@ def capacity_schedule(layer: int, stage: StageId, n_layers: int = 32):
     raise ConfigError(f"unknown stage {stage!r}")
 
 
-def make_desc(B, S, d, E, cap, h, hs, cfg: RouterConfig, act: torch.dtype) -> _lib.MoeDesc:
+def make_desc(B, S, d, E, cap, h, hs, cfg: RouterConfig, act: torch.dtype,
+              router: torch.dtype | None = None) -> _lib.MoeDesc:
+    """act: dtype of x_mod / expert weights / out; router: dtype of x_norm
+    (default act). float64 (both) is the reference's f64 storage mode."""
     return _lib.MoeDesc(B=B, S=S, d=d, E=E, cap=cap, h=h, h_shared=hs,
                         gate_scale=float(cfg.gate_scale), gate_eps=float(cfg.gate_eps),
-                        act_dtype=nimg_dtype(act), reserved=0)
+                        act_dtype=nimg_dtype(act), router_dtype=nimg_dtype(router or act),
+                        gate_scale_f64=float(cfg.gate_scale), gate_eps_f64=float(cfg.gate_eps))
 
 
-def alloc_route_out(B: int, S: int, E: int, cap: int, dev) -> dict:
+def alloc_route_out(B: int, S: int, E: int, cap: int, dev, value_dtype=torch.float32) -> dict:
+    """Routing buffers; logits / scores / gates are fp32, or float64 in the f64 mode."""
     n = E * B * cap
-    f32, i32 = torch.float32, torch.int32
+    f32, i32 = value_dtype, torch.int32
     return {
         "logits": torch.empty((B, S, E), dtype=f32, device=dev),
         "scores_bes": torch.empty((B, E, S), dtype=f32, device=dev),
@@ -149,10 +154,13 @@ def route_full(x_norm, t_emb, w_r, cfg: RouterConfig):
 
     x_norm (B,S,d) fp32 or bf16; t_emb (B,d); w_r (2d,E). Logits and scores
     are fp32 (bit-exact with the reference's fp32 mode); token_flat is the
-    expert-major (e, b, slot) flat row index into (B*S, d).
+    expert-major (e, b, slot) flat row index into (B*S, d). If any input is
+    float64, routing runs in the reference's f64 mode (logits, scores and
+    gates stay float64, router.py:120-143).
     """
     cfg.validate_weight(w_r)
-    xn = to_device(x_norm)
+    f64 = any_f64(x_norm, t_emb, w_r)
+    xn = to_device(x_norm, torch.float64 if f64 else None)
     B, S, d = xn.shape
     E = cfg.n_experts
     if d != cfg.d_model:
@@ -160,15 +168,16 @@ def route_full(x_norm, t_emb, w_r, cfg: RouterConfig):
     cap = capacity_for(S, E, cfg.capacity_factor)
     if cap < 1:
         raise ConfigError("computed capacity is zero")
-    te = to_device(t_emb, torch.float32)
-    wr = to_device(w_r, torch.float32)
+    vdt = torch.float64 if f64 else torch.float32
+    te = to_device(t_emb, vdt)
+    wr = to_device(w_r, vdt)
     if tuple(te.shape) != (B, d):
         raise ConfigError(f"t_emb shape {tuple(te.shape)}, expected {(B, d)}")
     desc = make_desc(B, S, d, E, cap, 1, 1, cfg, xn.dtype)
     nbytes = C.c_size_t()
     _lib.check(_lib.lib.nimg_route_workspace_bytes(C.byref(desc), C.byref(nbytes)))
     ws = workspace(nbytes.value)
-    r = alloc_route_out(B, S, E, cap, xn.device)
+    r = alloc_route_out(B, S, E, cap, xn.device, vdt)
     ro = route_struct(r)
     _lib.check(_lib.lib.nimg_route(C.byref(desc), ptr(xn), ptr(te), ptr(wr), C.byref(ro),
                                    ptr(ws), ws.numel(), stream_handle()))

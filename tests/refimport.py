@@ -1,7 +1,9 @@
 """Import the read-only reference package under the alias ``nimg_ref``.
 
-Only usable in the build container (the reference tree does not travel to
-the GPU box). Location: $NIMG_REF, else /root/reference/pkg/src/nimg.
+Location: $NIMG_REF, else /root/reference/pkg/src/nimg (build container),
+else the offline pip install of the reference under baseline/_ref/nimg (the
+one copy that travels to the GPU box; git-ignored, built by
+`pip install --no-index --target baseline/_ref`).
 """
 
 from __future__ import annotations
@@ -10,7 +12,11 @@ import importlib.util
 import os
 import sys
 
-REF_DIR = os.environ.get("NIMG_REF", "/root/reference/pkg/src/nimg")
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_CANDIDATES = [os.environ.get("NIMG_REF"), "/root/reference/pkg/src/nimg",
+               os.path.join(_ROOT, "baseline", "_ref", "nimg")]
+REF_DIR = next((c for c in _CANDIDATES if c and os.path.isfile(os.path.join(c, "__init__.py"))),
+               _CANDIDATES[1])
 
 
 def reference_available() -> bool:

@@ -43,7 +43,8 @@ def test_capacity_for_matches_reference_host_logic():
 def test_workspace_and_validation_codes():
     L = _lib()
     d = L.MoeDesc(B=16, S=1024, d=2048, E=64, cap=64, h=1344, h_shared=1344, gate_scale=1.0,
-                  gate_eps=1e-6, act_dtype=L.NIMG_BF16, reserved=0)
+                  gate_eps=1e-6, act_dtype=L.NIMG_BF16, router_dtype=L.NIMG_BF16,
+                  gate_scale_f64=1.0, gate_eps_f64=1e-6)
     n = C.c_size_t()
     assert L.lib.nimg_moe_workspace_bytes(C.byref(d), C.byref(n)) == 0
     R_rows, T = 64 * 16 * 64, 16 * 1024
@@ -105,3 +106,35 @@ def test_python_api_mirrors_reference_host_functions():
     from paper_2604_12163_b200 import moe as M
     with pytest.raises(M.ShapeError):
         M.GroupedBatch(np.zeros((3, 2)), np.array([0, 2, 1]))
+
+
+def test_router_dtype_and_f64_mode_validation():
+    """ABI v2: router_dtype is x_norm's own dtype; NIMG_F64 is the reference's
+    f64 storage mode (forward only, all-f64)."""
+    L = _lib()
+    assert L.lib.nimg_abi_version() == L.ABI_VERSION == 2
+    base = dict(B=2, S=256, d=256, E=8, cap=64, h=168, h_shared=168, gate_scale=1.0,
+                gate_eps=1e-6, gate_scale_f64=1.0, gate_eps_f64=1e-6)
+    n = C.c_size_t()
+    ok = [(L.NIMG_BF16, L.NIMG_BF16), (L.NIMG_BF16, L.NIMG_F32), (L.NIMG_F32, L.NIMG_BF16),
+          (L.NIMG_F32, L.NIMG_F32), (L.NIMG_F64, L.NIMG_F64)]
+    bad = [(L.NIMG_F64, L.NIMG_F32), (L.NIMG_BF16, L.NIMG_F64), (L.NIMG_F32, 7), (5, L.NIMG_F32)]
+    for act, rt in ok:
+        d = L.MoeDesc(act_dtype=act, router_dtype=rt, **base)
+        assert L.lib.nimg_moe_workspace_bytes(C.byref(d), C.byref(n)) == 0, (act, rt)
+    for act, rt in bad:
+        d = L.MoeDesc(act_dtype=act, router_dtype=rt, **base)
+        assert L.lib.nimg_moe_workspace_bytes(C.byref(d), C.byref(n)) == L.NIMG_ERR_CONFIG
+    # training: same dtype for x_norm and x_mod, and no f64 path
+    for act, rt, want in ((L.NIMG_BF16, L.NIMG_BF16, 0), (L.NIMG_BF16, L.NIMG_F32, L.NIMG_ERR_CONFIG),
+                          (L.NIMG_F64, L.NIMG_F64, L.NIMG_ERR_CONFIG)):
+        d = L.MoeDesc(act_dtype=act, router_dtype=rt, **base)
+        assert L.lib.nimg_moe_train_state_bytes(C.byref(d), C.byref(n)) == want
+    d = L.MoeDesc(act_dtype=L.NIMG_F64, router_dtype=L.NIMG_F64, **dict(base, gate_eps_f64=0.0))
+    assert L.lib.nimg_moe_workspace_bytes(C.byref(d), C.byref(n)) == L.NIMG_ERR_CONFIG
+    # the f64 mode runs the CUDA-core GEMMs and returns f64 rows
+    f = L.FfnDesc(n_rows=512, n_shared_rows=0, d=256, h=168, h_shared=168, n_experts=8,
+                  act_dtype=L.NIMG_F64, nseg=8)
+    p, y = C.c_int32(), C.c_int32()
+    assert L.lib.nimg_ffn_path(C.byref(f), C.byref(p), C.byref(y)) == 0
+    assert (p.value, y.value) == (L.NIMG_PATH_SIMT, L.NIMG_F64)

@@ -215,8 +215,9 @@ def test_decoupling_and_determinism_and_permutation():    # test_moe.py:194-217,
 def test_full_width_layer_vs_oracle_and_properties(B, S, C, seed):
     """cfg2 / cfg3 / cfg4 / bucket shapes at full width (d=2048, h=1344, E=64) in bf16.
     Routing for every sample is checked bit-exactly against the oracle's
-    router; the layer output of sample 0 against the oracle's full layer;
-    plus size-independent properties over the whole batch."""
+    router and EVERY sample's layer output against the oracle's full layer
+    (run on the host cores, one call for the batch); plus size-independent
+    properties over the whole batch."""
     from paper_2604_12163_b200 import moe as M
     from paper_2604_12163_b200 import router as R
     d, h, E = 2048, 1344, 64
@@ -246,11 +247,13 @@ def test_full_width_layer_vs_oracle_and_properties(B, S, C, seed):
         for e in range(E):
             assert len(np.unique(top[b, e])) == cap
     assert np.all(np.diff(aff, axis=-1) <= 0)                       # score descending
-    # --- full layer output of sample 0 against the oracle layer
+    # --- every sample's layer output against the oracle layer
     w_np = [np_of(w) for w in ws]
-    o_ref = O.moe_forward(xn_np[:1], np_of(xm)[:1], te_np[:1], wr_np, *w_np, capacity_factor=C)
-    err = rel_fro(np_of(out[:1]), o_ref)
-    assert err <= TOL_BF16, f"rel-err {err:.3e}"
+    o_ref = O.moe_forward(xn_np, np_of(xm), te_np, wr_np, *w_np, capacity_factor=C)
+    out_np = np_of(out)
+    errs = [rel_fro(out_np[b], o_ref[b]) for b in range(B)]
+    assert max(errs) <= TOL_BF16, f"per-sample rel-err {errs}"
+    assert rel_fro(out_np, o_ref) <= TOL_BF16
 
 
 def test_host_pipeline_matches_direct_calls():
@@ -425,11 +428,12 @@ def test_block_full_width_bf16():
     r = O.route_full(xn, inp["t_vec"], inp["w_r"], n_experts=E, capacity_factor=C)
     np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), r["token_flat"])
     w = {k: inp[k] for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")}
-    moe = O.moe_forward(xn[:1], xm[:1], inp["t_vec"][:1], inp["w_r"], w["w1"], w["w3"], w["w2"],
+    moe = O.moe_forward(xn, xm, inp["t_vec"], inp["w_r"], w["w1"], w["w3"], w["w2"],
                         w["sw1"], w["sw3"], w["sw2"], capacity_factor=C)
-    want = hh[:1].astype(f64) + np.tanh(inp["ff_gate"][:1].astype(f64))[:, None, :] * moe
-    err = rel_fro(np_of(out[:1]), want)
-    assert err <= TOL_BF16, f"block bf16 rel-err {err:.3e}"
+    want = hh.astype(f64) + np.tanh(inp["ff_gate"].astype(f64))[:, None, :] * moe
+    got = np_of(out)
+    errs = [rel_fro(got[b], want[b]) for b in range(B)]
+    assert max(errs) <= TOL_BF16, f"block bf16 per-sample rel-err {errs}"
 
 
 @pytest.mark.parametrize("B,S,d,E,h,C", [(1, 40, 256, 8, 128, 1.0), (3, 56, 512, 8, 192, 2.0)])
@@ -449,3 +453,84 @@ def test_ragged_routed_rows_tcgen05(B, S, d, E, h, C):
                                  capacity_factor=C, return_routing=True)
     np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), ref["token_flat"])
     assert rel_fro(np_of(out), ref_out) <= TOL_BF16
+
+
+# ---------------------------------------------------------------- dtypes
+def test_router_reads_x_norm_in_its_own_dtype():
+    """fp32 x_norm with bf16 x_mod: the routing is computed on the fp32 x_norm
+    values (router.py:120-122), bit-exact with the oracle's fp32 routing --
+    not on a bf16-rounded copy; the experts run bf16 on x_mod."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    B, S, d, E, h, C = 2, 1024, 2048, 64, 1344, 4.0
+    inp = make_layer_inputs(43, B, S, d, E, h, layer=17, mode="fp32")
+    g = to_gpu(inp, "bf16")
+    xn32 = torch.from_numpy(inp["x_norm"]).cuda()           # fp32, not bf16-representable
+    assert not torch.equal(xn32, xn32.to(torch.bfloat16).float())
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    out, dec, routing = M.moe_forward(g["x_mod"], xn32, g["x_mod"], g["t_emb"], cfg, bank_of(g),
+                                      g["w_r"], return_routing=True)
+    assert out.dtype == torch.bfloat16
+    r = O.route_full(inp["x_norm"], inp["t_emb"], inp["w_r"], n_experts=E, capacity_factor=C)
+    np.testing.assert_array_equal(np_of(routing["logits"]), r["logits"])
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), r["token_flat"])
+    np.testing.assert_array_equal(np_of(routing["gates"]), r["gates"])
+    # the bf16-rounded router input would have routed differently
+    r16 = O.route_full(np_of(xn32.to(torch.bfloat16)), inp["t_emb"], inp["w_r"], n_experts=E,
+                       capacity_factor=C)
+    assert not np.array_equal(r16["logits"], r["logits"])
+    xm_np = np_of(g["x_mod"])
+    w_np = [np_of(g[k]) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")]
+    o_ref = O.moe_forward(inp["x_norm"], xm_np, inp["t_emb"], inp["w_r"], *w_np, capacity_factor=C)
+    assert rel_fro(np_of(out), o_ref) <= TOL_BF16
+    # and route_full / route alone take the fp32 x_norm the same way
+    dec2, rt2 = R.route_full(xn32, g["t_emb"], g["w_r"], cfg)
+    np.testing.assert_array_equal(np_of(rt2["logits"]), r["logits"])
+
+
+@pytest.mark.parametrize("B,S,d,E,h,C,gs", [(2, 256, 256, 8, 168, 2.0, 1.0),
+                                            (3, 37, 24, 5, 20, 1.7, 1.7),
+                                            (1, 1024, 2048, 64, 1344, 4.0, 1.0)])
+def test_f64_mode_layer_vs_oracle(B, S, d, E, h, C, gs):
+    """The reference's f64 storage mode (tensor.py:39-47): f64 activations with
+    the backbone's fp32 weights promote the whole layer to f64 (routing,
+    experts, combine, output). Against the oracle in f64: selections equal,
+    f64 values to summation-order level."""
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    inp = make_layer_inputs(51, B, S, d, E, h, layer=5, mode="fp32")
+    f64 = np.float64
+    x64 = {k: inp[k].astype(f64) for k in ("x_norm", "x_mod", "t_emb")}
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    ws = [T(inp[k]) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")]      # fp32 weights
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C, gate_scale=gs)
+    out, dec, routing = M.moe_forward(T(x64["x_mod"]), T(x64["x_norm"]), T(x64["x_mod"]),
+                                      T(x64["t_emb"]), cfg, M.ExpertBank(*ws), T(inp["w_r"]),
+                                      return_routing=True)
+    assert out.dtype == torch.float64 and routing["gates"].dtype == torch.float64
+    ref_out, ref = O.moe_forward(x64["x_norm"], x64["x_mod"], x64["t_emb"], inp["w_r"], inp["w1"],
+                                 inp["w3"], inp["w2"], inp["sw1"], inp["sw3"], inp["sw2"],
+                                 capacity_factor=C, gate_scale=gs, return_routing=True)
+    assert ref_out.dtype == f64
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), ref["token_flat"])
+    assert rel_fro(routing["logits"].cpu().numpy(), ref["logits"]) < 1e-14
+    assert rel_fro(routing["gates"].cpu().numpy(), ref["gates"]) < 1e-14
+    assert rel_fro(out.cpu().numpy(), ref_out) < 1e-12
+    # grouped_forward / swiglu take the same f64 path
+    y = M.swiglu(T(x64["x_mod"][0]), ws[3], ws[4], ws[5])
+    y_ref = O.swiglu_arrays(x64["x_mod"][0], inp["sw1"], inp["sw3"], inp["sw2"])
+    assert y.dtype == torch.float64 and rel_fro(y.cpu().numpy(), y_ref) < 1e-13
+
+
+def test_f64_mode_is_forward_only():
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    from paper_2604_12163_b200.errors import ConfigError
+    inp = make_layer_inputs(52, 1, 64, 64, 4, 64, mode="fp32")
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    xn = T(inp["x_norm"].astype(np.float64)).requires_grad_(True)
+    bank = M.ExpertBank(*(T(inp[k]) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")))
+    cfg = R.RouterConfig(d_model=64, n_experts=4, capacity_factor=2.0)
+    with pytest.raises(ConfigError):
+        M.moe_forward(T(inp["x_mod"]), xn, T(inp["x_mod"]), T(inp["t_emb"]), cfg, bank,
+                      T(inp["w_r"]))
