@@ -636,6 +636,8 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     import torch
     import torch.distributed as dist
     from paper_2604_12163_b200.ep import ep_moe_forward
+    from paper_2604_12163_b200.nvlink import NvLinkCounters
+    nvl = NvLinkCounters(dev.index)
     inp, bank, cfg, w_r = _ep_setup(c, world, rank, dev)
     step = lambda: ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx)
     for _ in range(args.warmup):
@@ -646,6 +648,7 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     per = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     hts = []
     ms0 = torch.cuda.memory_stats(dev)
+    nv0 = nvl.snapshot()
     e0.record()
     h0 = time.perf_counter()
     for i in range(args.steps):
@@ -655,10 +658,22 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # issue time per step
     e1.record()
     torch.cuda.synchronize()
+    nv1 = nvl.snapshot()
     dist.barrier()
     t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     out = {"ms": float(t.item()), "host_issue_ms": round(host_ms, 4)}
+    # NVLink hardware counters (NVML) over the timed steps: what this GPU put
+    # on / took off its links, against the exchange's algorithmic bytes
+    from paper_2604_12163_b200.router import capacity_for
+    cap = capacity_for(c["S"], c["E"], c["C"])
+    chunk = c["E"] // world * (c["B"] // world) * cap * c["d"] * 2
+    nvd = NvLinkCounters.delta(nv0, nv1, e0.elapsed_time(e1) * 1e-3)
+    out["nvlink_counters"] = (
+        dict(nvd, steps=args.steps, algorithmic_bytes_per_dir=2 * chunk * (world - 1) * args.steps,
+             what="NVML per-link NVLink TX/RX counters summed over active links, rank-local, "
+                  "timed steps only; algorithmic = dispatch + return chunks sent (= received)")
+        if nvd is not None else {"unavailable": nvl.err})
     if os.environ.get("NIMG_BENCH_DEBUG"):
         dev_steps = [round(e0.elapsed_time(per[0]), 3)] + [
             round(per[i - 1].elapsed_time(per[i]), 3) for i in range(1, args.steps)]
@@ -789,6 +804,7 @@ def run_ep(args, c, peaks, peak_kind):
         strong = {"workload": workload_name(CFG4), "ms_per_step": st["ms"],
                   "value": wc4["T"] / (st["ms"] * 1e-3), "unit": "tokens/s",
                   "timeline_ms_rank0": st["timeline"], "nvlink_dispatch_rank0": st.get("dispatch"),
+                  "nvlink_counters_rank0": st.get("nvlink_counters"),
                   "host_issue_ms_rank0": st.get("host_issue_ms")}
         if ms1 is not None:
             strong["same_config_1gpu"] = {"ms_per_step": ms1, "value": wc4["T"] / (ms1 * 1e-3)}
@@ -815,6 +831,7 @@ def run_ep(args, c, peaks, peak_kind):
             "a2a_bytes_per_rank_per_direction": a2a,
             "timeline_ms_rank0": main["timeline"],
             "nvlink_dispatch_rank0": main.get("dispatch"),
+            "nvlink_counters_rank0": main.get("nvlink_counters"),
             "host_issue_ms_rank0": main.get("host_issue_ms"),
             "cfg4_strong": strong,
             "e2e": {"value": wcw["T"] / (main["e2e_ms"] * 1e-3), "unit": "tokens/s",

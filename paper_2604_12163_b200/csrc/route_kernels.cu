@@ -750,83 +750,109 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
   for (int i = tid; i < S; i += SEL_THREADS) scol[i] = (int16_t)(int32_t)keys[i];
 }
 
-// ------------------------------------------------------------------ select, warp per column
-// One warp per (b, e) column with the keys in registers (lane l holds tokens
-// l + 32 j): no block barriers. The cap-th largest key is found MSB-first, one
-// bit per step (thr grows while count(key >= thr | bit) >= cap, one redux.sync
-// per step); the winners are every key > thr plus the first (cap - #gt) keys
-// == thr in token order (ballot prefix in index order), then a warp bitonic
-// sort in shared memory orders them by (score desc, index asc) -- the order
-// of argsort(-x, kind="stable")[:cap] (router.py:98-101), as ec_select_kernel.
-// Padding keys are 0 (= NaN's key) with indices >= S, so they rank after
-// every real element and are never taken (cap <= S).
-constexpr int WS_WARPS = 4;
+// ------------------------------------------------------------------ select, block per column
+// One 128-thread block per (b, e) column with the keys in registers (warp w
+// holds tokens [w S/4, (w+1) S/4), lane l of it tokens l + 32 j): the cap-th
+// largest key is found MSB-first, two bits per step (16 steps, three
+// candidate counts per step, one redux.sync each, the four warps' counts
+// summed through shared memory behind one barrier). The winners are every key
+// > thr plus the first (cap - #gt) keys == thr in token order, then one warp
+// sorts them by (score desc, index asc) -- the order of argsort(-x,
+// kind="stable")[:cap] (router.py:98-101). Padding keys are 0 (= NaN's key)
+// with indices >= S, so they rank after every real element and are never
+// taken (cap <= S).
+constexpr int SB_WARPS = 4;
 template <int KPL>
-__global__ void __launch_bounds__(WS_WARPS * 32)
-ec_select_warp_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
-                      float* __restrict__ gate_raw, int16_t* __restrict__ slot_of, int B, int S,
-                      int E, int cap, int P) {
-  extern __shared__ __align__(16) uint64_t wsel[];   // [WS_WARPS][P]
+__global__ void __launch_bounds__(SB_WARPS * 32)
+ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
+                     float* __restrict__ gate_raw, int16_t* __restrict__ slot_of, int B, int S,
+                     int E, int cap, int P) {
+  extern __shared__ __align__(16) uint64_t wsel[];   // [P] winners
+  __shared__ int red[2][SB_WARPS][4];
+  __shared__ int wcnt[SB_WARPS][2];
   pdl_trigger();
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col = blockIdx.x * WS_WARPS + warp;      // b * E + e: scores_bes is (B, E, S)
-  if (col >= B * E) return;
+  const int col = blockIdx.x;                         // b * E + e: scores_bes is (B, E, S)
   const int b = col / E, e = col - b * E;
   const float* c = scores_bes + (int64_t)col * S;
+  const int i0 = warp * 32 * KPL + lane;              // token of key[0]
   uint32_t key[KPL];
 #pragma unroll
   for (int j = 0; j < KPL; ++j) {
-    const int i = lane + 32 * j;
+    const int i = i0 + 32 * j;
     key[j] = i < S ? score_key(__ldg(c + i)) : 0u;
   }
   uint32_t thr = 0u;
 #pragma unroll 1
-  for (int bit = 31; bit >= 0; --bit) {
-    const uint32_t cand = thr | (1u << bit);
-    int n = 0;
+  for (int sh = 30, buf = 0; sh >= 0; sh -= 2, buf ^= 1) {
+    int n1 = 0, n2 = 0, n3 = 0;
 #pragma unroll
-    for (int j = 0; j < KPL; ++j) n += key[j] >= cand ? 1 : 0;
-    if ((int)__reduce_add_sync(0xffffffffu, (unsigned)n) >= cap) thr = cand;
+    for (int j = 0; j < KPL; ++j) {
+      n1 += key[j] >= (thr | (1u << sh)) ? 1 : 0;
+      n2 += key[j] >= (thr | (2u << sh)) ? 1 : 0;
+      n3 += key[j] >= (thr | (3u << sh)) ? 1 : 0;
+    }
+    n1 = (int)__reduce_add_sync(0xffffffffu, (unsigned)n1);
+    n2 = (int)__reduce_add_sync(0xffffffffu, (unsigned)n2);
+    n3 = (int)__reduce_add_sync(0xffffffffu, (unsigned)n3);
+    if (lane == 0) { red[buf][warp][1] = n1; red[buf][warp][2] = n2; red[buf][warp][3] = n3; }
+    __syncthreads();   // double-buffered counts: one barrier per step
+    int t1 = 0, t2 = 0, t3 = 0;
+#pragma unroll
+    for (int w = 0; w < SB_WARPS; ++w) { t1 += red[buf][w][1]; t2 += red[buf][w][2]; t3 += red[buf][w][3]; }
+    thr |= (t3 >= cap ? 3u : t2 >= cap ? 2u : t1 >= cap ? 1u : 0u) << sh;
   }
-  int n_gt = 0;
+  int n_gt = 0, n_eq = 0;
 #pragma unroll
-  for (int j = 0; j < KPL; ++j) n_gt += key[j] > thr ? 1 : 0;
-  const int need_eq = cap - (int)__reduce_add_sync(0xffffffffu, (unsigned)n_gt);
-  uint64_t* win = wsel + (size_t)warp * P;
+  for (int j = 0; j < KPL; ++j) { n_gt += key[j] > thr ? 1 : 0; n_eq += key[j] == thr ? 1 : 0; }
+  n_gt = (int)__reduce_add_sync(0xffffffffu, (unsigned)n_gt);
+  n_eq = (int)__reduce_add_sync(0xffffffffu, (unsigned)n_eq);
+  if (lane == 0) { wcnt[warp][0] = n_gt; wcnt[warp][1] = n_eq; }
+  __syncthreads();
+  int gt_all = 0, eq_before = 0, w_before = 0;
+#pragma unroll
+  for (int w = 0; w < SB_WARPS; ++w) gt_all += wcnt[w][0];
+  const int need_eq = cap - gt_all;
+  for (int w = 0; w < warp; ++w) {
+    eq_before += wcnt[w][1];
+    w_before += wcnt[w][0] + max(0, min(wcnt[w][1], need_eq - (eq_before - wcnt[w][1])));
+  }
   const unsigned lt = (1u << lane) - 1u;
-  int n_eq = 0, n_w = 0;
+  int n_w = w_before;
 #pragma unroll
   for (int j = 0; j < KPL; ++j) {
     const bool eq = key[j] == thr;
     const unsigned me = __ballot_sync(0xffffffffu, eq);
-    const bool take = key[j] > thr || (eq && n_eq + __popc(me & lt) < need_eq);
+    const bool take = key[j] > thr || (eq && eq_before + __popc(me & lt) < need_eq);
     const unsigned mt = __ballot_sync(0xffffffffu, take);
     if (take)
-      win[n_w + __popc(mt & lt)] = ((uint64_t)key[j] << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(lane + 32 * j));
+      wsel[n_w + __popc(mt & lt)] =
+          ((uint64_t)key[j] << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)(i0 + 32 * j));
     n_w += __popc(mt);
-    n_eq += __popc(me);
+    eq_before += __popc(me);
   }
-  for (int i = cap + lane; i < P; i += 32) win[i] = 0ull;
+  for (int i = cap + threadIdx.x; i < P; i += SB_WARPS * 32) wsel[i] = 0ull;
   // the column of the slot table: -1, then the winners' slots (after the sort)
   int16_t* scol = slot_of + (int64_t)col * S;
-  for (int i = lane; i < S; i += 32) scol[i] = (int16_t)-1;
-  __syncwarp();
-  // bitonic sort of P composite keys, descending
+  for (int i = threadIdx.x; i < S; i += SB_WARPS * 32) scol[i] = (int16_t)-1;
+  __syncthreads();
+  // bitonic sort of P composite keys, descending, by all warps
   for (int size = 2; size <= P; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = lane; i < P / 2; i += 32) {
+      for (int i = threadIdx.x; i < P / 2; i += SB_WARPS * 32) {
         const int a = 2 * i - (i & (stride - 1));
         const int cc = a + stride;
         const bool desc = (a & size) == 0;
-        const uint64_t va = win[a], vc = win[cc];
-        if ((va < vc) == desc) { win[a] = vc; win[cc] = va; }
+        const uint64_t va = wsel[a], vc = wsel[cc];
+        if ((va < vc) == desc) { wsel[a] = vc; wsel[cc] = va; }
       }
-      __syncwarp();
+      if (P > 64) __syncthreads(); else __syncwarp();
     }
   }
-  for (int j = lane; j < cap; j += 32) {
-    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(win[j] & 0xFFFFFFFFull);
+  if (P <= 64 && warp != 0) return;   // the sort ran in warp 0 alone (P/2 <= 32 pairs)
+  for (int j = threadIdx.x; j < cap; j += (P <= 64 ? 32 : SB_WARPS * 32)) {
+    const uint32_t idx = 0xFFFFFFFFu - (uint32_t)(wsel[j] & 0xFFFFFFFFull);
     const int64_t o = ((int64_t)e * B + b) * cap + j;
     token_flat[o] = (int32_t)((int64_t)b * S + idx);
     gate_raw[o] = c[idx];
@@ -837,11 +863,11 @@ ec_select_warp_kernel(const float* __restrict__ scores_bes, int32_t* __restrict_
 // ------------------------------------------------------------------ gates, tile of 32 tokens
 // One block per 32 consecutive tokens of one sample (router.py:137-143): the
 // (B, E, S) slot table and scores are read coalesced (32 tokens of one expert
-// per warp load) and transposed through shared memory; then thread per token,
-// experts in ascending order: totals = fp32(sequential f64 sum -- the
-// np.add.at order), den = fp32(f64(tot) + f64(fp32 eps)), gate =
-// fp32(f64(fp32(f64(raw) / f64(den))) * f64(fp32 alpha)); the per-token
-// combine list. Same arithmetic as gate_norm_kernel.
+// per warp load) and transposed through shared memory; then warp per token as
+// gate_norm_kernel: the selecting experts in ascending order (ballot prefix),
+// totals = fp32(sequential f64 sum -- the np.add.at order), den = fp32(f64(tot)
+// + f64(fp32 eps)), gate = fp32(f64(fp32(f64(raw) / f64(den))) * f64(fp32
+// alpha)); the per-token combine list.
 constexpr int GT_TOK = 32, GT_THREADS = 256;
 __global__ void __launch_bounds__(GT_THREADS)
 gate_tile_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict__ slot_of,
@@ -849,8 +875,12 @@ gate_tile_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict
                  int32_t* __restrict__ comb_cnt, int B, int S, int E, int cap, float eps32,
                  float alpha32, int* __restrict__ bg_flags, int n_bg_flags) {
   extern __shared__ __align__(16) uint8_t gsm[];
-  int16_t* sl = reinterpret_cast<int16_t*>(gsm);                               // [E][32]
-  float* raw = reinterpret_cast<float*>(gsm + (((size_t)E * GT_TOK * 2 + 15) & ~size_t(15)));  // [E][32]
+  constexpr int NW = GT_THREADS / 32;
+  int16_t* sl = reinterpret_cast<int16_t*>(gsm);                                  // [E][32]
+  const size_t o1 = ((size_t)E * GT_TOK * 2 + 15) & ~size_t(15);
+  float* raw = reinterpret_cast<float*>(gsm + o1);                               // [E][32]
+  float* raw_l = raw + (size_t)E * GT_TOK;                                       // [NW][E]
+  int32_t* row_l = reinterpret_cast<int32_t*>(raw_l + (size_t)NW * E);           // [NW][E]
   pdl_trigger();
   pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_bg_flags;
@@ -861,33 +891,42 @@ gate_tile_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict
   const int s0 = (blockIdx.x - b * tiles_per_b) * GT_TOK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool in = s0 + lane < S;
-  for (int e = warp; e < E; e += GT_THREADS / 32) {
+  for (int e = warp; e < E; e += NW) {
     const int64_t o = ((int64_t)b * E + e) * S + s0 + lane;
     const int16_t j = in ? slot_of[o] : (int16_t)-1;
     sl[e * GT_TOK + lane] = j;
     raw[e * GT_TOK + lane] = (in && j >= 0) ? scores_bes[o] : 0.f;
   }
   __syncthreads();
-  if (threadIdx.x >= GT_TOK || !in) return;
-  const int tok = threadIdx.x;
-  const int64_t t = (int64_t)b * S + s0 + tok;
-  double tot = 0.0;
-  int cnt = 0;
-  int32_t* cr = comb_rows + t * E;
-  for (int e = 0; e < E; ++e) {
-    const int j = sl[e * GT_TOK + tok];
-    if (j < 0) continue;
-    tot += (double)raw[e * GT_TOK + tok];
-    cr[cnt++] = (int32_t)(((int64_t)e * B + b) * cap + j);
-  }
-  comb_cnt[t] = cnt;
-  const float den = (float)((double)(float)tot + (double)eps32);
-  for (int k = 0, e = 0; k < cnt; ++e) {
-    const int j = sl[e * GT_TOK + tok];
-    if (j < 0) continue;
-    const float q = (float)((double)raw[e * GT_TOK + tok] / (double)den);
-    gates[cr[k]] = (float)((double)q * (double)alpha32);
-    ++k;
+  float* rl = raw_l + (size_t)warp * E;
+  int32_t* ro = row_l + (size_t)warp * E;
+  for (int tok = warp; tok < GT_TOK && s0 + tok < S; tok += NW) {
+    const int64_t t = (int64_t)b * S + s0 + tok;
+    int cnt = 0;
+    for (int e0 = 0; e0 < E; e0 += 32) {
+      const int e = e0 + lane;
+      const int j = e < E ? (int)sl[e * GT_TOK + tok] : -1;
+      const unsigned m = __ballot_sync(0xffffffffu, j >= 0);
+      if (j >= 0) {
+        const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+        rl[pos] = raw[e * GT_TOK + tok];
+        ro[pos] = (int32_t)(((int64_t)e * B + b) * cap + j);
+      }
+      cnt += __popc(m);
+    }
+    __syncwarp();
+    double tot = 0.0;
+    if (lane == 0)
+      for (int k = 0; k < cnt; ++k) tot += (double)rl[k];
+    const float tot32 = __shfl_sync(0xffffffffu, (float)tot, 0);
+    const float den = (float)((double)tot32 + (double)eps32);
+    for (int k = lane; k < cnt; k += 32) {
+      const float q = (float)((double)rl[k] / (double)den);
+      gates[ro[k]] = (float)((double)q * (double)alpha32);
+      comb_rows[t * E + k] = ro[k];
+    }
+    if (lane == 0) comb_cnt[t] = cnt;
+    __syncwarp();
   }
 }
 
@@ -1201,27 +1240,23 @@ static bool select_warp_enabled() {
 
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s) {
-  static const bool wide = [] {   // warp kernel up to S = 4096 (A/B: NIMG_SELECT_WIDE=1)
-    const char* e = getenv("NIMG_SELECT_WIDE");
-    return e && e[0] == '1';
-  }();
-  if (select_warp_enabled() && (S <= 1024 || (wide && S <= 4096))) {
+  if (select_warp_enabled() && S <= 4096) {
     const int P = next_pow2(cap);
-    const size_t wsmem = (size_t)WS_WARPS * P * 8;
-    const dim3 grid((unsigned)((B * E + WS_WARPS - 1) / WS_WARPS));
-#define NIMG_WSEL(K)                                                                            \
+    const size_t wsmem = (size_t)P * 8;
+    const dim3 grid((unsigned)(B * E));
+#define NIMG_BSEL(K)                                                                            \
     do {                                                                                        \
-      cudaError_t e2 = set_max_dyn_smem(ec_select_warp_kernel<K>, (int)wsmem);                  \
+      cudaError_t e2 = set_max_dyn_smem(ec_select_blk_kernel<K>, (int)wsmem);                   \
       if (e2 != cudaSuccess) return e2;                                                         \
-      return launch_pdl(ec_select_warp_kernel<K>, grid, dim3(WS_WARPS * 32), wsmem, s,          \
+      return launch_pdl(ec_select_blk_kernel<K>, grid, dim3(SB_WARPS * 32), wsmem, s,           \
                         scores_bes, token_flat, gate_raw, slot_of, B, S, E, cap, P);           \
     } while (0)
-    if (S <= 256) NIMG_WSEL(8);
-    if (S <= 512) NIMG_WSEL(16);
-    if (S <= 1024) NIMG_WSEL(32);
-    if (S <= 2048) NIMG_WSEL(64);
-    NIMG_WSEL(128);
-#undef NIMG_WSEL
+    if (S <= 256) NIMG_BSEL(2);
+    if (S <= 512) NIMG_BSEL(4);
+    if (S <= 1024) NIMG_BSEL(8);
+    if (S <= 2048) NIMG_BSEL(16);
+    NIMG_BSEL(32);
+#undef NIMG_BSEL
   }
   const size_t smem = select_smem(S, cap);
   cudaError_t err = cudaFuncSetAttribute(ec_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1237,7 +1272,8 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
                              int n_bg_flags) {
   const int64_t T = (int64_t)B * S;
   if (select_warp_enabled()) {
-    const size_t smem = (((size_t)E * GT_TOK * 2 + 15) & ~size_t(15)) + (size_t)E * GT_TOK * 4;
+    const size_t smem = (((size_t)E * GT_TOK * 2 + 15) & ~size_t(15)) + (size_t)E * GT_TOK * 4 +
+                        (size_t)(GT_THREADS / 32) * E * 8;
     cudaError_t err = set_max_dyn_smem(gate_tile_kernel, (int)smem);
     if (err != cudaSuccess) return err;
     const int grid = B * ((S + GT_TOK - 1) / GT_TOK);

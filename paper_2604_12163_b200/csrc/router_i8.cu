@@ -47,22 +47,67 @@ namespace ri8 {
 
 constexpr int NE = 64;                       // experts = UMMA N
 constexpr int BM = 128;                      // tokens per CTA = UMMA M = TMEM lanes
-constexpr int KB = 128;                      // k per stage: one 128-B swizzle row of int8
+// k per stage = the int8 row of one swizzle atom: 64 (64-B swizzle, 4 stages of
+// 52 KB: the MMAs never wait on a refill) or 128 (128-B swizzle, 2 stages of
+// 104 KB: measured MMA-starved, profiles/r02_router_ncu.md)
+#ifndef NIMG_I8_KB
+#define NIMG_I8_KB 64
+#endif
+constexpr int KB = NIMG_I8_KB;
+static_assert(KB == 64 || KB == 128, "stage k width");
+constexpr int CPR = KB / 16;                 // 16-element chunks per row and stage
+// byte offset of 16-B chunk c of K-major row r inside a swizzled operand slice
+NIMG_DEV int swz_off(int r, int c) {
+  return KB == 128 ? r * KB + ((c ^ (r & 7)) << 4) : r * KB + ((c ^ ((r >> 1) & 3)) << 4);
+}
+NIMG_DEV uint64_t sdesc_k(uint32_t addr) {
+  if (KB == 128) return make_sdesc_k128(addr);
+  uint64_t dsc = 0;                           // K-major, 64-B swizzle: 8-row atoms of 64 B
+  dsc |= (uint64_t)((addr >> 4) & 0x3FFF);
+  dsc |= (uint64_t)1 << 16;                   // LBO (unused)
+  dsc |= (uint64_t)(512 >> 4) << 32;          // SBO: 8 rows x 64 B
+  dsc |= (uint64_t)1 << 46;                   // descriptor version (sm_100)
+  dsc |= (uint64_t)4 << 61;                   // SWIZZLE_64B
+  return dsc;
+}
 // x digit planes: 4 (28-bit window, the default) or 3 (21-bit: measured slower,
 // its narrower window sends ~1 element per row to the exact f64 list); W_r always 5
 #ifndef NIMG_I8_LX
 #define NIMG_I8_LX 4
 #endif
 constexpr int LX = NIMG_I8_LX, LW = 5, NG = LX + LW - 1;
-constexpr int XW = 7 * LX - 8;               // binades of the x window: 13 or 20
+// binades of the x window: 12 or 19. |X| < 2^(7 LX - 1) keeps every balanced
+// digit of the fast path (below) within [-64, 64] and the top digit of the
+// slow path's two's-complement split within [-64, 63].
+constexpr int XW = 7 * LX - 9;
+// Fast-path conversion on the FMA pipe (NIMG_I8_FCONV=0: the integer path)
+#ifndef NIMG_I8_FCONV
+#define NIMG_I8_FCONV 1
+#endif
+// NIMG_I8_TRACE=1: CTAs 0 and 64 printf a %globaltimer trace (A/B builds only)
+#ifndef NIMG_I8_TRACE
+#define NIMG_I8_TRACE 0
+#endif
+NIMG_DEV uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// timing probes for A/B builds only (wrong results): 1 = no conversion,
+// 2 = no MMAs, 3 = no epilogue
+#ifndef NIMG_I8_PROBE
+#define NIMG_I8_PROBE 0
+#endif
 constexpr int XH = LX == 3 ? 1 : 2;          // headroom over the first-stage max
 static_assert(LX == 3 || LX == 4, "x digit planes");
-constexpr int A_SLICE = BM * KB;             // 16 KB
-constexpr int W_SLICE = NE * KB;             // 8 KB
-constexpr int W_STAGE = LW * W_SLICE;        // 40 KB
-constexpr int STAGE = LX * A_SLICE + W_STAGE;   // 88 / 104 KB
-constexpr int NSTAGE = 2;
+constexpr int A_SLICE = BM * KB;             // 8 / 16 KB
+constexpr int W_SLICE = NE * KB;             // 4 / 8 KB
+constexpr int W_STAGE = LW * W_SLICE;        // 20 / 40 KB
+constexpr int STAGE = LX * A_SLICE + W_STAGE;   // 52 / 104 KB (LX = 4)
+constexpr int NSTAGE = KB == 64 ? 4 : 2;
 constexpr int NCONV = 512;                   // converter / epilogue threads (warps 0-15)
+constexpr int JOBS = BM * CPR / NCONV;       // 16-element chunks per converter thread and stage
+constexpr int XPF = KB == 64 ? 2 : 1;        // x stages prefetched ahead in registers
 constexpr int THREADS = NCONV + 64;          // + MMA warp 16 + W producer warp 17
 constexpr int CORR_MAX = 256;                // exact W corrections per expert (more: f64 path)
 constexpr int CORR_SM = 32;                  // of them staged in smem for the epilogue
@@ -88,8 +133,9 @@ static_assert(PM_OFF + (size_t)BM * 4 * 4 <= EPI_END, "epilogue smem");
 static_assert(EX_OFF + (size_t)BM * LGS * 8 <= WC_OFF, "epilogue smem");
 static_assert(LG_OFF + (size_t)BM * LGS * 4 <= EX_OFF, "epilogue smem");
 
+
 struct Ws {
-  uint8_t* wimg;      // [d/128][LW][64 rows x 128 B, swizzled]
+  uint8_t* wimg;      // [d/KB][LW][64 rows x KB B, swizzled]
   int* ew;            // [64] column exponent (biased)
   int* ccnt;          // [64] corrections per expert
   int* ck;            // [64][CORR_MAX] k of each correction (ascending)
@@ -138,6 +184,44 @@ NIMG_DEV uint32_t spread_signed(uint32_t X) {
 // per-byte negation of digits in [0, 127]
 NIMG_DEV uint32_t neg_bytes(uint32_t Y) { return (0x80808080u - Y) ^ 0x80808080u; }
 NIMG_DEV void bar_conv() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+
+// Fast-path digits on the FMA pipe. For an element inside the row's window,
+// X = x * 2^(134 + XW - e_t) is an integer, |X| < 2^(XW+8), and
+//   t3 = fl(X + 1.5*2^44)   rounds X to a multiple of 2^21: D3 = the rounded
+//                           quotient sits in t3's low mantissa bits
+//   r3 = X - (t3 - 1.5*2^44)   exact, |r3| <= 2^20
+// and likewise 2^14, 2^7, 1 for D2, D1, D0: balanced digits in [-64, 64]
+// with X = sum D_i 128^i, each the low byte (two's complement) of its float's
+// bit pattern. Every step is exact (the operands stay inside one binade of
+// the magic constant), so the integer MMA sees exactly X. Two FFMA and eight
+// FADD per element on the FMA pipe, against ~20 ALU-pipe shift / mask / add
+// operations for the integer split (ALU rt = 2/SMSP: that split bounded the
+// kernel, ncu profiles/r02_router_ncu.md).
+template <int LXD>
+NIMG_DEV void digits_fma(float x, float scale, uint32_t (&t)[LXD]) {
+  constexpr float M3 = 26388279066624.0f, M2 = 206158430208.0f, M1 = 1610612736.0f,
+                  M0 = 12582912.0f;   // 1.5 * 2^{44, 37, 30, 23}
+  if (LXD == 4) {
+    const float t3 = fmaf(x, scale, M3);
+    const float r3 = fmaf(x, scale, -(t3 - M3));
+    const float t2 = r3 + M2;
+    const float r2 = r3 - (t2 - M2);
+    const float t1 = r2 + M1;
+    const float r1 = r2 - (t1 - M1);
+    t[0] = __float_as_uint(t3);
+    t[1] = __float_as_uint(t2);
+    t[2] = __float_as_uint(t1);
+    t[3] = __float_as_uint(r1 + M0);
+  } else {
+    const float t2 = fmaf(x, scale, M2);
+    const float r2 = fmaf(x, scale, -(t2 - M2));
+    const float t1 = r2 + M1;
+    const float r1 = r2 - (t1 - M1);
+    t[0] = __float_as_uint(t2);
+    t[1] = __float_as_uint(t1);
+    t[2] = __float_as_uint(r1 + M0);
+  }
+}
 
 // ------------------------------------------------------------------ prep
 // blocks [0, B*KS): t-half partials (shared with the DMMA router).
@@ -207,7 +291,7 @@ router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__
         }
       }
       const int kb = kq / KB, kin = kq % KB;
-      const int off = e * KB + ((((kin >> 4) ^ (e & 7)) << 4) | (kin & 15));
+      const int off = swz_off(e, kin >> 4) | (kin & 15);
 #pragma unroll
       for (int j = 0; j < LW; ++j)
         *reinterpret_cast<uint32_t*>(ws.wimg + (size_t)kb * W_STAGE + j * W_SLICE + off) = dig[j];
@@ -282,6 +366,9 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
   const int rows = (int)(T - t0 < BM ? T - t0 : BM);
   const int nkb = d / KB;
   pdl_trigger();
+  const bool trace = NIMG_I8_TRACE && (blockIdx.x == 0 || blockIdx.x == 64);
+  __shared__ uint64_t trs[48];   // trace: 0 start, 1 W past pdl, 2+kb full[kb] (kb < 32), 40.. epilogue
+  if (trace && tid == 0) trs[0] = gtimer();
 
   if (tid == 0) {
     for (int s = 0; s < NSTAGE; ++s) { mbar_init(&full[s], NCONV + 1); mbar_init(&empty[s], 1); }
@@ -297,19 +384,20 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
 
   if (warp < NCONV / 32) {
     // ---------------------------------------------- converters
-    // job = tid + 512 jj: tile row job / 8, 16-element chunk job % 8 of the stage
-    const bf16* src[2];
-    bool rv[2];
+    // job = tid + 512 jj: tile row job / CPR, 16-element chunk job % CPR of the stage
+    const bf16* src[JOBS];
+    bool rv[JOBS];
 #pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
-      const int job = tid + NCONV * jj, r = job >> 3, c = job & 7;
+    for (int jj = 0; jj < JOBS; ++jj) {
+      const int job = tid + NCONV * jj, r = job / CPR, c = job % CPR;
       rv[jj] = r < rows;
       src[jj] = x + (t0 + (rv[jj] ? r : 0)) * d + c * 16;
     }
-    uint4 cur[4], nxt[4];
-    auto load = [&](int kb, uint4 (&buf)[4]) {
+    // x ring in registers: stage kb sits in xr[kb % (XPF + 1)]
+    uint4 xr[XPF + 1][2 * JOBS];
+    auto load = [&](int kb, uint4 (&buf)[2 * JOBS]) {
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
+      for (int jj = 0; jj < JOBS; ++jj) {
         if (rv[jj]) {
           const uint4* p = reinterpret_cast<const uint4*>(src[jj] + kb * KB);
           buf[2 * jj] = __ldg(p);
@@ -319,36 +407,41 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
         }
       }
     };
-    load(0, cur);
-    // row scale guess from the first stage: the 8 lanes of a row share it
-    int base[2];
-    uint32_t lo7[2], hi7[2];
 #pragma unroll
-    for (int jj = 0; jj < 2; ++jj) {
-      const uint4 a = cur[2 * jj], b = cur[2 * jj + 1];
+    for (int i = 0; i < XPF; ++i)
+      if (i < nkb) load(i, xr[i]);
+    // row scale guess from the first stage: the CPR lanes of a row share it
+    int base[JOBS];
+    uint32_t lo7[JOBS], hi7[JOBS];
+    float xscale[JOBS];   // 2^(134 + XW - e_t): x -> X on the fast path
+    bool sok[JOBS];       // the scale is a normal float (else: integer path)
+#pragma unroll
+    for (int jj = 0; jj < JOBS; ++jj) {
+      const uint4 a = xr[0][2 * jj], b = xr[0][2 * jj + 1];
       uint32_t m = __vmaxu2(__vmaxu2(__vmaxu2(a.x & 0x7FFF7FFFu, a.y & 0x7FFF7FFFu),
                                      __vmaxu2(a.z & 0x7FFF7FFFu, a.w & 0x7FFF7FFFu)),
                             __vmaxu2(__vmaxu2(b.x & 0x7FFF7FFFu, b.y & 0x7FFF7FFFu),
                                      __vmaxu2(b.z & 0x7FFF7FFFu, b.w & 0x7FFF7FFFu)));
       m = max(m & 0xFFFFu, m >> 16);
-      m = max(m, __shfl_xor_sync(0xffffffffu, m, 1));
-      m = max(m, __shfl_xor_sync(0xffffffffu, m, 2));
-      m = max(m, __shfl_xor_sync(0xffffffffu, m, 4));
+#pragma unroll
+      for (int o = 1; o < CPR; o <<= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
       const int eg = min(max((int)(m >> 7), 1), 254) + XH;
       base[jj] = XW - eg;
+      sok[jj] = NIMG_I8_FCONV && eg >= XW + 8 && eg <= XW + 260;
+      xscale[jj] = __uint_as_float((uint32_t)(sok[jj] ? 261 + XW - eg : 127) << 23);
       lo7[jj] = (uint32_t)max(eg - XW, 1) << 7;
       hi7[jj] = (uint32_t)min(eg, 254) << 7;
-      if ((tid & 7) == 0) emax_s[(tid + NCONV * jj) >> 3] = eg;
+      if ((tid % CPR) == 0) emax_s[(tid + NCONV * jj) / CPR] = eg;
     }
     int stage = 0;
     uint32_t phase = 0;
-    for (int kb = 0; kb < nkb; ++kb) {
-      if (kb + 1 < nkb) load(kb + 1, nxt);
+    // one stage: convert x stage kb (registers `cur`) into the smem digit planes
+    auto convert = [&](int kb, const uint4 (&cur)[2 * JOBS]) {
       mbar_wait(&empty[stage], phase ^ 1);
       uint8_t* sa = sm + (size_t)stage * STAGE;
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const int job = tid + NCONV * jj, r = job >> 3, c = job & 7;
+      for (int jj = 0; jj < (NIMG_I8_PROBE == 1 ? 0 : JOBS); ++jj) {
+        const int job = tid + NCONV * jj, r = job / CPR, c = job % CPR;
         const uint32_t wv[8] = {cur[2 * jj].x,     cur[2 * jj].y,     cur[2 * jj].z,     cur[2 * jj].w,
                                 cur[2 * jj + 1].x, cur[2 * jj + 1].y, cur[2 * jj + 1].z, cur[2 * jj + 1].w};
         // all 16 exponents inside [elo, ehi] (no zero / subnormal / inf / nan):
@@ -360,6 +453,23 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
           mxe = __vmaxu2(mxe, wv[i] & 0x7F807F80u);
         }
         const bool fast = min(mn & 0xFFFFu, mn >> 16) >= lo7[jj] && max(mxe & 0xFFFFu, mxe >> 16) <= hi7[jj];
+        uint32_t out[LX][4];
+        if (fast && sok[jj]) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint32_t tb[4][LX];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t w = wv[2 * g + (q >> 1)];
+              const float xv = __uint_as_float((q & 1) ? (w & 0xFFFF0000u) : (w << 16));
+              digits_fma<LX>(xv, xscale[jj], tb[q]);
+            }
+#pragma unroll
+            for (int i = 0; i < LX; ++i)   // plane i: byte 0 of the four elements' digit i
+              out[i][g] = __byte_perm(__byte_perm(tb[0][i], tb[1][i], 0x0040),
+                                      __byte_perm(tb[2][i], tb[3][i], 0x0040), 0x5410);
+          }
+        } else {
         uint32_t Y[16];
         if (fast) {
 #pragma unroll
@@ -392,7 +502,6 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
             }
           }
         }
-        uint32_t out[LX][4];
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           // 4x4 byte transpose: out[i] = digit i of elements 4g..4g+3 (byte 3 - i)
@@ -405,7 +514,8 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
           out[LX - 3][g] = __byte_perm(a2, a3, 0x5410);
           if (LX == 4) out[0][g] = __byte_perm(a2, a3, 0x7632);
         }
-        const int off = r * KB + ((c ^ (r & 7)) << 4);
+        }
+        const int off = swz_off(r, c);
 #pragma unroll
         for (int i = 0; i < LX; ++i)
           *reinterpret_cast<uint4*>(sa + i * A_SLICE + off) =
@@ -413,15 +523,28 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
       }
       fence_proxy_async_smem();
       mbar_arrive(&full[stage]);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) cur[i] = nxt[i];
       if (++stage == NSTAGE) { stage = 0; phase ^= 1; }
+    };
+    // the loop is unrolled by the ring length so every ring index is static
+    // (registers, not local memory)
+    for (int kb0 = 0; kb0 < nkb; kb0 += XPF + 1) {
+#pragma unroll
+      for (int u = 0; u <= XPF; ++u) {
+        const int kb = kb0 + u;
+        if (kb < nkb) {
+          if (kb + XPF < nkb) load(kb + XPF, xr[(u + XPF) % (XPF + 1)]);
+          convert(kb, xr[u]);
+        }
+      }
     }
 
     // ---------------------------------------------- epilogue
     mbar_wait(tfull, 0);
+    if constexpr (NIMG_I8_PROBE != 3) {   // (timing probe 3: no epilogue)
     tc_fence_after();
+    if (trace && tid == 0) trs[40] = gtimer();
     pdl_wait();   // prep outputs (t-bias partials, scales, corrections)
+    if (trace && tid == 0) trs[41] = gtimer();
     const int64_t b_first = t0 / S;
     const int nb = (int)((t0 + rows - 1) / S - b_first + 1);
     double* tbs = reinterpret_cast<double*>(sm + TBS_OFF);
@@ -441,6 +564,7 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
     }
     if (tid < NE) { wcn[tid] = __ldg(ws.ccnt + tid); wew[tid] = __ldg(ws.ew + tid); }
     bar_conv();
+    if (trace && tid == 0) trs[43] = gtimer();
 
     const int q = warp & 3, p = warp >> 2;   // TMEM lane quadrant, 16-expert quarter
     const int r = q * 32 + lane;
@@ -463,6 +587,9 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
 #pragma unroll
       for (int s = 0; s < NG; ++s) tmem_ld4(tl + s * NE + e0, g[s]);
       tmem_ld_wait();
+      // the four logits of this column quad side by side (independent chains)
+      double v4[4], cs4[4], ca4[4];
+      int ncs4[4], cmax = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int e = e0 + j;
@@ -472,20 +599,47 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
         for (int s = 0; s < NG - 4; ++s) H = H * 128 + (int64_t)(int)g[s][j];
         const int64_t L = (int64_t)(int)g[NG - 4][j] * 2097152 + (int64_t)(int)g[NG - 3][j] * 16384 +
                           (int64_t)(int)g[NG - 2][j] * 128 + (int64_t)(int)g[NG - 1][j];
-        const double v = fma((double)H, 268435456.0, (double)L) * pow2(er + wew[e] - 295 - XW);
-        double cs = 0.0, ca = 0.0;
-        const int ncw = wcn[e];
-        for (int c = 0; c < ncw; ++c) {   // x~ * (w - w~): x~ = 0 for the row's listed elements
-          const bool in_sm = c < CORR_SM;
-          const int kc = in_sm ? wck[e * CORR_SM + c] : __ldg(ws.ck + e * CORR_MAX + c);
-          const double dwc = in_sm ? wcd[e * CORR_SM + c] : __ldg(ws.cdw + e * CORR_MAX + c);
-          const uint32_t u = __bfloat16_as_ushort(xrow[kc]);
-          const int e8 = (int)((u >> 7) & 0xFFu), sh = e8 + XW - er;
-          const bool special = ((unsigned)sh > (unsigned)XW) | ((unsigned)(e8 - 1) > 253u);
-          const double pr = special ? 0.0 : (double)__uint_as_float(u << 16) * dwc;
-          cs += pr;
-          ca += fabs(pr);
+        v4[j] = fma((double)H, 268435456.0, (double)L) * pow2(er + wew[e] - 295 - XW);
+        cs4[j] = 0.0;
+        ca4[j] = 0.0;
+        ncs4[j] = wcn[e];
+        cmax = max(cmax, ncs4[j]);
+      }
+      // W corrections x~ * (w - w~) (x~ = 0 for the row's listed elements): the
+      // four logits' x loads are issued together, then consumed
+      for (int c = 0; c < cmax; ++c) {
+        uint32_t u4[4];
+        double dw4[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          u4[j] = 0u;
+          dw4[j] = 0.0;
+          if (c < ncs4[j]) {
+            const int e = e0 + j;
+            const bool in_sm = c < CORR_SM;
+            const int kc = in_sm ? wck[e * CORR_SM + c] : __ldg(ws.ck + e * CORR_MAX + c);
+            dw4[j] = in_sm ? wcd[e * CORR_SM + c] : __ldg(ws.cdw + e * CORR_MAX + c);
+            u4[j] = __bfloat16_as_ushort(xrow[kc]);
+          }
         }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (c < ncs4[j]) {
+            const uint32_t u = u4[j];
+            const int e8 = (int)((u >> 7) & 0xFFu), sh = e8 + XW - er;
+            const bool special = ((unsigned)sh > (unsigned)XW) | ((unsigned)(e8 - 1) > 253u);
+            const double pr = special ? 0.0 : (double)__uint_as_float(u << 16) * dw4[j];
+            cs4[j] += pr;
+            ca4[j] += fabs(pr);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int e = e0 + j;
+        const double v = v4[j];
+        double cs = cs4[j], ca = ca4[j];
+        const int ncw = wcn[e];
         for (int c = 0; c < nxu; ++c) {   // (x - x~) * w for the listed elements
           const double pr = (double)xcv[r * XC_MAX + c] * (double)__ldg(w_r + (int64_t)xck[r * XC_MAX + c] * NE + e);
           cs += pr;
@@ -508,9 +662,11 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
         pm = fmaxf(pm, rf);
       }
     }
+    if (trace && tid == 0) trs[45] = gtimer();
     if (fl && valid) atomicOr(&rflag_s[r], 1);
     pmx[r * 4 + p] = pm;
     bar_conv();
+    if (trace && tid == 0) trs[42] = gtimer();
     // numpy-order softmax over the 64 experts (tensor.py:467-479): the four
     // threads of a row compute the same max and sum; each writes its 16
     const double mxv = (double)fmaxf(fmaxf(pmx[r * 4], pmx[r * 4 + 1]), fmaxf(pmx[r * 4 + 2], pmx[r * 4 + 3]));
@@ -536,6 +692,8 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
                             lgs[r * LGS + p * 16 + 4 * i + 2], lgs[r * LGS + p * 16 + 4 * i + 3]);
       if (p == 0 && rflag_s[r]) ws.list[atomicAdd(ws.counter, 1u)] = (int)t;
     }
+    if (trace && tid == 0) trs[44] = gtimer();
+    }
   } else if (warp == NCONV / 32) {
     // ---------------------------------------------- MMA issuer
     if (lane == 0) {
@@ -548,19 +706,22 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
       uint32_t phase = 0;
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full[stage], phase);
+        if (trace && kb < 38) trs[2 + kb] = gtimer();
         tc_fence_after();
         const uint32_t sa = smem_u32(sm + (size_t)stage * STAGE);
         const uint32_t sw = sa + LX * A_SLICE;
-        const uint64_t b03 = make_sdesc_k128(sw);
-        const uint64_t b4 = make_sdesc_k128(sw + 4 * W_SLICE);
+        const uint64_t b03 = sdesc_k(sw);
+        const uint64_t b4 = sdesc_k(sw + 4 * W_SLICE);
 #pragma unroll
         for (int kk = 0; kk < KB / 32; ++kk) {
           const bool first = kb == 0 && kk == 0;
 #pragma unroll
           for (int i = 0; i < LX; ++i) {
-            const uint64_t adesc = make_sdesc_k128(sa + i * A_SLICE) + 2 * kk;
-            umma_i8(tmem_base + i * NE, adesc, b03 + 2 * kk, idesc256, (first && i == 0) ? 0u : 1u);
-            umma_i8(tmem_base + (i + 4) * NE, adesc, b4 + 2 * kk, idesc64, first ? 0u : 1u);
+            const uint64_t adesc = sdesc_k(sa + i * A_SLICE) + 2 * kk;
+            if (NIMG_I8_PROBE != 2) {
+              umma_i8(tmem_base + i * NE, adesc, b03 + 2 * kk, idesc256, (first && i == 0) ? 0u : 1u);
+              umma_i8(tmem_base + (i + 4) * NE, adesc, b4 + 2 * kk, idesc64, first ? 0u : 1u);
+            }
           }
         }
         umma_commit(&empty[stage]);
@@ -572,6 +733,7 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
     // ---------------------------------------------- W digit producer
     if (lane == 0) {
       pdl_wait();   // the prep kernel wrote the digit image
+      if (trace) trs[1] = gtimer();
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = 0; kb < nkb; ++kb) {
@@ -588,6 +750,16 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
   if (warp == NCONV / 32) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
+  }
+  if (trace && tid == 0) {
+    const double t0s = (double)trs[0];
+    printf("ri8 cta %d (us): Wpdl %.1f | full kb0 %.1f kb1 %.1f kb2 %.1f kb3 %.1f kb8 %.1f kb16 %.1f kb24 %.1f kbL %.1f | "
+           "tfull %.1f pdl %.1f setup %.1f thr0 %.1f logits %.1f end %.1f\n", (int)blockIdx.x, (trs[1] - t0s) * 1e-3,
+           (trs[2] - t0s) * 1e-3, (trs[3] - t0s) * 1e-3, (trs[4] - t0s) * 1e-3, (trs[5] - t0s) * 1e-3,
+           (trs[10] - t0s) * 1e-3, (trs[18] - t0s) * 1e-3, (trs[26] - t0s) * 1e-3,
+           (trs[1 + nkb] - t0s) * 1e-3, (trs[40] - t0s) * 1e-3, (trs[41] - t0s) * 1e-3,
+           (trs[43] - t0s) * 1e-3, (trs[45] - t0s) * 1e-3,
+           (trs[42] - t0s) * 1e-3, (trs[44] - t0s) * 1e-3);
   }
 }
 

@@ -36,7 +36,7 @@ def _inputs(B, S, d, E, h, seed, dev):
                 sw3=tn(h, d, std=0.02).to(bf), sw2=tn(d, h, std=0.02).to(bf))
 
 
-def _worker(rank, world, port, q, shape, modes=("plain", "nccl", "ce")):
+def _worker(rank, world, port, q, shape, modes=("plain", "nccl", "ce"), oracle=False):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     ngpu = torch.cuda.device_count()
@@ -72,17 +72,28 @@ def _worker(rank, world, port, q, shape, modes=("plain", "nccl", "ce")):
                 torch.cuda.synchronize()
                 ok = ok and bool(torch.equal(out, full[sl]))
             res[mode] = ok
+        if oracle:
+            # this rank's samples of the EP output against the CPU oracle
+            # (moe.py:138-164 restated), per sample
+            from oracle import nimg_oracle as O
+            f = lambda t: t.float().cpu().numpy()
+            ref = O.moe_forward(f(a["x_norm"][sl]), f(a["x_mod"][sl]), f(a["t_emb"][sl]), f(a["w_r"]),
+                                *(f(a[k]) for k in ("w1", "w3", "w2", "sw1", "sw3", "sw2")),
+                                capacity_factor=C)
+            o = f(out)
+            res["oracle_rel_err"] = [float(np.linalg.norm(o[i] - ref[i]) / np.linalg.norm(ref[i]))
+                                     for i in range(o.shape[0])]
         q.put((rank, res))
         dist.barrier()
     finally:
         dist.destroy_process_group()
 
 
-def _run(world, shape, modes=("plain", "nccl", "ce")):
+def _run(world, shape, modes=("plain", "nccl", "ce"), oracle=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shape, modes))
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, shape, modes, oracle))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -117,17 +128,23 @@ def test_ep_loopback_bitwise(shape):
 def test_ep_two_gpus_bitwise():
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
-    res = _run(2, (4, 1024, 2048, 64, 1344, 4.0))
+    res = _run(2, (4, 1024, 2048, 64, 1344, 4.0), oracle=True)
+    print("EP2 per-sample rel-err vs oracle:", {r: res[r]["oracle_rel_err"] for r in res})
     for r in range(2):
+        errs = res[r].pop("oracle_rel_err")
+        assert max(errs) <= 2e-2, errs
         assert res[r] == {"plain": True, "nccl": True, "ce": True}, res
 
 
 def test_ep_four_gpus_bitwise():
     if torch.cuda.device_count() < 4:
         pytest.skip("needs 4 GPUs")
-    res = _run(4, (4, 1024, 2048, 64, 1344, 4.0), modes=("ce",))
+    res = _run(4, (4, 1024, 2048, 64, 1344, 4.0), modes=("ce", "nccl"), oracle=True)
+    print("EP4 per-sample rel-err vs oracle:", {r: res[r]["oracle_rel_err"] for r in res})
     for r in range(4):
-        assert res[r] == {"ce": True}, res
+        errs = res[r].pop("oracle_rel_err")
+        assert max(errs) <= 2e-2, errs
+        assert res[r] == {"ce": True, "nccl": True}, res
 
 
 @pytest.mark.parametrize("world", [4, 8])
