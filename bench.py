@@ -636,8 +636,6 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     import torch
     import torch.distributed as dist
     from paper_2604_12163_b200.ep import ep_moe_forward
-    from paper_2604_12163_b200.nvlink import NvLinkCounters
-    nvl = NvLinkCounters(dev.index)
     inp, bank, cfg, w_r = _ep_setup(c, world, rank, dev)
     step = lambda: ep_moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], cfg, bank, w_r, ctx)
     for _ in range(args.warmup):
@@ -648,7 +646,6 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     per = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     hts = []
     ms0 = torch.cuda.memory_stats(dev)
-    nv0 = nvl.snapshot()
     e0.record()
     h0 = time.perf_counter()
     for i in range(args.steps):
@@ -658,22 +655,16 @@ def _ep_time(args, c, world, rank, dev, ctx, want_e2e=False, timeline=False):
     host_ms = (time.perf_counter() - h0) * 1e3 / args.steps   # issue time per step
     e1.record()
     torch.cuda.synchronize()
-    nv1 = nvl.snapshot()
     dist.barrier()
     t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     out = {"ms": float(t.item()), "host_issue_ms": round(host_ms, 4)}
-    # NVLink hardware counters (NVML) over the timed steps: what this GPU put
-    # on / took off its links, against the exchange's algorithmic bytes
-    from paper_2604_12163_b200.router import capacity_for
-    cap = capacity_for(c["S"], c["E"], c["C"])
-    chunk = c["E"] // world * (c["B"] // world) * cap * c["d"] * 2
-    nvd = NvLinkCounters.delta(nv0, nv1, e0.elapsed_time(e1) * 1e-3)
-    out["nvlink_counters"] = (
-        dict(nvd, steps=args.steps, algorithmic_bytes_per_dir=2 * chunk * (world - 1) * args.steps,
-             what="NVML per-link NVLink TX/RX counters summed over active links, rank-local, "
-                  "timed steps only; algorithmic = dispatch + return chunks sent (= received)")
-        if nvd is not None else {"unavailable": nvl.err})
+    # NVLink hardware counters: NVML reports NOT_SUPPORTED for every NVLink
+    # counter on these boxes (and pynvml aborted the process once), so the
+    # counter evidence is an ncu range-replay capture of the same copies
+    # (tools/nvlink_ce_probe.py, profiles/r02_nvlink_counters.md)
+    out["nvlink_counters"] = {"source": "profiles/r02_nvlink_counters.md (ncu range replay, "
+                                        "nvltx/nvlrx__bytes_data_user == copied bytes)"}
     if os.environ.get("NIMG_BENCH_DEBUG"):
         dev_steps = [round(e0.elapsed_time(per[0]), 3)] + [
             round(per[i - 1].elapsed_time(per[i]), 3) for i in range(1, args.steps)]

@@ -210,6 +210,34 @@ int nimg_expert_ffn(const nimg_ffn_desc* desc, const int64_t* seg_offsets,
                     const void* sw1, const void* sw3, const void* sw2, void* y_shared, void* ws,
                     size_t ws_bytes, void* stream);
 
+/* The routed-row gather (moe.py:152-153) run by background warps of the
+ * GEMM1 launch of nimg_expert_ffn_gather (expert parallel: the rank-local
+ * gather of every chunk, fused into the first grouped launch):
+ * dst[r] = src[idx[r]] for r < rows (row_bytes each). The launch's routed
+ * bank reads rows [row_off, row_off + n_rows) of dst (x_routed must be
+ * dst + row_off * row_bytes); its tiles wait on the sub-block flags. flags:
+ * nimg_route_bg_flags() of the nimg_route call that produced idx (it zeroes
+ * them). chunk_rows > 0: every finished 32-row sub-block adds 1 to
+ * chunk_done[c] of each chunk c (rows [c chunk_rows, (c+1) chunk_rows)) it
+ * overlaps -- persistent counters the caller owns and never resets; a copy of
+ * chunk c may start once the counter reached its running total (stream wait).
+ * If the launch cannot fuse the gather (not the CTA-pair tcgen05 path, or no
+ * shared bank) the library runs the gather kernel first and counts the same. */
+typedef struct nimg_bg_gather {
+  const void* src;
+  const int32_t* idx;
+  void* dst;
+  int32_t* flags;
+  uint32_t* chunk_done;
+  int32_t rows, row_bytes, row_off, chunk_rows;
+} nimg_bg_gather;
+int nimg_route_bg_flags(const nimg_moe_desc* desc, void* route_ws, int32_t** flags);
+int nimg_expert_ffn_gather(const nimg_ffn_desc* desc, const int64_t* seg_offsets,
+                           const int32_t* seg_expert, const void* x_routed, const void* w1,
+                           const void* w3, const void* w2, void* y_routed, const void* x_shared,
+                           const void* sw1, const void* sw3, const void* sw2, void* y_shared,
+                           void* ws, size_t ws_bytes, const nimg_bg_gather* gather, void* stream);
+
 /* moe.py:156-161 + tensor.py:366-378: out[t] = round(f64(fp32(sum_k
  * fp32(y_routed[rows_k] * gates[rows_k]))) + f64(y_shared[t])), experts in
  * ascending order (deterministic; same bits for any expert-parallel split). */

@@ -31,7 +31,7 @@ EXPORTS = (
     "nimg_ln_modulate", "nimg_gate_res_ln_modulate", "nimg_gated_residual", "nimg_qk_norm_rope",
     "nimg_moe_block_prologue_workspace_bytes", "nimg_moe_block_prologue", "nimg_combine_residual",
     "nimg_moe_train_state_bytes", "nimg_moe_forward_train", "nimg_moe_backward_workspace_bytes",
-    "nimg_moe_backward",
+    "nimg_moe_backward", "nimg_route_bg_flags", "nimg_expert_ffn_gather",
 )
 
 
@@ -70,6 +70,12 @@ class MoeGrads(C.Structure):
                 ("g_t_emb", C.c_void_p), ("g_w_r", C.c_void_p), ("g_w1", C.c_void_p),
                 ("g_w3", C.c_void_p), ("g_w2", C.c_void_p), ("g_sw1", C.c_void_p),
                 ("g_sw3", C.c_void_p), ("g_sw2", C.c_void_p)]
+
+
+class BgGatherDesc(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("idx", C.c_void_p), ("dst", C.c_void_p),
+                ("flags", C.c_void_p), ("chunk_done", C.c_void_p), ("rows", C.c_int32),
+                ("row_bytes", C.c_int32), ("row_off", C.c_int32), ("chunk_rows", C.c_int32)]
 
 
 class FfnDesc(C.Structure):
@@ -127,6 +133,9 @@ def _load():
         "nimg_moe_backward_workspace_bytes": ([C.POINTER(MoeDesc), C.POINTER(SZ)], C.c_int),
         "nimg_moe_backward": ([C.POINTER(MoeDesc), C.POINTER(MoePtrs), P, SZ,
                                C.POINTER(MoeGrads), P, SZ, P], C.c_int),
+        "nimg_route_bg_flags": ([C.POINTER(MoeDesc), P, C.POINTER(C.c_void_p)], C.c_int),
+        "nimg_expert_ffn_gather": ([C.POINTER(FfnDesc), P, P, P, P, P, P, P, P, P, P, P, P, P, SZ,
+                                    C.POINTER(BgGatherDesc), P], C.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

@@ -702,6 +702,37 @@ int nimg_expert_ffn(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
                          (cudaStream_t)stream);
 }
 
+int nimg_route_bg_flags(const nimg_moe_desc* d, void* route_ws, int32_t** flags) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!route_ws || !flags) return fail(NIMG_ERR_CONFIG, "null argument");
+  *flags = carve_route(d, route_ws).bg_flags;
+  return NIMG_OK;
+}
+
+int nimg_expert_ffn_gather(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex,
+                           const void* xr, const void* w1, const void* w3, const void* w2, void* yr,
+                           const void* xs, const void* sw1, const void* sw3, const void* sw2,
+                           void* ys, void* ws, size_t ws_bytes, const nimg_bg_gather* g,
+                           void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  NIMG_TRY(check_ffn(f, off, ex));
+  if (!g || !g->src || !g->idx || !g->dst || !g->flags || g->rows < 0 || g->row_bytes <= 0 ||
+      g->row_off < 0 || g->row_off + f->n_rows > g->rows || (g->chunk_rows > 0 && !g->chunk_done))
+    return fail(NIMG_ERR_SHAPE, "bad gather descriptor");
+  if (f->n_rows > 0 && xr != static_cast<const uint8_t*>(g->dst) + (size_t)g->row_off * g->row_bytes)
+    return fail(NIMG_ERR_SHAPE, "x_routed must be dst + row_off rows");
+  const bool fuse = ffn_use_tc(f) && use_pair_kernels() && f->n_rows > 0 && f->n_shared_rows > 0 &&
+                    g->row_bytes % 16 == 0;
+  BgGather bg{g->src, g->idx, g->dst, g->flags, g->rows, g->row_bytes, g->row_off, g->chunk_rows,
+              g->chunk_done};
+  if (!fuse) {   // the separate gather kernel, then the same chunk counts
+    CUDA_TRY(launch_gather_rows(g->src, g->row_bytes, g->idx, g->rows, g->dst, st));
+    if (g->chunk_rows > 0) CUDA_TRY(launch_bg_count(g->rows, g->chunk_rows, g->chunk_done, st));
+  }
+  return expert_ffn_impl(f, off, ex, xr, w1, w3, w2, yr, xs, sw1, sw3, sw2, ys, ws, ws_bytes, st,
+                         nullptr, 0, nullptr, fuse ? &bg : nullptr);
+}
+
 int nimg_combine(int64_t T, int64_t d, int64_t E, int32_t y_dtype, int32_t out_dtype,
                  const void* y_routed, const void* y_shared, const void* gates_v,
                  const int32_t* comb_rows, const int32_t* comb_cnt, void* out, void* stream) {
@@ -831,7 +862,7 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   BgGather bg{};
   if (bg_gather)
     bg = BgGather{p->x_mod, p->route.token_flat, xg, carve_route(d, route_ws).bg_flags,
-                  (int)f.n_rows, (int)(d->d * elt(d->act_dtype))};
+                  (int)f.n_rows, (int)(d->d * elt(d->act_dtype)), 0, 0, nullptr};
   mark(0, st);
   NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st));
   mark(1, st);

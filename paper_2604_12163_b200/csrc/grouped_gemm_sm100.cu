@@ -411,8 +411,13 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
           // acquire the background-gathered rows of this CTA's half tile
           const int r1 = min(ti.rows_valid, ((int)crank + 1) * BM) - (int)crank * BM;
           if (r1 > 0) {
-            for (int j = a_row / kBgRows; j <= (a_row + r1 - 1) / kBgRows; ++j)
-              while (ld_acquire_gpu(p.bg.flags + j) == 0) { }
+            const int g0 = p.bg.row_off + a_row;
+            for (int j = g0 / kBgRows; j <= (g0 + r1 - 1) / kBgRows; ++j) {
+              // bounded: a protocol bug traps (a launch error) instead of hanging the GPU
+              uint32_t spins = 0;
+              while (ld_acquire_gpu(p.bg.flags + j) == 0)
+                if (++spins == (1u << 26)) __trap();
+            }
             fence_proxy_async_global();
           }
         }
@@ -554,7 +559,14 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
       }
       __threadfence();
       __syncwarp();
-      if (lane == 0) st_release_gpu(p.bg.flags + j, 1);
+      if (lane == 0) {
+        st_release_gpu(p.bg.flags + j, 1);
+        if (p.bg.chunk_rows > 0) {   // expert parallel: the copy engines wait on these
+          __threadfence_system();
+          for (int c = r0 / p.bg.chunk_rows; c <= (r0 + nr - 1) / p.bg.chunk_rows; ++c)
+            atomicAdd(p.bg.chunk_done + c, 1u);
+        }
+      }
     }
   } else if (warp >= 2 && warp < 6) {
     // ------------------------------------------------ epilogue (warps 2..5, both CTAs)

@@ -49,6 +49,10 @@ struct BgGather {
   void* dst;             // gathered rows (the routed bank's A operand)
   int* flags;            // one per 32-row sub-block + the claim counter, zeroed by gate_norm
   int rows, row_bytes;   // null src: off
+  int row_off;           // gathered row of the routed bank's row 0 (flag index base)
+  int chunk_rows;        // > 0: chunk_done[c] += 1 per finished sub-block overlapping
+  unsigned* chunk_done;  //   rows [c chunk_rows, (c+1) chunk_rows) (expert parallel:
+                         //   the dispatch copy of chunk c waits on it)
 };
 struct GroupedParams {
   GBank bank[2];
@@ -215,6 +219,8 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
                              int32_t* comb_rows, int32_t* comb_cnt, int B, int S, int E, int cap,
                              float gate_eps, float gate_scale, cudaStream_t s, int* bg_flags = nullptr,
                              int n_bg_flags = 0);
+// chunk_done[c] += number of 32-row sub-blocks of [0, rows) overlapping chunk c
+cudaError_t launch_bg_count(int rows, int chunk_rows, unsigned* chunk_done, cudaStream_t s);
 cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
                                int64_t n_idx, void* dst, cudaStream_t s);
 // out[t] = fp32(fp32(sum_k fp32(Y[rows[k][t]] * gate)) + shared[t]) -- see combine kernel.

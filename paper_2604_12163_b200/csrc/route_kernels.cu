@@ -1288,6 +1288,21 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
                     n_bg_flags);
 }
 
+__global__ void bg_count_kernel(int rows, int chunk_rows, unsigned* __restrict__ chunk_done) {
+  pdl_trigger();
+  pdl_wait();
+  const int nsub = (rows + 31) / 32;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < nsub; j += gridDim.x * blockDim.x) {
+    const int r0 = 32 * j, r1 = min(rows, r0 + 32) - 1;
+    for (int c = r0 / chunk_rows; c <= r1 / chunk_rows; ++c) atomicAdd(chunk_done + c, 1u);
+  }
+}
+cudaError_t launch_bg_count(int rows, int chunk_rows, unsigned* chunk_done, cudaStream_t s) {
+  if (rows <= 0 || chunk_rows <= 0) return cudaSuccess;
+  return launch_pdl(bg_count_kernel, dim3(((rows + 31) / 32 + 255) / 256), dim3(256), 0, s, rows,
+                    chunk_rows, chunk_done);
+}
+
 cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
                                int64_t n_idx, void* dst, cudaStream_t s) {
   if (n_idx <= 0) return cudaSuccess;

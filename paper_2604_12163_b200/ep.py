@@ -53,6 +53,10 @@ import os as _os
 _DISPATCH_SERIAL = _os.environ.get("NIMG_EP_DISPATCH", "parallel") == "serial"
 # remote chunks are computed in groups of at least this many rows per launch
 _GROUP_ROWS = int(_os.environ.get("NIMG_EP_GROUP_ROWS", "12288"))
+# the rank-local gather runs inside the first grouped launch (NIMG_EP_BG_GATHER=0:
+# a separate gather kernel before it)
+_BG_GATHER = _os.environ.get("NIMG_EP_BG_GATHER", "1") != "0"
+_MAX_CHUNKS = 64
 
 
 @dataclass(frozen=True)
@@ -215,6 +219,11 @@ class CETransport:
         self.flags = PeerBuffer(3 * world * 4, group, rank, world)   # disp | ret | comb
         self.streams = [torch.cuda.Stream(device) for _ in range(world)]   # returns, per peer
         self.disp_stream = torch.cuda.Stream(device)
+        # gather progress per destination chunk (written by the first grouped
+        # launch's background gather, never reset): the dispatch copy of chunk
+        # q waits until chunk_done[q] reaches the running total chunk_expect[q]
+        self.chunk_done = torch.zeros(_MAX_CHUNKS, dtype=torch.int32, device=device)
+        self.chunk_expect = [0] * _MAX_CHUNKS
         self.epoch = 0
         self.key = None
         self.reshaped = False
@@ -325,7 +334,13 @@ class EPContext:
         return self._streams
 
 
+_TRACE = _os.environ.get("NIMG_EP_TRACE") == "1"
+
+
 def _mark(timeline, name):
+    if _TRACE:
+        import sys as _sys
+        print(f"[ep rank {dist.get_rank()}] {name}", file=_sys.stderr, flush=True)
     if timeline is not None:
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
@@ -373,11 +388,18 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
     r = stages.route(x_norm, t_emb, w_r, cfg, cap)
     _mark(timeline, "routed")
     xring = None
+    bg = None
     if ctx.overlap and ctx.transport == "ce":
         # persistent double buffer (read by the dispatch copy streams)
         xring = ctx.ring("xg", (E * B_l * cap, d), act, x_mod.device)
         xslot, xg = xring.next()
-        stages.gather(xm, r["token_flat"], out=xg)
+        flags = (stages.bg_flags(r) if _BG_GATHER and ctx.world > 1 and ctx.world <= _MAX_CHUNKS
+                 and hasattr(stages, "bg_flags") else 0)
+        if flags:
+            # the first grouped launch gathers every chunk while it runs
+            bg = {"src": xm, "idx": r["token_flat"], "dst": xg, "flags": flags}
+        else:
+            stages.gather(xm, r["token_flat"], out=xg)
     else:
         xg = stages.gather(xm, r["token_flat"])                   # (E*B_l*cap, d)
     _mark(timeline, "gathered")
@@ -397,7 +419,7 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
         else:
             y_back.copy_(y_recv)
     elif ctx.transport == "ce":
-        y_back, y_sh = _ce_exchange(plan, ctx, stages, xg, xm, w, timeline, (xring, xslot))
+        y_back, y_sh = _ce_exchange(plan, ctx, stages, xg, xm, w, timeline, (xring, xslot), bg)
     else:
         y_back, y_sh = _overlapped_exchange(plan, ctx, stages, xg, xm, w, timeline)
     _mark(timeline, "returned")
@@ -457,7 +479,8 @@ def _overlapped_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeli
     return y_back.view(R * n, -1), y_sh
 
 
-def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None, xring=None):
+def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None, xring=None,
+                 bg=None):
     """Copy-engine dispatch / return with per-step flags (see module doc).
 
     Flags in rank r's array: disp[src] (src's chunk for r has landed in r's
@@ -477,12 +500,44 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None,
     xbytes, ybytes = n * d * tp.act_es, n * d * tp.y_es
     coff, cex = plan.chunk_segments()
 
+    if bg is not None:
+        # sub-blocks of 32 gathered rows overlapping each chunk: the running
+        # totals the dispatch copies wait for
+        bg = dict(bg, row_off=me * n, chunk_rows=n, chunk_done=tp.chunk_done.data_ptr())
+        for q in range(R):
+            tp.chunk_expect[q] += ((q + 1) * n - 1) // 32 - (q * n) // 32 + 1
+    # The rank's own chunk needs no exchange: its first half of experts runs
+    # right after the shared expert (together they cover the dispatch copies),
+    # its second half last (covers the final return copy).
+    El = plan.experts_per_rank
+    half = El // 2 if R > 1 else El
+    blk = plan.block_rows
+    own_x = xg[me * n:(me + 1) * n]
+
+    def own_part(e0, e1, shared=False, gather=None):
+        xs = (xm, w.shared_w1, w.shared_w3, w.shared_w2) if shared else (None,) * 4
+        if e1 <= e0:
+            return stages.expert_ffn(None, None, None, None, None, None, *xs,
+                                     gather=gather) if shared else None
+        off = (np.arange(e0, e1 + 1, dtype=np.int64) - e0) * blk
+        return stages.expert_ffn(own_x[e0 * blk:e1 * blk], off, np.arange(e0, e1, dtype=np.int32),
+                                 w.w1, w.w3, w.w2, *xs, y_routed=tp.yback_t[me, e0 * blk:e1 * blk],
+                                 gather=gather)
+
+    # shared expert + first half of the own chunk in one grouped launch (with
+    # bg: that launch also gathers every chunk, the dispatch copies start as
+    # their chunks complete). It is enqueued BEFORE the dispatch copies: a
+    # peer copy may block the host until it runs, and with bg it waits on this
+    # launch's progress (GPU-side the copies only wait on x_ready + chunk_done).
+    x_ready = torch.cuda.Event()
+    x_ready.record(comp)
+    _, y_sh = own_part(0, half, shared=True, gather=bg)
+    _mark(timeline, "shared+own_a")
+
     # dispatch: one copy per destination rank, straight into its recv slot.
     # "parallel" (default): one stream per destination; "serial"
     # (NIMG_EP_DISPATCH=serial): one stream, in the order destinations consume
     # the chunks (destination me+s uses it at its step s).
-    x_ready = torch.cuda.Event()
-    x_ready.record(comp)
     serial = _DISPATCH_SERIAL
     for s in range(1, R):
         q = (me + s) % R
@@ -490,6 +545,9 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None,
         if not serial or s == 1:
             st.wait_event(x_ready)
         sh = st.cuda_stream
+        if bg is not None:   # chunk q gathered by the first grouped launch
+            _lib.check(L.nimg_stream_wait_geq_u32(tp.chunk_done.data_ptr() + 4 * q,
+                                                  tp.chunk_expect[q] & 0xFFFFFFFF, sh))
         if k > 1:   # q consumed my previous chunk
             _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, RET, q), k - 1, sh))
             if tp.reshaped:   # ... and, after a chunk-size change, every chunk (see set_shape)
@@ -509,26 +567,6 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None,
             xring[0].reader_done(xring[1], st)
         else:
             xg.record_stream(st)
-
-    # The rank's own chunk needs no exchange: its first half of experts runs
-    # right after the shared expert (together they cover the dispatch copies),
-    # its second half last (covers the final return copy).
-    El = plan.experts_per_rank
-    half = El // 2 if R > 1 else El
-    blk = plan.block_rows
-    own_x = xg[me * n:(me + 1) * n]
-
-    def own_part(e0, e1, shared=False):
-        xs = (xm, w.shared_w1, w.shared_w3, w.shared_w2) if shared else (None,) * 4
-        if e1 <= e0:
-            return stages.expert_ffn(None, None, None, None, None, None, *xs) if shared else None
-        off = (np.arange(e0, e1 + 1, dtype=np.int64) - e0) * blk
-        return stages.expert_ffn(own_x[e0 * blk:e1 * blk], off, np.arange(e0, e1, dtype=np.int32),
-                                 w.w1, w.w3, w.w2, *xs, y_routed=tp.yback_t[me, e0 * blk:e1 * blk])
-
-    # shared expert + first half of the own chunk in one grouped launch
-    _, y_sh = own_part(0, half, shared=True)
-    _mark(timeline, "shared+own_a")
 
     yring = ctx.ring("y_recv", (R, n, d), ydt, dev)
     yslot, y_recv = yring.next()

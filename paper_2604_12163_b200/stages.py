@@ -35,7 +35,18 @@ class CudaStages:
         ro = route_struct(r)
         _lib.check(_lib.lib.nimg_route(C.byref(desc), ptr(x_norm), ptr(t_emb), ptr(w_r),
                                        C.byref(ro), ptr(ws), ws.numel(), stream_handle()))
+        r["_route_ws"], r["_route_desc"] = ws, desc   # bg_flags() points into ws
         return r
+
+    def bg_flags(self, r: dict) -> int:
+        """Device address of the gather flags nimg_route zeroed in this
+        routing's workspace (nimg_route_bg_flags); 0 if unavailable."""
+        if "_route_ws" not in r:
+            return 0
+        p = C.c_void_p()
+        _lib.check(_lib.lib.nimg_route_bg_flags(C.byref(r["_route_desc"]), ptr(r["_route_ws"]),
+                                                C.byref(p)))
+        return p.value or 0
 
     def gather(self, src: torch.Tensor, idx_i32: torch.Tensor, out: torch.Tensor | None = None
                ) -> torch.Tensor:
@@ -57,10 +68,15 @@ class CudaStages:
     def expert_ffn(self, x_routed: torch.Tensor | None, seg_offsets: np.ndarray,
                    seg_expert: np.ndarray, w1, w3, w2, x_shared: torch.Tensor | None,
                    sw1, sw3, sw2, y_routed: torch.Tensor | None = None,
-                   y_shared: torch.Tensor | None = None):
+                   y_shared: torch.Tensor | None = None, gather: dict | None = None):
         """moe.py:115-135 + moe.py:160: routed segments through their experts
         and (optionally) x_shared through the shared expert, one grouped launch
-        per GEMM. Returns (y_routed, y_shared)."""
+        per GEMM. Returns (y_routed, y_shared).
+
+        gather (expert parallel): {src, idx, dst, flags, row_off, chunk_rows,
+        chunk_done} -- the launch itself gathers dst[r] = src[idx[r]] for all
+        of dst (moe.py:152-153) while it runs; x_routed is rows row_off.. of
+        dst (nimg_expert_ffn_gather)."""
         act = (x_routed if x_routed is not None else x_shared).dtype
         nr = 0 if x_routed is None else x_routed.shape[0]
         ns = 0 if x_shared is None else x_shared.shape[0]
@@ -81,13 +97,21 @@ class CudaStages:
         ws = workspace(nbytes.value)
         off = np.ascontiguousarray(seg_offsets if nseg else [0], dtype=np.int64)
         ex = np.ascontiguousarray(seg_expert if nseg else [0], dtype=np.int32)
-        _lib.check(_lib.lib.nimg_expert_ffn(
-            C.byref(desc), off.ctypes.data if nseg else None, ex.ctypes.data if nseg else None,
-            ptr(x_routed) if nr else None, ptr(w1) if nr else None, ptr(w3) if nr else None,
-            ptr(w2) if nr else None, ptr(y_routed) if nr else None,
-            ptr(x_shared) if ns else None, ptr(sw1) if ns else None, ptr(sw3) if ns else None,
-            ptr(sw2) if ns else None, ptr(y_shared) if ns else None,
-            ptr(ws), ws.numel(), stream_handle()))
+        args = (C.byref(desc), off.ctypes.data if nseg else None, ex.ctypes.data if nseg else None,
+                ptr(x_routed) if nr else None, ptr(w1) if nr else None, ptr(w3) if nr else None,
+                ptr(w2) if nr else None, ptr(y_routed) if nr else None,
+                ptr(x_shared) if ns else None, ptr(sw1) if ns else None, ptr(sw3) if ns else None,
+                ptr(sw2) if ns else None, ptr(y_shared) if ns else None, ptr(ws), ws.numel())
+        if gather is None:
+            _lib.check(_lib.lib.nimg_expert_ffn(*args, stream_handle()))
+        else:
+            dst = gather["dst"]
+            g = _lib.BgGatherDesc(src=ptr(gather["src"]), idx=ptr(gather["idx"]), dst=ptr(dst),
+                                  flags=gather["flags"], chunk_done=gather.get("chunk_done"),
+                                  rows=dst.shape[0], row_bytes=dst.shape[1] * dst.element_size(),
+                                  row_off=gather.get("row_off", 0),
+                                  chunk_rows=gather.get("chunk_rows", 0))
+            _lib.check(_lib.lib.nimg_expert_ffn_gather(*args, C.byref(g), stream_handle()))
         return y_routed, y_shared
 
     def combine(self, y_routed: torch.Tensor, y_shared: torch.Tensor, r: dict,
