@@ -317,6 +317,9 @@ def run_single(args, c, peaks, peak_kind):
     # ---- training step: forward (keeping the pullback's inputs) + backward
     train = None if args.no_train else run_train(args, c, inp, cfg, bank, tf_peak)
 
+    # ---- the reference's own storage precision: the same layer in fp32 mode
+    fp32 = None if args.no_fp32 else run_fp32(args, c, inp, cfg, bank, ms)
+
     # ---- e2e through the public API with host buffers
     e2e = run_e2e(args, c, inp, cfg, bank)
 
@@ -356,6 +359,7 @@ def run_single(args, c, peaks, peak_kind):
         "stages": stage_detail,
         "block": block,
         "train": train,
+        "fp32_mode": fp32,
         "cpu_baseline": cpu,
         "e2e": e2e,
         # router (prep + scores [+ INT8 fix-up]) + select + gates [+ gather] + GEMM1 + GEMM2 + combine
@@ -576,6 +580,39 @@ def run_block(args, c, inp, cfg, bank, layer_ms):
             "what": "h = x + tanh(sa_gate) r; x_norm = rmsnorm(h)/sqrt(l+1); x_mod = x_norm (1+ff_scale); "
                     "layer; out = h + tanh(ff_gate) moe (one prologue kernel + residual in combine)",
             "prologue_algorithmic_bytes": T * d * 2 * 5}
+
+
+def run_fp32(args, c, inp, cfg, bank, bf16_ms):
+    """The layer in the reference's own storage precision (fp32 activations and
+    weights, no TF32; CUDA-core grouped GEMMs with fp32 accumulation), same
+    workload, same plan API. A few steps: it is ~30x the bf16 step."""
+    import torch
+    from paper_2604_12163_b200 import moe as M
+    f32 = torch.float32
+    a = {k: inp[k].to(f32) for k in ("x_norm", "x_mod")}
+    plan = M.MoEPlan(cfg, M.ExpertBank(*(inp[k].to(f32) for k in ("w1", "w3", "w2", "sw1", "sw3",
+                                                                   "sw2"))),
+                     c["B"], c["S"], f32)
+    f = lambda: plan.forward(a["x_norm"], a["x_mod"], inp["t_emb"], inp["w_r"])
+    f()
+    torch.cuda.synchronize()
+    n = 3
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    wc = work_counts(c)
+    tf = (wc["flops_g1"] + wc["flops_g2"]) / (ms * 1e-3) / 1e12
+    del plan, a
+    torch.cuda.empty_cache()
+    return {"ms_per_step": ms, "tokens_per_s": wc["T"] / (ms * 1e-3),
+            "vs_bf16_step": ms / bf16_ms, "expert_gemm_tflops_upper_bound": tf,
+            "what": "fp32 mode (the reference's storage precision, rel-err <= 1e-4 bar): fp32 "
+                    "inputs and weights, exact f64-accumulated (DMMA) fp32 routing, CUDA-core fp32 grouped "
+                    "GEMMs (no TF32); steps=3"}
 
 
 def run_e2e(args, c, inp, cfg, bank):
@@ -855,6 +892,7 @@ def main():
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the training-step leg")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-mode leg")
     ap.add_argument("--no-overlap", action="store_true", help="EP: plain all-to-alls")
     ap.add_argument("--ep-transport", default="ce", choices=["ce", "nccl"],
                     help="EP exchange: copy engines over NVLink (default) or NCCL")

@@ -53,9 +53,13 @@ import os as _os
 _DISPATCH_SERIAL = _os.environ.get("NIMG_EP_DISPATCH", "parallel") == "serial"
 # remote chunks are computed in groups of at least this many rows per launch
 _GROUP_ROWS = int(_os.environ.get("NIMG_EP_GROUP_ROWS", "12288"))
-# the rank-local gather runs inside the first grouped launch (NIMG_EP_BG_GATHER=0:
-# a separate gather kernel before it)
-_BG_GATHER = _os.environ.get("NIMG_EP_BG_GATHER", "1") != "0"
+# NIMG_EP_BG_GATHER=1: the rank-local gather runs inside the first grouped
+# launch (background warps; the dispatch copies wait on per-chunk completion
+# counters). Off by default: measured equal at EP2 (1.280 vs 1.290 ms weak)
+# and slower at EP4 (1.53 vs 1.39 ms weak): inside the GEMM the gather runs on
+# 2 warps per CTA, so the remote chunks -- and their dispatch copies -- finish
+# later than with the dedicated gather kernel.
+_BG_GATHER = _os.environ.get("NIMG_EP_BG_GATHER", "0") == "1"
 _MAX_CHUNKS = 64
 
 
