@@ -35,8 +35,13 @@ constexpr int kChunk = 64 * BK * 2;            // one {64 MN, 64 K} box = 8 KB
 // 256-M (W modes) tile; each CTA stages its own 128 A rows / M-columns and
 // half of the N columns of B, the leader issues UMMA M=256 (as the forward
 // pair kernel). Per-SM operand traffic per MMA drops by ~1/3.
+// D2: one more warp streams the tile's saved h1 | h3 into shared memory with
+// bulk copies (NIMG_D2_HSTAGE=0: the epilogue loads them from global itself)
+#ifndef NIMG_D2_HSTAGE
+#define NIMG_D2_HSTAGE 1
+#endif
 template <int MODE, bool PAIR> struct Cfg;
-template <> struct Cfg<BWD_D2, false> { static constexpr int BN = 192, STAGES = 5; };
+template <> struct Cfg<BWD_D2, false> { static constexpr int BN = 192, STAGES = NIMG_D2_HSTAGE ? 4 : 5; };
 template <> struct Cfg<BWD_D1, false> { static constexpr int BN = 256, STAGES = 4; };
 template <> struct Cfg<BWD_W2, false> { static constexpr int BN = 192, STAGES = 4; };
 template <> struct Cfg<BWD_W1, false> { static constexpr int BN = 256, STAGES = 4; };
@@ -53,7 +58,14 @@ template <> struct Cfg<BWD_W1, true> { static constexpr int BN = 256, STAGES = 6
 // epilogue warps: 8 for the SwiGLU-derivative epilogue (two warps per TMEM
 // lane quadrant split the column groups), 4 elsewhere
 template <int MODE> constexpr int epi_warps() { return MODE == BWD_D2 ? 8 : 4; }
-template <int MODE> constexpr int threads() { return 64 + 32 * epi_warps<MODE>(); }
+template <int MODE> constexpr bool h_staged() { return MODE == BWD_D2 && NIMG_D2_HSTAGE; }
+template <int MODE> constexpr int threads() { return 64 + 32 * epi_warps<MODE>() + (h_staged<MODE>() ? 32 : 0); }
+// D2 h1 | h3 staging: a slot holds 2 column chunks of 16 (h1 and h3) for the
+// CTA's 128 rows, [chunk][h1|h3][128 rows][16 bf16] = 16 KB; 2 slots
+constexpr int kHChunkBytes = 128 * 16 * 2;
+constexpr int kHSlotBytes = 4 * kHChunkBytes;
+constexpr int kHSlots = 2;
+template <int MODE> constexpr int h_bytes() { return h_staged<MODE>() ? kHSlots * kHSlotBytes : 0; }
 template <int MODE> constexpr bool a_mn() { return MODE == BWD_W2 || MODE == BWD_W1 || MODE == BWD_WR; }
 // per-CTA B columns and their 64-wide TMA boxes (pair: the last box may be
 // partly outside this CTA's half; UMMA reads only BN/2 columns of it)
@@ -64,7 +76,8 @@ template <int MODE, bool PAIR> constexpr int stage_bytes() { return BM * BK * 2 
 constexpr int kStageOut = 4096;
 template <int MODE> constexpr int out_bytes() { return a_mn<MODE>() ? 4 * 2 * kStageOut : 0; }
 template <int MODE, bool PAIR> constexpr int smem_bytes() {
-  return Cfg<MODE, PAIR>::STAGES * stage_bytes<MODE, PAIR>() + out_bytes<MODE>() + 1024 + 256;
+  return Cfg<MODE, PAIR>::STAGES * stage_bytes<MODE, PAIR>() + out_bytes<MODE>() + h_bytes<MODE>() +
+         1024 + 256;
 }
 
 struct Tile {
@@ -132,11 +145,14 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* stage_out = smem + STAGES * SB;                  // W modes: TMA-store staging
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * SB + out_bytes<MODE>());
+  uint8_t* hbuf = stage_out + out_bytes<MODE>();             // D2: staged h1 | h3 slots
+  uint64_t* full = reinterpret_cast<uint64_t*>(hbuf + h_bytes<MODE>());
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* hfull = tempty + 2;                             // D2 staging slots
+  uint64_t* hempty = hfull + kHSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(hempty + kHSlots);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t crank = PAIR ? cluster_ctarank() : 0;
   const bool leader = crank == 0;
@@ -147,6 +163,8 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], (PAIR ? 2 : 1) * EPI); }
+    if (h_staged<MODE>())
+      for (int sl = 0; sl < kHSlots; ++sl) { mbar_init(&hfull[sl], 1); mbar_init(&hempty[sl], EPI); }
     fence_barrier_init();
     for (int b = 0; b < 2; ++b) {
       tma_prefetch_desc(&tm.a[b]);
@@ -230,6 +248,52 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
+  } else if (h_staged<MODE>() && warp == 2 + EPI) {
+    // ------------------------------------------------ D2: h1 | h3 stager (both CTAs, own 128 rows)
+    // The row-blocked h1 | h3 layout (hblk_off) keeps 128 rows x 16 columns of a
+    // chunk contiguous (4 KB), so a CTA's rows of one chunk are 1 bulk copy (2
+    // when they straddle a 128-row block).
+    if (lane == 0) {
+      constexpr int NCH = BN / 16, NG2 = (NCH + 1) / 2;
+      const int rc = (int)crank * BM;
+      int hs = 0; uint32_t hph = 0;
+      for (int t = unit; t < p.total_tiles; t += n_units) {
+        Tile ti; decode<MODE, PAIR>(p, t, ti);
+        const BwdBank& bk = p.bank[ti.bank];
+        const int N = ti.bank ? p.bank[1].N : p.bank[0].N;
+        const int h = ti.bank ? p.bank[1].h : p.bank[0].h;
+        const int nch = h >> 4;
+        const bf16* hb = reinterpret_cast<const bf16*>(bk.aux);
+        const int rv = min(BM, ti.rows_valid - rc);
+        const int64_t R0 = ti.row0 + rc;
+        const int n1 = rv > 0 ? min(rv, 128 - (int)(R0 & 127)) : 0;   // rows in R0's 128-row block
+        for (int g = 0; g < NG2; ++g) {
+          mbar_wait(&hempty[hs], hph ^ 1);
+          uint32_t bytes = 0;
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * g + cc;
+            if (rv > 0 && c < NCH && ti.n0 + 16 * c < N) bytes += 2u * (uint32_t)rv * 32u;
+          }
+          mbar_arrive_expect_tx(&hfull[hs], bytes);
+#pragma unroll
+          for (int cc = 0; cc < 2; ++cc) {
+            const int c = 2 * g + cc;
+            if (!(rv > 0 && c < NCH && ti.n0 + 16 * c < N)) continue;
+#pragma unroll
+            for (int part = 0; part < 2; ++part) {   // h1, h3
+              const int chunk = (ti.n0 >> 4) + c + (part ? nch : 0);
+              uint8_t* dst = hbuf + hs * kHSlotBytes + (cc * 2 + part) * kHChunkBytes;
+              bulk_load(dst, hb + hblk_off(R0, chunk, nch), (uint32_t)n1 * 32u, &hfull[hs]);
+              if (rv > n1)
+                bulk_load(dst + n1 * 32, hb + hblk_off(R0 + n1, chunk, nch), (uint32_t)(rv - n1) * 32u,
+                          &hfull[hs]);
+            }
+          }
+          if (++hs == kHSlots) { hs = 0; hph ^= 1; }
+        }
+      }
+    }
   } else {
     // ------------------------------------------------ epilogue (warps 2..2+EPI, each CTA its 128 rows)
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
@@ -240,12 +304,13 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
     const uint32_t te1 = PAIR ? mapa_shared(smem_u32(&tempty[1]), 0) : 0;
     int acc = 0; uint32_t acc_phase = 0;
     int obuf = 0;   // W modes: staging tile of this warp in use next
+    int hslot = 0; uint32_t hphase = 0;   // D2: staged h1 | h3 slot
     for (int t = unit; t < p.total_tiles; t += n_units) {
       Tile ti; decode<MODE, PAIR>(p, t, ti);
       const BwdBank& bk = p.bank[ti.bank];
       const int N = ti.bank ? p.bank[1].N : p.bank[0].N;   // immediate-offset constant reads
       const int h = ti.bank ? p.bank[1].h : p.bank[0].h;
-      if (MODE == BWD_D2 && t + n_units < p.total_tiles) {
+      if (MODE == BWD_D2 && !h_staged<MODE>() && t + n_units < p.total_tiles) {
         // warm L2 with the next tile's h1 | h3 (row-blocked: one 128-B line per
         // 4 rows and chunk; lanes 0, 4, .. cover this warp's 32 rows)
         Tile nx; decode<MODE, PAIR>(p, t + n_units, nx);
@@ -264,7 +329,57 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
       tc_fence_after();
       const uint32_t tb = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
       const bool rv = rc + r < ti.rows_valid;
-      if constexpr (MODE == BWD_D2) {
+      if constexpr (h_staged<MODE>()) {
+        // chunk pairs staged in shared memory by the stager warp: half h of
+        // the quadrant's two warps takes chunk 2g + h of pair g
+        constexpr int NCH = BN / 16, NG2 = (NCH + 1) / 2;
+        const int64_t row = ti.row0 + rc + r;
+        bf16* o = reinterpret_cast<bf16*>(bk.out) + row * (int64_t)(2 * h);
+#pragma unroll 1
+        for (int g = 0; g < NG2; ++g) {
+          const int c = 2 * g + half;
+          mbar_wait(&hfull[hslot], hphase);
+          if (c < NCH) {
+            uint32_t a[16];
+            tmem_ld16(tb + c * 16, a);
+            tmem_ld_wait();
+            const int n = ti.n0 + c * 16;
+            if (rv && n < N) {
+              const uint8_t* sl = hbuf + hslot * kHSlotBytes + (half * 2) * kHChunkBytes + r * 32;
+              const uint4 v1[2] = {reinterpret_cast<const uint4*>(sl)[0], reinterpret_cast<const uint4*>(sl)[1]};
+              const uint4 v3[2] = {reinterpret_cast<const uint4*>(sl + kHChunkBytes)[0],
+                                   reinterpret_cast<const uint4*>(sl + kHChunkBytes)[1]};
+              float h1[16], h3[16];
+              unpack16(v1, h1);
+              unpack16(v3, h3);
+              uint32_t p1[8], p3[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float g1[2], g3[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                  const int i = 2 * j + u;
+                  const float v = __uint_as_float(a[i]);
+                  const float sig = __fdividef(1.0f, 1.0f + __expf(-h1[i]));
+                  g1[u] = v * h3[i] * sig * (1.0f + h1[i] * (1.0f - sig));
+                  g3[u] = v * h1[i] * sig;
+                }
+                p1[j] = pack_bf16x2(g1[0], g1[1]);
+                p3[j] = pack_bf16x2(g3[0], g3[1]);
+              }
+              uint4* d1 = reinterpret_cast<uint4*>(o + n);
+              uint4* d3 = reinterpret_cast<uint4*>(o + h + n);
+              d1[0] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
+              d1[1] = make_uint4(p1[4], p1[5], p1[6], p1[7]);
+              d3[0] = make_uint4(p3[0], p3[1], p3[2], p3[3]);
+              d3[1] = make_uint4(p3[4], p3[5], p3[6], p3[7]);
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&hempty[hslot]);
+          if (++hslot == kHSlots) { hslot = 0; hphase ^= 1; }
+        }
+      } else if constexpr (MODE == BWD_D2) {
         // groups of G 16-column chunks: every h1 / h3 load of the group is in
         // flight before the first use (the rows are strided: latency-bound otherwise)
         constexpr int G = 3, NCH = BN / 16;
