@@ -14,7 +14,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libnimg_moe.so")
 SOURCES = ["capi.cu", "route_kernels.cu", "grouped_gemm_sm100.cu", "grouped_gemm_simt.cu",
            "block_kernels.cu", "stack_kernels.cu", "backward_kernels.cu",
-           "grouped_gemm_bwd_sm100.cu", "router_i8.cu", "f64_kernels.cu"]
+           "grouped_gemm_bwd_sm100.cu", "router_i8.cu", "f64_kernels.cu", "split_kernels.cu"]
 HEADERS = ["common.cuh", "nimg_internal.h", os.path.join("..", "..", "include", "nimg_moe.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -228,6 +228,45 @@ RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   return r;
 }
 
+bool use_pair_kernels();
+// fp32 mode on the bf16 tensor cores (split_kernels.cu, "bf16x3"): fp32
+// layers whose widths tile the tcgen05 pair kernels; NIMG_FP32_TC=0 keeps the
+// CUDA-core fp32 GEMMs
+bool ffn_use_x3(const nimg_ffn_desc* f) {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_FP32_TC");
+    return !(e && e[0] == '0');
+  }();
+  if (!on || f->act_dtype != NIMG_F32 || !use_pair_kernels()) return false;
+  if (f->d % 64 || f->h % 64) return false;
+  if (f->n_shared_rows > 0 && f->h_shared % 64) return false;
+  return true;
+}
+struct X3Ws {
+  void *xr, *xs, *w1, *w3, *w2, *sw1, *sw3, *sw2, *pre_r, *pre_s;
+  size_t bytes;
+};
+X3Ws x3_layout(const nimg_ffn_desc* f, void* base) {
+  X3Ws w{};
+  uint8_t* p = static_cast<uint8_t*>(base);
+  size_t o = 0;
+  auto take = [&](size_t elems) { void* q = p ? p + o : nullptr; o += align_up(elems * 2); return q; };
+  const size_t d = f->d, h = f->h, hs = f->h_shared, E = f->n_experts;
+  const size_t nr = f->n_rows, ns = f->n_shared_rows;
+  w.xr = take(nr * 3 * d);
+  w.xs = take(ns * 3 * d);
+  w.w1 = take(nr ? E * h * 3 * d : 0);
+  w.w3 = take(nr ? E * h * 3 * d : 0);
+  w.w2 = take(nr ? E * d * 3 * h : 0);
+  w.sw1 = take(ns ? hs * 3 * d : 0);
+  w.sw3 = take(ns ? hs * 3 * d : 0);
+  w.sw2 = take(ns ? d * 3 * hs : 0);
+  w.pre_r = take(nr * 3 * h);
+  w.pre_s = take(ns * 3 * hs);
+  w.bytes = o;
+  return w;
+}
+
 bool ffn_use_tc(const nimg_ffn_desc* f) {
   if (f->act_dtype != NIMG_BF16) return false;
   if (f->d % 16 || f->h % 16) return false;
@@ -235,6 +274,7 @@ bool ffn_use_tc(const nimg_ffn_desc* f) {
   return true;
 }
 size_t ffn_ws_bytes(const nimg_ffn_desc* f) {
+  if (ffn_use_x3(f)) return x3_layout(f, nullptr).bytes;
   const size_t e = ffn_use_tc(f) ? 2 : (f->act_dtype == NIMG_F64 ? 8 : 4);
   return align_up((size_t)f->n_rows * f->h * e) + align_up((size_t)f->n_shared_rows * f->h_shared * e);
 }
@@ -320,6 +360,84 @@ struct FfnTrain {
   void *pre_r, *pre_s, *h_r, *h_s;
 };
 
+// fp32 layer on the bf16 tcgen05 pair kernels: split operands (K' = 3K), GEMM1
+// writes `pre` split, GEMM2 writes fp32 rows (split_kernels.cu).
+int expert_ffn_x3(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex, const void* xr,
+                  const void* w1, const void* w3, const void* w2, void* yr, const void* xs,
+                  const void* sw1, const void* sw3, const void* sw2, void* ys, void* ws,
+                  cudaStream_t st) {
+  const X3Ws L = x3_layout(f, ws);
+  const bool has_r = f->n_rows > 0, has_s = f->n_shared_rows > 0;
+  const int d = (int)f->d, h = (int)f->h, hs = (int)(has_s ? f->h_shared : f->h);
+  const int64_t E = f->n_experts;
+  const float* F = nullptr;
+  if (has_r) {
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(xr), nullptr, L.xr, f->n_rows, d, 0, st));
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(w1), nullptr, L.w1, E * h, d, 1, st));
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(w3), nullptr, L.w3, E * h, d, 1, st));
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(w2), nullptr, L.w2, E * d, h, 1, st));
+  }
+  if (has_s) {
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(xs), nullptr, L.xs, f->n_shared_rows, d, 0, st));
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(sw1), nullptr, L.sw1, hs, d, 1, st));
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(sw3), nullptr, L.sw3, hs, d, 1, st));
+    CUDA_TRY(launch_split3_rows(static_cast<const float*>(sw2), nullptr, L.sw2, d, hs, 1, st));
+  }
+  (void)F;
+  int sms = 0;
+  NIMG_TRY(device_sms(&sms));
+  const int tile_rows = tc_pair_rows();
+  const int rb = has_r ? 0 : 1;
+  {  // GEMM1: pre' = split(SiLU(x' W1'^T) * (x' W3'^T)), K' = 3d
+    GroupedParams p;
+    memset(&p, 0, sizeof(p));
+    const int bn = tc_bn_out(0), box = tc_b_box(0);
+    NIMG_TRY(fill_segments(p, f, off, ex, tile_rows, (h + bn - 1) / bn, (hs + bn - 1) / bn));
+    TmapSet tm;
+    memset(&tm, 0, sizeof(tm));
+    if (has_r) {
+      NIMG_TRY(map_2d(&tm.a[0], L.xr, f->n_rows, 3 * (uint64_t)d, 128));
+      NIMG_TRY(map_3d(&tm.b[0], L.w1, E, h, 3 * (uint64_t)d, box));
+      NIMG_TRY(map_3d(&tm.b3[0], L.w3, E, h, 3 * (uint64_t)d, box));
+    }
+    if (has_s) {
+      NIMG_TRY(map_2d(&tm.a[1], L.xs, f->n_shared_rows, 3 * (uint64_t)d, 128));
+      NIMG_TRY(map_3d(&tm.b[1], L.sw1, 1, hs, 3 * (uint64_t)d, box));
+      NIMG_TRY(map_3d(&tm.b3[1], L.sw3, 1, hs, 3 * (uint64_t)d, box));
+    }
+    if (!has_r) { tm.a[0] = tm.a[1]; tm.b[0] = tm.b[1]; tm.b3[0] = tm.b3[1]; }
+    if (!has_s) { tm.a[1] = tm.a[rb]; tm.b[1] = tm.b[rb]; tm.b3[1] = tm.b3[rb]; }
+    p.bank[0] = GBank{L.pre_r, 3 * h, 3 * d, h, (h + bn - 1) / bn, kSplit3Out, nullptr, nullptr, nullptr};
+    p.bank[1] = GBank{L.pre_s, 3 * hs, 3 * d, hs, (hs + bn - 1) / bn, kSplit3Out, nullptr, nullptr, nullptr};
+    CUDA_TRY(launch_grouped_tc_pair(0, tm, p, sms, st));
+    mark(3, st);
+  }
+  {  // GEMM2: y = pre' W2'^T in fp32, K' = 3h
+    GroupedParams p;
+    memset(&p, 0, sizeof(p));
+    const int bn = tc_bn_out(1), box = tc_b_box(1) / 2;
+    NIMG_TRY(fill_segments(p, f, off, ex, tile_rows, (d + bn - 1) / bn, (d + bn - 1) / bn));
+    TmapSet tm;
+    memset(&tm, 0, sizeof(tm));
+    if (has_r) {
+      NIMG_TRY(map_2d(&tm.a[0], L.pre_r, f->n_rows, 3 * (uint64_t)h, 128));
+      NIMG_TRY(map_3d(&tm.b[0], L.w2, E, d, 3 * (uint64_t)h, box));
+    }
+    if (has_s) {
+      NIMG_TRY(map_2d(&tm.a[1], L.pre_s, f->n_shared_rows, 3 * (uint64_t)hs, 128));
+      NIMG_TRY(map_3d(&tm.b[1], L.sw2, 1, d, 3 * (uint64_t)hs, box));
+    }
+    if (!has_r) { tm.a[0] = tm.a[1]; tm.b[0] = tm.b[1]; }
+    if (!has_s) { tm.a[1] = tm.a[0]; tm.b[1] = tm.b[0]; }
+    tm.b3[0] = tm.b[0];
+    tm.b3[1] = tm.b[1];
+    p.bank[0] = GBank{yr, d, 3 * h, d, (d + bn - 1) / bn, kF32Out, nullptr, nullptr, nullptr};
+    p.bank[1] = GBank{ys, d, 3 * hs, d, (d + bn - 1) / bn, kF32Out, nullptr, nullptr, nullptr};
+    CUDA_TRY(launch_grouped_tc_pair(1, tm, p, sms, st));
+  }
+  return NIMG_OK;
+}
+
 int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* ex,
                     const void* xr, const void* w1, const void* w3, const void* w2, void* yr,
                     const void* xs, const void* sw1, const void* sw3, const void* sw2, void* ys,
@@ -333,6 +451,12 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
   if ((has_r && (!xr || !w1 || !w3 || !w2 || !yr)) || (has_s && (!xs || !sw1 || !sw3 || !sw2 || !ys)))
     return fail(NIMG_ERR_SHAPE, "null tensor pointer");
   const bool tc = ffn_use_tc(f) && !(tr && tr->force_simt);
+  if (!tc && !tr && !gather_idx && !bg && ffn_use_x3(f)) {
+    const void* ptrs[] = {xr, w1, w3, w2, yr, xs, sw1, sw3, sw2, ys};
+    for (const void* q : ptrs)
+      if (q && !aligned16(q)) return fail(NIMG_ERR_SHAPE, "tensor not 16-byte aligned");
+    return expert_ffn_x3(f, off, ex, xr, w1, w3, w2, yr, xs, sw1, sw3, sw2, ys, ws, st);
+  }
   const bool f64 = f->act_dtype == NIMG_F64;
   if (f64 && (tr || gather_idx || bg)) return fail(NIMG_ERR_CONFIG, "internal: f64 mode is forward-only");
   const size_t e = tc ? 2 : (f64 ? 8 : 4);
@@ -504,7 +628,7 @@ bool use_fused_gather(int32_t path, int64_t d) {
     const char* e = getenv("NIMG_FUSED_GATHER");
     return e && e[0] == '1';
   }();
-  return on && path == NIMG_PATH_TCGEN05 && d % 64 == 0;
+  return on && path == NIMG_PATH_TCGEN05 && d % 64 == 0;   // (bf16 layers: checked by the caller)
 }
 
 // ------------------------------------------------------------- training state
@@ -683,7 +807,7 @@ int nimg_gather_rows(const void* src, int64_t n_src_rows, int64_t row_bytes, con
 int nimg_ffn_path(const nimg_ffn_desc* f, int32_t* path, int32_t* y_dtype) {
   if (!f || !path || !y_dtype) return fail(NIMG_ERR_CONFIG, "null argument");
   const bool tc = ffn_use_tc(f);
-  *path = tc ? NIMG_PATH_TCGEN05 : NIMG_PATH_SIMT;
+  *path = tc || ffn_use_x3(f) ? NIMG_PATH_TCGEN05 : NIMG_PATH_SIMT;
   *y_dtype = tc ? NIMG_BF16 : (f->act_dtype == NIMG_F64 ? NIMG_F64 : NIMG_F32);
   return NIMG_OK;
 }
@@ -811,7 +935,8 @@ int nimg_moe_workspace_bytes(const nimg_moe_desc* d, size_t* bytes) {
   int32_t path, ydt;
   nimg_ffn_path(&f, &path, &ydt);
   // the gathered-row buffer exists only when the gather is not fused into GEMM1
-  const size_t xg = use_fused_gather(path, d->d) ? 0 : align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
+  const size_t xg = d->act_dtype == NIMG_BF16 && use_fused_gather(path, d->d)
+                        ? 0 : align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
   // the training forward (moe_forward_impl with a state blob) keeps the shared
   // expert's outputs in fp32 on the CUDA-core training path: size for both
   const size_t ys_elt = std::max<size_t>(elt(ydt), train_use_tc(d) ? 2 : 4);
@@ -845,7 +970,10 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
     ydt = ts.tc ? NIMG_BF16 : NIMG_F32;
     path = ts.tc ? NIMG_PATH_TCGEN05 : NIMG_PATH_SIMT;
   }
-  const bool fused_gather = !state && use_fused_gather(path, d->d);
+  // gathers inside GEMM1 copy bf16 rows of the bf16 tcgen05 path (fp32 layers
+  // on the tensor cores split their gathered rows first)
+  const bool bf_tc = path == NIMG_PATH_TCGEN05 && d->act_dtype == NIMG_BF16;
+  const bool fused_gather = !state && bf_tc && use_fused_gather(path, d->d);
   uint8_t* w = static_cast<uint8_t*>(ws);
   void* route_ws = w;                 w += route_ws_bytes(d);
   void* xg = w;                       if (!fused_gather) w += align_up((size_t)f.n_rows * d->d * elt(d->act_dtype));
@@ -856,7 +984,7 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
 
   // the routed-row gather runs inside GEMM1 (background warps) on the tcgen05
   // pair path; NIMG_BG_GATHER=0 keeps the separate gather kernel
-  const bool bg_gather = !fused_gather && path == NIMG_PATH_TCGEN05 && use_pair_kernels() &&
+  const bool bg_gather = !fused_gather && bf_tc && use_pair_kernels() &&
                          use_bg_gather() && f.n_rows > 0 && f.n_shared_rows > 0 &&
                          (d->d * elt(d->act_dtype)) % 16 == 0;
   BgGather bg{};

@@ -586,30 +586,52 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
       const int row = (int)crank * BM + r;                 // row within the pair tile
       const bool rv = row < ti.rows_valid;
       bf16* orow = reinterpret_cast<bf16*>(bk.out) + (int64_t)(ti.a_row + row) * bk.out_ld + ti.n0;
+      const int oflags = ti.bank ? p.bank[1].flags : p.bank[0].flags;
 #pragma unroll 1
       for (int c = 0; c < C::BN_OUT / 16; ++c) {
         uint32_t a[16], g[16];
         tmem_ld16(tb + c * 16, a);
-        uint32_t pk[8];
+        float v[16];
         if (MODE == 0) {
           tmem_ld16(tb + C::B_ROWS + c * 16, g);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            pk[j] = pack_bf16x2(silu_mul(__uint_as_float(a[2 * j]), __uint_as_float(g[2 * j])),
-                                silu_mul(__uint_as_float(a[2 * j + 1]), __uint_as_float(g[2 * j + 1])));
+          for (int j = 0; j < 16; ++j) v[j] = silu_mul(__uint_as_float(a[j]), __uint_as_float(g[j]));
         } else {
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            pk[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(a[j]);
         }
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pk[j] = pack_bf16x2(v[2 * j], v[2 * j + 1]);
         if (rv && ti.n0 + c * 16 < Nb) {
-          uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          if (MODE == 0 && h_out != nullptr)   // training forward: keep h1 | h3
-            store_h1h3(h_out, Nb, ti.a_row + row, ti.n0 + c * 16, a, g);
+          if (MODE == 1 && (oflags & kF32Out)) {   // fp32 mode: fp32 rows
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(bk.out) +
+                                                    (int64_t)(ti.a_row + row) * bk.out_ld + ti.n0 + c * 16);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
+            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            if (MODE == 0 && (oflags & kSplit3Out)) {   // fp32 mode: pre as [hi | hi | lo]
+              uint32_t lo[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const __nv_bfloat162 hv = *reinterpret_cast<const __nv_bfloat162*>(&pk[j]);
+                lo[j] = pack_bf16x2(v[2 * j] - __low2float(hv), v[2 * j + 1] - __high2float(hv));
+              }
+              uint4* d2 = reinterpret_cast<uint4*>(orow + Nb + c * 16);
+              uint4* d3 = reinterpret_cast<uint4*>(orow + 2 * Nb + c * 16);
+              d2[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              d2[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+              d3[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+              d3[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+            }
+            if (MODE == 0 && h_out != nullptr)   // training forward: keep h1 | h3
+              store_h1h3(h_out, Nb, ti.a_row + row, ti.n0 + c * 16, a, g);
+          }
         }
       }
       tc_fence_before();

@@ -24,13 +24,15 @@ constexpr int kMaxSeg = 264;  // routed segments + shared; EP: R * E/R + 1
 
 // One weight bank of a grouped launch: bank 0 = routed experts (3-D weights
 // [E, N, K]), bank 1 = the shared expert (3-D with E = 1).
+constexpr int kSplit3Out = 1, kF32Out = 2;
 struct GBank {
   void* out;       // output rows (bank-local row index), row stride out_ld elements
   int64_t out_ld;
   int K;           // reduction length (d for GEMM1, h for GEMM2)
   int N;           // output columns (h for GEMM1, d for GEMM2)
   int ntn;         // N tiles
-  int pad_;
+  int flags;       // output form: 0 bf16; kSplit3Out (GEMM1, fp32 mode): bf16 [hi | hi | lo]
+                   // rows of 3N (out_ld = 3N); kF32Out (GEMM2, fp32 mode): fp32 rows
   const int32_t* a_idx;  // GEMM1 only: A row r is source row a_idx[r]; null = contiguous
   const void* a_src;     // gather source rows (bf16, K elements per row) when a_idx != null
   void* h_out;           // GEMM1, training forward: h1 | h3 rows (2N bf16 per row) or null
@@ -183,6 +185,11 @@ int simt_bm();
 int simt_bn();
 cudaError_t launch_grouped_simt(int mode, bool in_bf16, const SimtParams& p, cudaStream_t stream,
                                 bool f64 = false);
+
+// fp32 mode on the bf16 tensor cores (split_kernels.cu): rows -> bf16 [hi|hi|lo]
+// (pattern 0, activations) or [hi|lo|hi] (pattern 1, weights), K' = 3K
+cudaError_t launch_split3_rows(const float* src, const int32_t* idx, void* dst, int64_t rows, int K,
+                               int pattern, cudaStream_t s);
 
 // f64 storage mode (f64_kernels.cu): routing and combine with every value in f64
 cudaError_t launch_route_f64(const double* x_norm, const double* t_emb, const double* w_r,

@@ -68,7 +68,12 @@ def test_ffn_path_selection():
     p, y = C.c_int32(), C.c_int32()
     assert L.lib.nimg_ffn_path(C.byref(f), C.byref(p), C.byref(y)) == 0
     assert (p.value, y.value) == (L.NIMG_PATH_TCGEN05, L.NIMG_BF16)
+    # fp32 layers whose widths tile the pair kernels run on the tensor cores
+    # (bf16x3 split, fp32 output); others on the CUDA cores
     f.act_dtype = L.NIMG_F32
+    L.lib.nimg_ffn_path(C.byref(f), C.byref(p), C.byref(y))
+    assert (p.value, y.value) == (L.NIMG_PATH_TCGEN05, L.NIMG_F32)
+    f.h = 168
     L.lib.nimg_ffn_path(C.byref(f), C.byref(p), C.byref(y))
     assert (p.value, y.value) == (L.NIMG_PATH_SIMT, L.NIMG_F32)
     f.act_dtype, f.h = L.NIMG_BF16, 20

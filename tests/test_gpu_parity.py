@@ -534,3 +534,35 @@ def test_f64_mode_is_forward_only():
     with pytest.raises(ConfigError):
         M.moe_forward(T(inp["x_mod"]), xn, T(inp["x_mod"]), T(inp["t_emb"]), cfg, bank,
                       T(inp["w_r"]))
+
+
+@pytest.mark.parametrize("B,S,d,E,h,C", [(2, 192, 256, 8, 128, 2.0), (3, 100, 512, 16, 192, 1.7)])
+def test_fp32_mode_tensor_core_split(B, S, d, E, h, C):
+    """fp32 layers whose widths tile the pair kernels run on the bf16 tensor
+    cores with split operands (bf16x3, csrc/split_kernels.cu): routing
+    bit-exact, layer and swiglu within the fp32 bar against the oracle."""
+    from paper_2604_12163_b200 import _lib as L
+    from paper_2604_12163_b200 import moe as M
+    from paper_2604_12163_b200 import router as R
+    f = L.FfnDesc(n_rows=B * S, n_shared_rows=B * S, d=d, h=h, h_shared=h, n_experts=E,
+                  act_dtype=L.NIMG_F32, nseg=E)
+    import ctypes as C_
+    p, y = C_.c_int32(), C_.c_int32()
+    L.lib.nimg_ffn_path(C_.byref(f), C_.byref(p), C_.byref(y))
+    assert p.value == L.NIMG_PATH_TCGEN05 and y.value == L.NIMG_F32
+    inp = make_layer_inputs(91, B, S, d, E, h, mode="fp32")
+    g = to_gpu(inp, "fp32")
+    cfg = R.RouterConfig(d_model=d, n_experts=E, capacity_factor=C)
+    out, _, routing = M.moe_forward(g["x_mod"], g["x_norm"], g["x_mod"], g["t_emb"], cfg, bank_of(g),
+                                    g["w_r"], return_routing=True)
+    ref_out, ref = O.moe_forward(inp["x_norm"], inp["x_mod"], inp["t_emb"], inp["w_r"], inp["w1"],
+                                 inp["w3"], inp["w2"], inp["sw1"], inp["sw3"], inp["sw2"],
+                                 capacity_factor=C, return_routing=True)
+    assert out.dtype == torch.float32
+    np.testing.assert_array_equal(routing["token_flat"].cpu().numpy(), ref["token_flat"])
+    np.testing.assert_array_equal(np_of(routing["gates"]), ref["gates"])
+    err = rel_fro(np_of(out), ref_out)
+    assert err <= TOL_FP32, f"fp32 (tensor-core split) rel-err {err:.3e}"
+    ys = M.swiglu(g["x_mod"][0], g["sw1"], g["sw3"], g["sw2"])
+    ys_ref = O.swiglu_arrays(inp["x_mod"][0], inp["sw1"], inp["sw3"], inp["sw2"])
+    assert rel_fro(np_of(ys), ys_ref) <= TOL_FP32
