@@ -608,11 +608,22 @@ def run_fp32(args, c, inp, cfg, bank, bf16_ms):
     tf = (wc["flops_g1"] + wc["flops_g2"]) / (ms * 1e-3) / 1e12
     del plan, a
     torch.cuda.empty_cache()
+    import ctypes as C
+    from paper_2604_12163_b200 import _lib
+    fd = _lib.FfnDesc(n_rows=wc["R"], n_shared_rows=wc["T"], d=c["d"], h=c["h"], h_shared=c["h"],
+                      n_experts=c["E"], act_dtype=_lib.NIMG_F32, nseg=c["E"])
+    path, ydt = C.c_int32(), C.c_int32()
+    _lib.check(_lib.lib.nimg_ffn_path(C.byref(fd), C.byref(path), C.byref(ydt)))
+    tc = path.value == _lib.NIMG_PATH_TCGEN05
+    gemms = ("bf16 tensor cores with split operands (bf16x3: x = x1 + x2, w = w1 + w2, "
+             "x1w1 + x1w2 + x2w1 as one bf16 GEMM over K' = 3K; per-call operand splits "
+             "included)" if tc else "CUDA-core fp32 grouped GEMMs (no TF32)")
     return {"ms_per_step": ms, "tokens_per_s": wc["T"] / (ms * 1e-3),
-            "vs_bf16_step": ms / bf16_ms, "expert_gemm_tflops_upper_bound": tf,
+            "vs_bf16_step": ms / bf16_ms, "expert_gemm_tflops_fp32_equiv": tf,
+            "path": "tcgen05 bf16x3" if tc else "simt fp32",
             "what": "fp32 mode (the reference's storage precision, rel-err <= 1e-4 bar): fp32 "
-                    "inputs and weights, exact f64-accumulated (DMMA) fp32 routing, CUDA-core fp32 grouped "
-                    "GEMMs (no TF32); steps=3"}
+                    "inputs and weights, exact f64-accumulated (DMMA) fp32 routing, " + gemms +
+                    ", fp32 expert outputs and the reference's f64 combine chain; steps=3"}
 
 
 def run_e2e(args, c, inp, cfg, bank):
