@@ -783,9 +783,29 @@ ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__
     const int i = i0 + 32 * j;
     key[j] = i < S ? score_key(__ldg(c + i)) : 0u;
   }
-  uint32_t thr = 0u;
+  // bits every key of the column shares (router scores cluster near 1/E, so
+  // the sign and most exponent bits agree): the search starts below them
+  uint32_t kand = 0xFFFFFFFFu, kor = 0u;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    if (i0 + 32 * j < S) { kand &= key[j]; kor |= key[j]; }
+  }
+  kand = __reduce_and_sync(0xffffffffu, kand);
+  kor = __reduce_or_sync(0xffffffffu, kor);
+  if (lane == 0) { red[0][warp][0] = (int)kand; red[1][warp][0] = (int)kor; }
+  __syncthreads();
+  kand = 0xFFFFFFFFu;
+  kor = 0u;
+#pragma unroll
+  for (int w = 0; w < SB_WARPS; ++w) { kand &= (uint32_t)red[0][w][0]; kor |= (uint32_t)red[1][w][0]; }
+  const uint32_t diff = kand ^ kor;        // bits that differ somewhere in the column
+  const int top = diff ? 31 - __clz(diff) : -1;
+  // every key agrees above bit `top`: the cap-th largest key has those bits
+  uint32_t thr = top < 0 ? kand : (top >= 31 ? 0u : (kand & ~((2u << top) - 1u)));
+  const int sh0 = top < 0 ? -2 : (top | 1) - 1;   // first 2-bit step covering bit `top`
+  __syncthreads();   // red[] reused by the search
 #pragma unroll 1
-  for (int sh = 30, buf = 0; sh >= 0; sh -= 2, buf ^= 1) {
+  for (int sh = sh0, buf = 0; sh >= 0; sh -= 2, buf ^= 1) {
     int n1 = 0, n2 = 0, n3 = 0;
 #pragma unroll
     for (int j = 0; j < KPL; ++j) {
