@@ -345,7 +345,7 @@ router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__
 // emax] -- and any zero-exponent or non-finite one -- is left out of the
 // integer sum and added back exactly in f64 from a short per-row list.
 __global__ void __launch_bounds__(THREADS, 1)
-router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_r,
+router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_r, int tpc,
                         const double* __restrict__ part, Ws ws, float* __restrict__ logits,
                         float* __restrict__ scores_bes, int B, int S, int d) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -363,8 +363,10 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t T = (int64_t)B * S;
-  const int64_t t0 = (int64_t)blockIdx.x * BM;
-  const int rows = (int)(T - t0 < BM ? T - t0 : BM);
+  // tpc <= BM tokens per CTA (the MMA tile stays M = 128; rows past tpc are
+  // zero digits): sized on the host so the grid fills whole waves of SMs
+  const int64_t t0 = (int64_t)blockIdx.x * tpc;
+  const int rows = (int)(T - t0 < tpc ? T - t0 : tpc);
   const int nkb = d / KB;
   pdl_trigger();
   const bool trace = NIMG_I8_TRACE && (blockIdx.x == 0 || blockIdx.x == 64);
@@ -851,9 +853,30 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
   err = set_max_dyn_smem(ri8::router_scores_i8_kernel, (int)ri8::SMEM);
   if (err != cudaSuccess) return err;
   const bf16* x = reinterpret_cast<const bf16*>(x_norm);
-  err = launch_pdl(ri8::router_scores_i8_kernel, dim3((unsigned)((T + ri8::BM - 1) / ri8::BM)),
-                   dim3(ri8::THREADS), ri8::SMEM, s, x, w_r, (const double*)part, ws, logits, scores_bes,
-                   B, S, d);
+  // tokens per CTA: 128 (the MMA tile). NIMG_I8_BALANCE=1 sizes CTAs to fill
+  // whole waves of SMs instead (T = 16384: 147 CTAs of 112 tokens) -- measured
+  // slower (78.6 vs 67.6 us in the launch list: every CTA still streams the
+  // whole W digit image and runs the full M = 128 MMAs)
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  static const bool balance = [] {
+    const char* v = getenv("NIMG_I8_BALANCE");
+    return v && v[0] == '1';
+  }();
+  int tpc = ri8::BM;
+  if (balance) {
+    const int64_t waves = (T + (int64_t)sms * ri8::BM - 1) / ((int64_t)sms * ri8::BM);
+    const int64_t per = (T + sms * waves - 1) / (sms * waves);
+    tpc = (int)((per + 7) / 8 * 8);
+    if (tpc > ri8::BM) tpc = ri8::BM;
+    if (tpc < 8) tpc = 8;
+  }
+  err = launch_pdl(ri8::router_scores_i8_kernel, dim3((unsigned)((T + tpc - 1) / tpc)),
+                   dim3(ri8::THREADS), ri8::SMEM, s, x, w_r, tpc, (const double*)part, ws, logits,
+                   scores_bes, B, S, d);
   if (err != cudaSuccess) return err;
   static const bool stats = [] {   // debugging only (synchronises)
     const char* v = getenv("NIMG_ROUTER_I8_STATS");
