@@ -198,6 +198,13 @@ struct RouteWs {
   unsigned* counters;
   void* i8;        // INT8 router scratch (router_i8.cu)
   int* bg_flags;   // GEMM1 background-gather flags, one per 32 routed rows
+  // token-ordered expert outputs (1-GPU layer): GEMM2 writes routed row r to
+  // row_map[r]; token t's rows are [tok_off[t], tok_off[t] + comb_cnt[t]) in
+  // expert-ascending order, their gates gate_tok[..]; cursor: per sample
+  int* tok_off;
+  int* row_map;
+  float* gate_tok;
+  int* cursor;
 };
 // one flag per 32 routed rows, plus the sub-block claim counter (flags[nsub])
 int64_t bg_flag_count(const nimg_moe_desc* d) { return (d->E * d->B * d->cap + 31) / 32 + 1; }
@@ -207,7 +214,8 @@ size_t route_ws_bytes(const nimg_moe_desc* d) {
          align_up(router_part_bytes((int)d->B, (int)d->d, (int)d->E)) +
          align_up(router_wd_bytes((int)d->d, (int)d->E)) + align_up(slot_bytes(d)) +
          align_up((size_t)d->B * 4) + align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d)) +
-         align_up((size_t)bg_flag_count(d) * 4);
+         align_up((size_t)bg_flag_count(d) * 4) + align_up((size_t)d->B * d->S * 4) +
+         2 * align_up((size_t)d->E * d->B * d->cap * 4) + align_up((size_t)d->B * 4);
 }
 RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
@@ -225,10 +233,19 @@ RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   r.i8 = p;
   p += align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d));
   r.bg_flags = reinterpret_cast<int*>(p);
+  p += align_up((size_t)bg_flag_count(d) * 4);
+  r.tok_off = reinterpret_cast<int*>(p);
+  p += align_up((size_t)d->B * d->S * 4);
+  r.row_map = reinterpret_cast<int*>(p);
+  p += align_up((size_t)d->E * d->B * d->cap * 4);
+  r.gate_tok = reinterpret_cast<float*>(p);
+  p += align_up((size_t)d->E * d->B * d->cap * 4);
+  r.cursor = reinterpret_cast<int*>(p);
   return r;
 }
 
 bool use_pair_kernels();
+bool use_tok_order();
 // fp32 mode on the bf16 tensor cores (split_kernels.cu, "bf16x3"): fp32
 // layers whose widths tile the tcgen05 pair kernels; NIMG_FP32_TC=0 keeps the
 // CUDA-core fp32 GEMMs
@@ -443,7 +460,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
                     const void* xs, const void* sw1, const void* sw3, const void* sw2, void* ys,
                     void* ws, size_t ws_bytes, cudaStream_t st,
                     const int32_t* gather_idx = nullptr, int64_t gather_src_rows = 0,
-                    const FfnTrain* tr = nullptr, const BgGather* bg = nullptr) {
+                    const FfnTrain* tr = nullptr, const BgGather* bg = nullptr,
+                    const int32_t* y_row_map = nullptr) {
   NIMG_TRY(check_ffn(f, off, ex));
   if (!tr && ws_bytes < ffn_ws_bytes(f)) return fail(NIMG_ERR_CONFIG, "workspace too small");
   const bool has_r = f->n_rows > 0, has_s = f->n_shared_rows > 0;
@@ -529,7 +547,8 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
       if (!has_s) { tm.a[1] = tm.a[0]; tm.b[1] = tm.b[0]; }
       tm.b3[0] = tm.b[0];
       tm.b3[1] = tm.b[1];
-      p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0, nullptr, nullptr};
+      // y_row_map (pair kernel): routed row r -> row y_row_map[r] of yr
+      p.bank[0] = GBank{yr, d, h, d, (d + bn - 1) / bn, 0, pair ? y_row_map : nullptr, nullptr};
       p.bank[1] = GBank{ys, d, hs, d, (d + bn - 1) / bn, 0, nullptr, nullptr};
       if (pair) CUDA_TRY(launch_grouped_tc_pair(1, tm, p, sms, st));
       else CUDA_TRY(launch_grouped_tc(1, tm, p, sms, st));
@@ -600,11 +619,13 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const void* t_emb_v, 
                            scores_bes, B, S, dd, E, st));
   mark(6, st);   // router scores done (inside stage 0 -> 1)
   CUDA_TRY(launch_ec_select(scores_bes, o->token_flat, static_cast<float*>(o->gate_raw), w.slot_of, B,
-                            S, E, cap, st));
+                            S, E, cap, st, w.cursor));
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
   CUDA_TRY(launch_gate_norm(scores_bes, w.slot_of, static_cast<float*>(o->gates), o->comb_rows, o->comb_cnt, B, S,
                             E, cap, d->gate_eps, d->gate_scale, st, w.bg_flags,
-                            (int)bg_flag_count(d)));
+                            (int)bg_flag_count(d),
+                            use_tok_order() ? TokOrder{w.tok_off, w.row_map, w.gate_tok, w.cursor}
+                                            : TokOrder{nullptr, nullptr, nullptr, nullptr}));
   return NIMG_OK;
 }
 
@@ -620,6 +641,18 @@ bool use_bg_gather() {
   static const bool on = [] {
     const char* e = getenv("NIMG_BG_GATHER");
     return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// NIMG_TOK_ORDER=1: GEMM2 writes the routed rows in token order and the
+// combine streams each token's rows (bitwise equal). Off by default: measured
+// equal at cfg2 (combine 89.2 -> 86.8 us, GEMM2 +1.7 us, gates +3.6 us for the
+// row allocation) -- the combine is bound by mixed read/write DRAM
+// efficiency, not by its row gather.
+bool use_tok_order() {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_TOK_ORDER");
+    return e && e[0] == '1';
   }();
   return on;
 }
@@ -1001,11 +1034,18 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   int64_t off[kMaxSeg + 1];
   if (f.nseg > kMaxSeg - 8) return fail(NIMG_ERR_CONFIG, "too many experts for one grouped launch");
   for (int e = 0; e <= f.nseg; ++e) off[e] = (int64_t)e * d->B * d->cap;  // moe.py:154
+  // token-ordered expert outputs: GEMM2 writes each routed row where its
+  // token's rows are consecutive, the combine streams them (same sums, same
+  // expert-ascending order: bitwise equal). Inference on the bf16 pair path.
+  const RouteWs rw = carve_route(d, route_ws);
+  const bool tok_order = !state && bf_tc && use_pair_kernels() && gate_tok_supported() &&
+                         use_tok_order() && f.n_rows > 0;
   // fused path: GEMM1 gathers x_mod rows by token_flat itself (TMA gather4)
   NIMG_TRY(expert_ffn_impl(&f, off, nullptr, fused_gather ? p->x_mod : xg, p->w1, p->w3, p->w2, yr,
                            p->x_mod, p->sw1, p->sw3, p->sw2, ys, ffn_ws, ffn_ws_bytes(&f), st,
                            fused_gather ? p->route.token_flat : nullptr, d->B * d->S,
-                           state ? &tr : nullptr, bg_gather ? &bg : nullptr));
+                           state ? &tr : nullptr, bg_gather ? &bg : nullptr,
+                           tok_order ? rw.row_map : nullptr));
   mark(4, st);
   if (d->act_dtype == NIMG_F64)
     CUDA_TRY(launch_combine_f64(static_cast<const double*>(yr), static_cast<const double*>(ys),
@@ -1014,9 +1054,9 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
                                 (int)d->d, (int)d->E, st));
   else
     CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys,
-                            static_cast<const float*>(p->route.gates), p->route.comb_rows,
-                            p->route.comb_cnt, p->out, d->B * d->S, (int)d->d, (int)d->E, st,
-                            resid_h, th_ff, (int)d->S));
+                            tok_order ? rw.gate_tok : static_cast<const float*>(p->route.gates),
+                            p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,
+                            (int)d->E, st, resid_h, th_ff, (int)d->S, tok_order ? rw.tok_off : nullptr));
   mark(5, st);
   return NIMG_OK;
 }

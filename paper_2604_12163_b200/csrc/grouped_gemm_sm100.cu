@@ -585,7 +585,11 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
       const uint32_t tb = tmem_base + acc * 256 + ((uint32_t)(q * 32) << 16);
       const int row = (int)crank * BM + r;                 // row within the pair tile
       const bool rv = row < ti.rows_valid;
-      bf16* orow = reinterpret_cast<bf16*>(bk.out) + (int64_t)(ti.a_row + row) * bk.out_ld + ti.n0;
+      // GEMM2 with a row map (1-GPU layer): routed row r lands at row a_idx[r]
+      // (token order, the combine then reads each token's rows contiguously)
+      const int64_t orow_i = (MODE == 1 && bk.a_idx != nullptr && rv) ? (int64_t)__ldg(bk.a_idx + ti.a_row + row)
+                                                                      : (int64_t)(ti.a_row + row);
+      bf16* orow = reinterpret_cast<bf16*>(bk.out) + orow_i * bk.out_ld + ti.n0;
       const int oflags = ti.bank ? p.bank[1].flags : p.bank[0].flags;
 #pragma unroll 1
       for (int c = 0; c < C::BN_OUT / 16; ++c) {
@@ -608,7 +612,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
         if (rv && ti.n0 + c * 16 < Nb) {
           if (MODE == 1 && (oflags & kF32Out)) {   // fp32 mode: fp32 rows
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(bk.out) +
-                                                    (int64_t)(ti.a_row + row) * bk.out_ld + ti.n0 + c * 16);
+                                                    orow_i * bk.out_ld + ti.n0 + c * 16);
 #pragma unroll
             for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {

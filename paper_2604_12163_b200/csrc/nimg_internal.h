@@ -221,11 +221,21 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
                              cudaStream_t s);
 size_t router_part_bytes(int B, int d, int E);
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
-                             int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s);
+                             int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s,
+                             int* cursor = nullptr);
+// Token-ordered expert outputs for the 1-GPU combine (gate_tile_kernel):
+// null tok_off = off
+struct TokOrder {
+  int* tok_off;
+  int* row_map;
+  float* gate_tok;
+  int* cursor;
+};
+bool gate_tok_supported();   // the gate kernel that fills TokOrder is in use
 cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,
                              int32_t* comb_rows, int32_t* comb_cnt, int B, int S, int E, int cap,
                              float gate_eps, float gate_scale, cudaStream_t s, int* bg_flags = nullptr,
-                             int n_bg_flags = 0);
+                             int n_bg_flags = 0, TokOrder tko = TokOrder{nullptr, nullptr, nullptr, nullptr});
 // chunk_done[c] += number of 32-row sub-blocks of [0, rows) overlapping chunk c
 cudaError_t launch_bg_count(int rows, int chunk_rows, unsigned* chunk_done, cudaStream_t s);
 cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t* idx,
@@ -236,7 +246,8 @@ cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
                            void* out, int64_t T, int d, int E, cudaStream_t s,
-                           const void* hres = nullptr, const void* th_gate = nullptr, int S = 1);
+                           const void* hres = nullptr, const void* th_gate = nullptr, int S = 1,
+                           const int32_t* tok_off = nullptr);
 // backbone MoE branch prologue (block_kernels.cu)
 cudaError_t launch_block_modvec(const float* sa_gate, const float* ff_scale, const float* ff_gate,
                                 double* th_sa, double* th_ff, float* onep, float* th_sa_f,

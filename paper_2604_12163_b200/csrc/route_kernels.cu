@@ -630,7 +630,7 @@ inline size_t select_smem(int S, int cap) {
 __global__ void __launch_bounds__(SEL_THREADS)
 ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
                  float* __restrict__ gate_raw, int16_t* __restrict__ slot_of, int B, int S, int E,
-                 int cap) {
+                 int cap, int* __restrict__ cursor) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int P = next_pow2(cap);
   uint64_t* win = reinterpret_cast<uint64_t*>(sm);                  // [P]
@@ -644,6 +644,7 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
   pdl_wait();
   const int b = blockIdx.x, e = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (cursor && e == 0 && tid == 0) cursor[b] = 0;
   const float* col = scores_bes + ((int64_t)b * E + e) * S;
   for (int i = tid; i < S; i += SEL_THREADS) keys[i] = score_key(col[i]);
 
@@ -766,7 +767,7 @@ template <int KPL>
 __global__ void __launch_bounds__(SB_WARPS * 32)
 ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
                      float* __restrict__ gate_raw, int16_t* __restrict__ slot_of, int B, int S,
-                     int E, int cap, int P) {
+                     int E, int cap, int P, int* __restrict__ cursor) {
   extern __shared__ __align__(16) uint64_t wsel[];   // [P] winners
   __shared__ int red[2][SB_WARPS][4];
   __shared__ int wcnt[SB_WARPS][2];
@@ -775,6 +776,7 @@ ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = blockIdx.x;                         // b * E + e: scores_bes is (B, E, S)
   const int b = col / E, e = col - b * E;
+  if (cursor && e == 0 && threadIdx.x == 0) cursor[b] = 0;   // gate_tile's row allocator
   const float* c = scores_bes + (int64_t)col * S;
   const int i0 = warp * 32 * KPL + lane;              // token of key[0]
   uint32_t key[KPL];
@@ -893,7 +895,7 @@ __global__ void __launch_bounds__(GT_THREADS)
 gate_tile_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict__ slot_of,
                  float* __restrict__ gates, int32_t* __restrict__ comb_rows,
                  int32_t* __restrict__ comb_cnt, int B, int S, int E, int cap, float eps32,
-                 float alpha32, int* __restrict__ bg_flags, int n_bg_flags) {
+                 float alpha32, int* __restrict__ bg_flags, int n_bg_flags, TokOrder tko) {
   extern __shared__ __align__(16) uint8_t gsm[];
   constexpr int NW = GT_THREADS / 32;
   int16_t* sl = reinterpret_cast<int16_t*>(gsm);                                  // [E][32]
@@ -916,6 +918,35 @@ gate_tile_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict
     const int16_t j = in ? slot_of[o] : (int16_t)-1;
     sl[e * GT_TOK + lane] = j;
     raw[e * GT_TOK + lane] = (in && j >= 0) ? scores_bes[o] : 0.f;
+  }
+  __shared__ int tcnt[GT_TOK], toff[GT_TOK];
+  if (tko.tok_off) {
+    // token-ordered layout: this tile's rows get a contiguous range of its
+    // sample's E * cap rows (tiles in any order: per-sample atomic cursor)
+    __syncthreads();
+    for (int tok = warp; tok < GT_TOK; tok += NW) {
+      int n = 0;
+      if (s0 + tok < S)
+        for (int e0 = 0; e0 < E; e0 += 32) {
+          const int e = e0 + lane;
+          n += __popc(__ballot_sync(0xffffffffu, e < E && sl[e * GT_TOK + tok] >= 0));
+        }
+      if (lane == 0) tcnt[tok] = n;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int n = tcnt[lane];
+      int incl = n;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int base = 0;
+      if (lane == 31) base = atomicAdd(tko.cursor + b, incl);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      toff[lane] = (int)((int64_t)b * E * cap) + base + incl - n;
+    }
   }
   __syncthreads();
   float* rl = raw_l + (size_t)warp * E;
@@ -942,10 +973,19 @@ gate_tile_kernel(const float* __restrict__ scores_bes, const int16_t* __restrict
     const float den = (float)((double)tot32 + (double)eps32);
     for (int k = lane; k < cnt; k += 32) {
       const float q = (float)((double)rl[k] / (double)den);
-      gates[ro[k]] = (float)((double)q * (double)alpha32);
+      const float gk = (float)((double)q * (double)alpha32);
+      gates[ro[k]] = gk;
       comb_rows[t * E + k] = ro[k];
+      if (tko.tok_off) {
+        const int o = toff[tok] + k;
+        tko.row_map[ro[k]] = o;
+        tko.gate_tok[o] = gk;
+      }
     }
-    if (lane == 0) comb_cnt[t] = cnt;
+    if (lane == 0) {
+      comb_cnt[t] = cnt;
+      if (tko.tok_off) tko.tok_off[t] = toff[tok];
+    }
     __syncwarp();
   }
 }
@@ -1067,7 +1107,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
                TO* __restrict__ out, int64_t T, int d, int E, const TO* __restrict__ hres,
-               const ACC* __restrict__ thg, int S) {
+               const ACC* __restrict__ thg, int S, const int32_t* __restrict__ tok_off) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
@@ -1083,8 +1123,11 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
   // row list is known: the column loop's loads then hit L2
   if (lane == 0 && row_bytes % 16 == 0) bulk_prefetch_l2(ys + t * d, row_bytes);
 #endif
+  // tok_off: the token's rows are consecutive in the token-ordered yr (and
+  // `gates` is indexed the same way); else the expert-major row list
+  const int32_t rbase = tok_off != nullptr ? tok_off[t] : 0;
   for (int k = lane; k < cnt; k += 32) {
-    const int32_t r = comb_rows[t * E + k];
+    const int32_t r = tok_off != nullptr ? rbase + k : comb_rows[t * E + k];
     rows[k] = r;
 #ifndef NIMG_CB_NO_PREFETCH
     if (row_bytes % 16 == 0) bulk_prefetch_l2(yr + (int64_t)r * d, row_bytes);
@@ -1250,6 +1293,8 @@ size_t router_part_bytes(int B, int d, int E) {
 size_t router_wd_bytes(int d, int E) { return (size_t)d * (E <= DM_EP ? DM_EP : router_geom(E).EP) * 8; }
 
 // NIMG_SELECT=cta: the block-per-column radix-select kernel for every S
+static bool select_warp_enabled();
+bool gate_tok_supported() { return select_warp_enabled(); }
 static bool select_warp_enabled() {
   static const bool on = [] {
     const char* e = getenv("NIMG_SELECT");
@@ -1259,7 +1304,8 @@ static bool select_warp_enabled() {
 }
 
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
-                             int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s) {
+                             int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s,
+                             int* cursor) {
   if (select_warp_enabled() && S <= 4096) {
     const int P = next_pow2(cap);
     const size_t wsmem = (size_t)P * 8;
@@ -1269,7 +1315,7 @@ cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float
       cudaError_t e2 = set_max_dyn_smem(ec_select_blk_kernel<K>, (int)wsmem);                   \
       if (e2 != cudaSuccess) return e2;                                                         \
       return launch_pdl(ec_select_blk_kernel<K>, grid, dim3(SB_WARPS * 32), wsmem, s,           \
-                        scores_bes, token_flat, gate_raw, slot_of, B, S, E, cap, P);           \
+                        scores_bes, token_flat, gate_raw, slot_of, B, S, E, cap, P, cursor);   \
     } while (0)
     if (S <= 256) NIMG_BSEL(2);
     if (S <= 512) NIMG_BSEL(4);
@@ -1283,13 +1329,13 @@ cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float
   if (err != cudaSuccess) return err;
   dim3 grid(B, E);
   return launch_pdl(ec_select_kernel, grid, dim3(SEL_THREADS), smem, s, scores_bes, token_flat,
-                    gate_raw, slot_of, B, S, E, cap);
+                    gate_raw, slot_of, B, S, E, cap, cursor);
 }
 
 cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, float* gates,
                              int32_t* comb_rows, int32_t* comb_cnt, int B, int S, int E, int cap,
                              float gate_eps, float gate_scale, cudaStream_t s, int* bg_flags,
-                             int n_bg_flags) {
+                             int n_bg_flags, TokOrder tko) {
   const int64_t T = (int64_t)B * S;
   if (select_warp_enabled()) {
     const size_t smem = (((size_t)E * GT_TOK * 2 + 15) & ~size_t(15)) + (size_t)E * GT_TOK * 4 +
@@ -1299,7 +1345,7 @@ cudaError_t launch_gate_norm(const float* scores_bes, const int16_t* slot_of, fl
     const int grid = B * ((S + GT_TOK - 1) / GT_TOK);
     return launch_pdl(gate_tile_kernel, dim3(grid), dim3(GT_THREADS), smem, s, scores_bes, slot_of,
                       gates, comb_rows, comb_cnt, B, S, E, cap, gate_eps, gate_scale, bg_flags,
-                      n_bg_flags);
+                      n_bg_flags, tko);
   }
   const int grid = (int)((T + GN_WARPS - 1) / GN_WARPS);
   const size_t smem = (size_t)GN_WARPS * E * 8;
@@ -1342,14 +1388,15 @@ cudaError_t launch_gather_rows(const void* src, int64_t row_bytes, const int32_t
 template <typename TY, typename TO, bool RESID>
 static cudaError_t combine_dispatch(const void* yr, const void* ys, const float* gates,
                              const int32_t* rows, const int32_t* cnt, void* out, int64_t T, int d,
-                             int E, const void* hres, const void* thg, int S, cudaStream_t s) {
+                             int E, const void* hres, const void* thg, int S, cudaStream_t s,
+                             const int32_t* tok_off) {
   const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
   const size_t smem = (size_t)CB_WARPS * E * 8;
   using ACC = typename std::conditional<sizeof(TO) == 2, float, double>::type;
 #define NIMG_COMBINE(V, U)                                                                      \
   launch_pdl(combine_kernel<TY, TO, V, ACC, U, RESID>, dim3(grid), dim3(CB_WARPS * 32), smem, s, \
              (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E, (const TO*)hres, \
-             (const ACC*)thg, S)
+             (const ACC*)thg, S, tok_off)
   if (d % 512 == 0) return NIMG_COMBINE(8, 2);
   if (d % 8 == 0) return NIMG_COMBINE(8, 1);
   return NIMG_COMBINE(1, 1);
@@ -1359,14 +1406,14 @@ static cudaError_t combine_dispatch(const void* yr, const void* ys, const float*
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
                            void* out, int64_t T, int d, int E, cudaStream_t s, const void* hres,
-                           const void* th_gate, int S) {
+                           const void* th_gate, int S, const int32_t* tok_off) {
   if (T <= 0) return cudaSuccess;
   const bool r = hres != nullptr;
 #define NIMG_CD(TY, TO)                                                                              \
   (r ? combine_dispatch<TY, TO, true>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, \
-                                      hres, th_gate, S, s)                                          \
+                                      hres, th_gate, S, s, tok_off)                                 \
      : combine_dispatch<TY, TO, false>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, \
-                                       hres, th_gate, S, s))
+                                       hres, th_gate, S, s, tok_off))
   cudaError_t err;
   if (y_bf16 && out_bf16) err = NIMG_CD(bf16, bf16);
   else if (y_bf16) err = NIMG_CD(bf16, float);
