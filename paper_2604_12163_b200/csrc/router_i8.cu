@@ -233,7 +233,6 @@ __global__ void __launch_bounds__(256)
 router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
                       double* __restrict__ part, Ws ws, int B, int d) {
   pdl_trigger();
-  pdl_wait();   // launched with PDL: only the launch overlaps the previous kernel's tail
   const int KS = router_tpart_ks(d);
   if ((int)blockIdx.x < B * KS) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *ws.counter = 0u;
@@ -845,10 +844,13 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
                              cudaStream_t s) {
   const int64_t T = (int64_t)B * S;
   ri8::Ws ws = ri8::carve(i8ws, T, d);
-  // the first kernel of the chain: a PDL launch whose first act is to wait for
-  // its predecessor (so only launch latency overlaps the previous kernel's tail)
-  cudaError_t err = launch_pdl(ri8::router_prep_i8_kernel, dim3(B * router_tpart_ks(d) + ri8::NE),
-                               dim3(256), 0, s, t_emb, w_r, part, ws, B, d);
+  // the first kernel of the chain: an ORDINARY launch (full stream order). The
+  // scores kernel's converters read x_norm before any griddepcontrol.wait, so
+  // everything that wrote x_norm (e.g. the block prologue) must have completed
+  // before this kernel starts and triggers its dependents. (A PDL launch here
+  // would let the scores kernel start while the prologue still writes x_norm.)
+  ri8::router_prep_i8_kernel<<<B * router_tpart_ks(d) + ri8::NE, 256, 0, s>>>(t_emb, w_r, part, ws, B, d);
+  cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   err = set_max_dyn_smem(ri8::router_scores_i8_kernel, (int)ri8::SMEM);
   if (err != cudaSuccess) return err;

@@ -2,7 +2,7 @@
 # usage: bash tools/c_sweep.sh   (writes gpurun_out/cfg3_C*.json)
 mkdir -p gpurun_out
 for C in 8 4 2; do
-  timeout 600 python bench.py --config cfg3 --capacity $C --steps 10 --warmup 3 --no-cpu-baseline \
+  timeout 600 python bench.py --config cfg3 --capacity $C --steps 10 --warmup 3 --no-cpu-baseline --no-train --no-fp32 \
     > gpurun_out/cfg3_C$C.json 2> gpurun_out/cfg3_C$C.err
   echo "== C=$C rc=$?"
   python - <<PY
