@@ -67,7 +67,7 @@ def load_peaks():
 
 def gemm1_traffic():
     """DRAM bytes per GEMM1 launch from the committed ncu --set full capture."""
-    p = os.path.join(ROOT, "profiles", "gemm_traffic_r01c.json")
+    p = os.path.join(ROOT, "profiles", "gemm_traffic_r02.json")
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f)["traffic_bytes_per_launch"]
