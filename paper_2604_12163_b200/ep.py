@@ -384,6 +384,8 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
         raise ConfigError(f"local bank has {bank_local.w1.shape[0]} experts, plan needs "
                           f"{plan.experts_per_rank}")
     act = x_mod.dtype
+    if act == torch.float64 or x_norm.dtype == torch.float64:
+        raise ConfigError("expert parallel runs the fp32 / bf16 modes (the f64 mode is 1-GPU)")
     T = B_l * S
     xm = x_mod.reshape(T, d)
     w = bank_local
