@@ -47,12 +47,17 @@ template <> struct Cfg<BWD_W2, false> { static constexpr int BN = 192, STAGES = 
 template <> struct Cfg<BWD_W1, false> { static constexpr int BN = 256, STAGES = 4; };
 // router weight gradient dW_r[:d] = x_norm^T dlogits per sample (N = E = 64)
 template <> struct Cfg<BWD_WR, false> { static constexpr int BN = 64, STAGES = 8; };
+// h = 6 x 224. 256-wide tiles (h = 5 x 256 + 64, the last tile of a row block
+// at N = 128, see the MMA issuer) measured 1-3% slower for both dgrad2 and dW2.
 #ifndef NIMG_D2_BN
 #define NIMG_D2_BN 224
 #endif
-template <> struct Cfg<BWD_D2, true> { static constexpr int BN = NIMG_D2_BN, STAGES = 6; };   // h = 6 x 224
+#ifndef NIMG_W2_BN
+#define NIMG_W2_BN 224
+#endif
+template <> struct Cfg<BWD_D2, true> { static constexpr int BN = NIMG_D2_BN, STAGES = 6; };
 template <> struct Cfg<BWD_D1, true> { static constexpr int BN = 256, STAGES = 6; };
-template <> struct Cfg<BWD_W2, true> { static constexpr int BN = 224, STAGES = 6; };
+template <> struct Cfg<BWD_W2, true> { static constexpr int BN = NIMG_W2_BN, STAGES = 6; };
 template <> struct Cfg<BWD_W1, true> { static constexpr int BN = 256, STAGES = 6; };
 
 // epilogue warps: 8 for the SwiGLU-derivative epilogue (two warps per TMEM
@@ -74,6 +79,14 @@ template <int MODE, bool PAIR> constexpr int b_boxes() { return (bn_cta<MODE, PA
 template <int MODE, bool PAIR> constexpr int stage_bytes() { return BM * BK * 2 + b_boxes<MODE, PAIR>() * kChunk; }
 // W modes: per epilogue warp two 4-KB staging tiles (32 rows x 32 fp32, 128-B swizzle) for TMA stores
 constexpr int kStageOut = 4096;
+// W modes: fp32 tiles staged in smem for TMA stores. (Stored straight from
+// registers, one row per thread, 8 x 16 B per 32 columns: dW2 395 -> 486 us,
+// dW1 728 -> 858 us, profiles/r02_bwd2_*.)
+// timing probes for A/B builds only (wrong results): 1 = W epilogues skip the
+// staging and stores, 2 = the dgrad2 epilogue skips h1 | h3 and its stores
+#ifndef NIMG_BWD_PROBE
+#define NIMG_BWD_PROBE 0
+#endif
 template <int MODE> constexpr int out_bytes() { return a_mn<MODE>() ? 4 * 2 * kStageOut : 0; }
 template <int MODE, bool PAIR> constexpr int smem_bytes() {
   return Cfg<MODE, PAIR>::STAGES * stage_bytes<MODE, PAIR>() + out_bytes<MODE>() + h_bytes<MODE>() +
@@ -219,6 +232,10 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
     if (leader && lane == 0) {
       // ---------------------------------------------- MMA issuer (leader)
       constexpr uint32_t idesc = make_idesc_bf16_major(PAIR ? 2 * BM : BM, BN, AMN, true);
+      // narrow last tile of a 256-wide pair row: N = 128 reads each CTA's first
+      // 64 B columns, which hold all nval <= 64 valid ones (the epilogue reads
+      // accumulator columns < nval only)
+      constexpr uint32_t idesc_tail = make_idesc_bf16_major(PAIR ? 2 * BM : BM, BN / 2, AMN, true);
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
       for (int t = unit; t < p.total_tiles; t += n_units) {
@@ -226,6 +243,8 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
+        const int nval = (ti.bank ? p.bank[1].N : p.bank[0].N) - ti.n0;
+        const uint32_t id = (PAIR && BN == 256 && nval <= BN / 4) ? idesc_tail : idesc;
         for (int kb = 0; kb < ti.nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -238,8 +257,8 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
             // K step of 16: K-major +32 B inside the swizzle row; MN-major +16 rows = 2048 B
             const uint64_t ao = AMN ? (uint64_t)(k * 2048 >> 4) : (uint64_t)(2 * k);
             const uint64_t bo = (uint64_t)(k * 2048 >> 4);
-            if (PAIR) umma_bf16_cg2(d_tmem, adesc + ao, bdesc + bo, idesc, (kb | k) != 0);
-            else umma_bf16(d_tmem, adesc + ao, bdesc + bo, idesc, (kb | k) != 0);
+            if (PAIR) umma_bf16_cg2(d_tmem, adesc + ao, bdesc + bo, id, (kb | k) != 0);
+            else umma_bf16(d_tmem, adesc + ao, bdesc + bo, id, (kb | k) != 0);
           }
           if (PAIR) umma_commit_cg2(&empty[stage], 0x3); else umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -339,7 +358,11 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
         for (int g = 0; g < NG2; ++g) {
           const int c = 2 * g + half;
           mbar_wait(&hfull[hslot], hphase);
-          if (c < NCH) {
+          if (c < NCH && NIMG_BWD_PROBE == 2) {
+            uint32_t a[16];
+            tmem_ld16(tb + c * 16, a);
+            tmem_ld_wait();
+          } else if (c < NCH) {
             uint32_t a[16];
             tmem_ld16(tb + c * 16, a);
             tmem_ld_wait();
@@ -471,7 +494,7 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
           tmem_ld16(tb + cc * 32 + 16, *reinterpret_cast<uint32_t(*)[16]>(&a[16]));
           tmem_ld_wait();
           const int n = ti.n0 + cc * 32;
-          if (!any || n >= N) continue;
+          if (!any || n >= N || NIMG_BWD_PROBE == 1) continue;
           uint8_t* sbuf = stage_out + (q * 2 + obuf) * kStageOut;
           if (lane == 0) bulk_wait_read<1>();                 // the store that used this tile is done
           __syncwarp();

@@ -763,6 +763,9 @@ ec_select_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ tok
 // with indices >= S, so they rank after every real element and are never
 // taken (cap <= S).
 constexpr int SB_WARPS = 4;
+#ifndef NIMG_SEL_R8
+#define NIMG_SEL_R8 1
+#endif
 template <int KPL>
 __global__ void __launch_bounds__(SB_WARPS * 32)
 ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
@@ -804,6 +807,58 @@ ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__
   const int top = diff ? 31 - __clz(diff) : -1;
   // every key agrees above bit `top`: the cap-th largest key has those bits
   uint32_t thr = top < 0 ? kand : (top >= 31 ? 0u : (kand & ~((2u << top) - 1u)));
+#if NIMG_SEL_R8
+  // Radix search, 8 bits per pass below the common prefix: every key that
+  // still matches the prefix bumps a shared-memory histogram bin; warp 0 scans
+  // the 256 bins from the top for the bin holding the need-th largest key,
+  // zeroes the other histogram and publishes (digit, keys above it). Two
+  // barriers per pass, ceil((top + 1) / 8) passes.
+  __shared__ int hist[2][256];
+  __shared__ int rres[2];
+  for (int i = threadIdx.x; i < 512; i += SB_WARPS * 32) (&hist[0][0])[i] = 0;
+  __syncthreads();   // red[] free, histograms zeroed
+  int need = cap;
+#pragma unroll 1
+  for (int rem = top + 1, buf = 0; rem > 0; buf ^= 1) {
+    const int nb = rem < 8 ? rem : 8, sh = rem - nb, hi = rem;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const bool match = hi >= 32 || ((key[j] ^ thr) >> hi) == 0u;
+      if (match) atomicAdd(&hist[buf][(key[j] >> sh) & ((1u << nb) - 1u)], 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      int c[8], ls = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {   // lane l: bins 255 - 8 l - i, descending
+        c[i] = hist[buf][255 - 8 * lane - i];
+        ls += c[i];
+        hist[buf ^ 1][8 * lane + i] = 0;
+      }
+      int incl = ls;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int excl = incl - ls;
+      if (excl < need && incl >= need) {
+        int run = excl, dsel = 0, above = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (run < need && run + c[i] >= need) { dsel = 255 - 8 * lane - i; above = run; }
+          run += c[i];
+        }
+        rres[0] = dsel;
+        rres[1] = above;
+      }
+    }
+    __syncthreads();
+    thr |= (uint32_t)rres[0] << sh;
+    need -= rres[1];
+    rem = sh;
+  }
+#else
   const int sh0 = top < 0 ? -2 : (top | 1) - 1;   // first 2-bit step covering bit `top`
   __syncthreads();   // red[] reused by the search
 #pragma unroll 1
@@ -825,6 +880,7 @@ ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__
     for (int w = 0; w < SB_WARPS; ++w) { t1 += red[buf][w][1]; t2 += red[buf][w][2]; t3 += red[buf][w][3]; }
     thr |= (t3 >= cap ? 3u : t2 >= cap ? 2u : t1 >= cap ? 1u : 0u) << sh;
   }
+#endif
   int n_gt = 0, n_eq = 0;
 #pragma unroll
   for (int j = 0; j < KPL; ++j) { n_gt += key[j] > thr ? 1 : 0; n_eq += key[j] == thr ? 1 : 0; }

@@ -1,0 +1,11 @@
+"""Build timing-probe variants of the backward kernels (NIMG_BWD_PROBE) next to the
+library; tools/gpu_bwd_probe.sh times each with bench.py (A/B only: probe results are wrong)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
+from paper_2604_12163_b200 import _build  # noqa: E402
+
+for tag, defs in (("probe1", ("NIMG_BWD_PROBE=1",)), ("probe2", ("NIMG_BWD_PROBE=2",))):
+    out = os.path.join(os.path.dirname(_build.LIB), f"libnimg_moe_{tag}.so")
+    print(_build.build(out=out, defines=defs))
