@@ -1244,7 +1244,9 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
     memset(&P, 0, sizeof(P));
     memset(&tm, 0, sizeof(tm));
     P.bank[0] = BwdBank{w.dy_r, dd, ts.pre_r, nullptr, h, nullptr, g->g_w2, nullptr, 0, dd, h, 0, h, 0, 0};
-    P.bank[1] = BwdBank{dys, dd, ts.pre_s, nullptr, hs, nullptr, g->g_sw2, nullptr, 0, dd, hs, 0, hs, 0, 0};
+    // (shared bank with ks > 1: the row-chunk partials, folded below)
+    P.bank[1] = BwdBank{dys, dd, ts.pre_s, nullptr, hs, nullptr, ks > 1 ? (void*)w.sp2 : g->g_sw2, nullptr,
+                        0, dd, hs, 0, hs, 0, 0};
     if (tc) {
       NIMG_TRY(map_3d(&tm.a[0], w.dy_r, E, rows_e, dd, 64));
       NIMG_TRY(map_3d(&tm.b[0], ts.pre_r, E, rows_e, h, 64));
@@ -1284,7 +1286,9 @@ int nimg_moe_backward(const nimg_moe_desc* d, const nimg_moe_ptrs* p, const void
     memset(&P, 0, sizeof(P));
     memset(&tm, 0, sizeof(tm));
     P.bank[0] = BwdBank{w.dh_r, 2 * (int64_t)h, ts.xg, nullptr, dd, nullptr, g->g_w1, g->g_w3, 0, 2 * h, dd, 0, h, 0, 0};
-    P.bank[1] = BwdBank{w.dh_s, 2 * (int64_t)hs, p->x_mod, nullptr, dd, nullptr, g->g_sw1, g->g_sw3, 0, 2 * hs, dd, 0, hs, 0, 0};
+    P.bank[1] = BwdBank{w.dh_s, 2 * (int64_t)hs, p->x_mod, nullptr, dd, nullptr,
+                        ks > 1 ? (void*)w.sp1 : g->g_sw1, ks > 1 ? (void*)w.sp3 : g->g_sw3, 0, 2 * hs, dd, 0,
+                        hs, 0, 0};
     if (tc) {
       NIMG_TRY(map_3d(&tm.a[0], w.dh_r, E, rows_e, 2 * h, 64));
       NIMG_TRY(map_3d(&tm.b[0], ts.xg, E, rows_e, dd, 64));

@@ -79,15 +79,20 @@ template <int MODE, bool PAIR> constexpr int b_boxes() { return (bn_cta<MODE, PA
 template <int MODE, bool PAIR> constexpr int stage_bytes() { return BM * BK * 2 + b_boxes<MODE, PAIR>() * kChunk; }
 // W modes: per epilogue warp two 4-KB staging tiles (32 rows x 32 fp32, 128-B swizzle) for TMA stores
 constexpr int kStageOut = 4096;
-// W modes: fp32 tiles staged in smem for TMA stores. (Stored straight from
-// registers, one row per thread, 8 x 16 B per 32 columns: dW2 395 -> 486 us,
-// dW1 728 -> 858 us, profiles/r02_bwd2_*.)
+// (Stored from registers one row per thread, 8 x 16 B per 32 columns -- 32
+// partial sectors per warp store: dW2 395 -> 486 us, dW1 728 -> 858 us.)
 // timing probes for A/B builds only (wrong results): 1 = W epilogues skip the
 // staging and stores, 2 = the dgrad2 epilogue skips h1 | h3 and its stores
 #ifndef NIMG_BWD_PROBE
 #define NIMG_BWD_PROBE 0
 #endif
-template <int MODE> constexpr int out_bytes() { return a_mn<MODE>() ? 4 * 2 * kStageOut : 0; }
+// W epilogues: whole 32-B sectors stored from registers (16x256b TMEM loads,
+// the default: dW1 766 vs 804 us, dW2 equal), or (0) fp32 tiles staged in smem
+// for TMA stores (profiles/r02_bwd_epilogue_probe.txt)
+#ifndef NIMG_W_SECTOR
+#define NIMG_W_SECTOR 1
+#endif
+template <int MODE> constexpr int out_bytes() { return (a_mn<MODE>() && !NIMG_W_SECTOR) ? 4 * 2 * kStageOut : 0; }
 template <int MODE, bool PAIR> constexpr int smem_bytes() {
   return Cfg<MODE, PAIR>::STAGES * stage_bytes<MODE, PAIR>() + out_bytes<MODE>() + h_bytes<MODE>() +
          1024 + 256;
@@ -477,6 +482,41 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
           dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
+      } else if constexpr (NIMG_W_SECTOR) {
+        // weight gradient stored from registers in whole 32-B sectors: the
+        // 16x256b TMEM load gives four lanes 8 contiguous fp32 of one row, so
+        // each warp store writes 8 rows x 32 B (no shared-memory staging, no
+        // partial-sector writes). W1: rows [0, h) -> dW1, [h, 2h) -> dW3.
+        const int m_w = ti.m0 + rc + q * 32;                  // this warp's first row
+        const bool to3 = MODE == BWD_W1 && m_w >= h;
+        const int mrows = MODE == BWD_W1 ? h : bk.M;          // rows of one output slice
+        float* ob = reinterpret_cast<float*>(to3 ? bk.out3 : bk.out) +
+                    ((int64_t)ti.expert * mrows + (to3 ? m_w - h : m_w)) * (int64_t)N;
+        const int lr = lane >> 2, lc = 2 * (lane & 3);
+#pragma unroll 1
+        for (int cc = 0; cc < BN / 32; ++cc) {
+          uint32_t a0[16], a1[16];
+          tmem_ld16x256(tb + cc * 32, a0);                          // rows 0-15 of the warp
+          tmem_ld16x256(tb + ((uint32_t)16 << 16) + cc * 32, a1);   // rows 16-31
+          tmem_ld_wait();
+          const int n = ti.n0 + cc * 32;
+          if (n >= N) continue;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t* a = hh ? a1 : a0;
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+              const int row = 16 * hh + 8 * rr + lr;
+              if (m_w + row >= bk.M) continue;
+              float* o = ob + (int64_t)row * N + n + lc;
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (n + 8 * i + lc < N)
+                  *reinterpret_cast<float2*>(o + 8 * i) =
+                      make_float2(__uint_as_float(a[4 * i + 2 * rr]), __uint_as_float(a[4 * i + 2 * rr + 1]));
+            }
+          }
+        }
       } else {
         // weight gradient: 32 rows x 32 fp32 per warp per step, staged in a
         // 128-B-swizzled smem tile and written by one TMA store (coalesced,
@@ -519,7 +559,7 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
-    if (AMN && lane == 0) bulk_wait<0>();
+    if (AMN && !NIMG_W_SECTOR && lane == 0) bulk_wait<0>();
   }
 
   tc_fence_before();

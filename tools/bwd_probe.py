@@ -6,6 +6,8 @@ import sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 from paper_2604_12163_b200 import _build  # noqa: E402
 
-for tag, defs in (("probe1", ("NIMG_BWD_PROBE=1",)), ("probe2", ("NIMG_BWD_PROBE=2",))):
+VARIANTS = {"probe1": ("NIMG_BWD_PROBE=1",), "probe2": ("NIMG_BWD_PROBE=2",), "staged": ("NIMG_W_SECTOR=0",)}
+for tag in (sys.argv[1:] or VARIANTS):
+    defs = VARIANTS[tag]
     out = os.path.join(os.path.dirname(_build.LIB), f"libnimg_moe_{tag}.so")
     print(_build.build(out=out, defines=defs))
