@@ -53,6 +53,10 @@ import os as _os
 _DISPATCH_SERIAL = _os.environ.get("NIMG_EP_DISPATCH", "parallel") == "serial"
 # remote chunks are computed in groups of at least this many rows per launch
 _GROUP_ROWS = int(_os.environ.get("NIMG_EP_GROUP_ROWS", "12288"))
+# expert slices of the last remote chunk, each returned as soon as computed
+_RET_SPLIT = int(_os.environ.get("NIMG_EP_RET_SPLIT", "1"))
+# own experts computed before the remote chunks (-1: half)
+_OWN_A = int(_os.environ.get("NIMG_EP_OWN_A", "-1"))
 # NIMG_EP_BG_GATHER=1: the rank-local gather runs inside the first grouped
 # launch (background warps; the dispatch copies wait on per-chunk completion
 # counters). Off by default: measured equal at EP2 (1.280 vs 1.290 ms weak)
@@ -516,7 +520,7 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None,
     # right after the shared expert (together they cover the dispatch copies),
     # its second half last (covers the final return copy).
     El = plan.experts_per_rank
-    half = El // 2 if R > 1 else El
+    half = (min(El, max(0, _OWN_A)) if _OWN_A >= 0 else El // 2) if R > 1 else El
     blk = plan.block_rows
     own_x = xg[me * n:(me + 1) * n]
 
@@ -578,9 +582,35 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None,
     yslot, y_recv = yring.next()
     recv_all = tp.recv_t.view(R * n, d)
     y_all = y_recv.view(R * n, d)
-    for gi, grp in enumerate(plan.chunk_groups(_GROUP_ROWS)):
+    groups = plan.chunk_groups(_GROUP_ROWS)
+    for gi, grp in enumerate(groups):
         for src in grp:
             _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, DISP, src), k, comp.cuda_stream))
+        if len(grp) == 1 and gi == len(groups) - 1 and _RET_SPLIT > 1:
+            # the last remote chunk in expert slices, each returned as soon as
+            # it is computed: only the last slice's copy is left for the own
+            # second half to hide
+            src = grp[0]
+            st = tp.streams[src]
+            sh = st.cuda_stream
+            cuts = [El * i // _RET_SPLIT for i in range(_RET_SPLIT + 1)]
+            for i in range(_RET_SPLIT):
+                e0, e1 = cuts[i], cuts[i + 1]
+                if e1 <= e0:
+                    continue
+                r0, r1 = e0 * blk, e1 * blk
+                stages.expert_ffn(tp.recv_t[src][r0:r1], coff[e0:e1 + 1] - coff[e0], cex[e0:e1],
+                                  w.w1, w.w3, w.w2, None, None, None, None, y_routed=y_recv[src][r0:r1])
+                done = torch.cuda.Event()
+                done.record(comp)
+                st.wait_event(done)
+                if k > 1 and i == 0:   # src has combined the previous step: its y_back slot is free
+                    _lib.check(L.nimg_stream_wait_geq_u32(tp.flag(me, COMB, src), k - 1, sh))
+                _lib.check(L.nimg_copy_async(tp.yback.ptrs[src] + me * ybytes + r0 * d * tp.y_es,
+                                             y_recv[src][r0:r1].data_ptr(), (r1 - r0) * d * tp.y_es, sh))
+            _lib.check(L.nimg_stream_write_u32(tp.flag(src, RET, me), k, sh))
+            _mark(timeline, f"group{gi + 1}")
+            continue
         if len(grp) == 1:
             src = grp[0]
             stages.expert_ffn(tp.recv_t[src], coff, cex, w.w1, w.w3, w.w2, None, None, None, None,
