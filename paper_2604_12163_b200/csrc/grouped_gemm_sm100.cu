@@ -30,10 +30,15 @@ constexpr int kThreads = 192;
 constexpr int kATileBytes = BM * BK * 2;  // 16 KB
 
 template <int MODE> struct Cfg;
+// GEMM1 output columns per tile: 112 (h = 1344 = 12 x 112) or 128 (UMMA N =
+// 256; the last tile of a row block runs N = 128 in the pair kernel)
+#ifndef NIMG_G1_BN
+#define NIMG_G1_BN 112
+#endif
 template <> struct Cfg<0> {
-  static constexpr int BN_OUT = 112;                 // output columns per tile
-  static constexpr int BN_MMA = 224;                 // W1 half + W3 half
-  static constexpr int B_BOX = 112;                  // rows per TMA box (each of W1, W3)
+  static constexpr int BN_OUT = NIMG_G1_BN;          // output columns per tile
+  static constexpr int BN_MMA = 2 * NIMG_G1_BN;      // W1 half + W3 half
+  static constexpr int B_BOX = NIMG_G1_BN;           // rows per TMA box (each of W1, W3)
   static constexpr int STAGES = 4;
   static constexpr int kBTileBytes = BN_MMA * BK * 2;  // 28 KB
 };
@@ -279,7 +284,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
 // tmem_empty barrier. Each CTA's epilogue drains its own TMEM (its 128 rows).
 template <int MODE> struct PairCfg;
 template <> struct PairCfg<0> {
-  static constexpr int BN_OUT = 112, BN_MMA = 224, B_ROWS = 112, STAGES = 6;
+  static constexpr int BN_OUT = NIMG_G1_BN, BN_MMA = 2 * NIMG_G1_BN, B_ROWS = NIMG_G1_BN, STAGES = 6;
 };
 template <> struct PairCfg<1> {
   static constexpr int BN_OUT = 256, BN_MMA = 256, B_ROWS = 128, STAGES = 6;
@@ -289,6 +294,14 @@ template <int MODE, int STAGES = PairCfg<MODE>::STAGES>
 constexpr int pair_smem_bytes() { return STAGES * pair_stage_bytes<MODE>() + 1024 + 256; }
 
 constexpr int PBM = 256;  // rows per pair tile
+
+// GEMM1 with 128-column tiles: a row block's last tile holding <= 64 valid
+// columns runs at half width
+template <int MODE>
+NIMG_DEV bool pair_tail_tile(const GroupedParams& p, const TileInfo& ti) {
+  if (MODE != 0 || PairCfg<MODE>::BN_OUT != 128) return false;
+  return (ti.bank ? p.bank[1].N : p.bank[0].N) - ti.n0 <= PairCfg<MODE>::BN_OUT / 2;
+}
 
 template <int MODE>
 NIMG_DEV void decode_pair_tile(const GroupedParams& p, int t, TileInfo& ti) {
@@ -443,6 +456,10 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
     if (leader && lane == 0) {
       // ------------------------------------------------ MMA issuer (leader only)
       constexpr uint32_t idesc = make_idesc_bf16(PBM, C::BN_MMA);
+      // GEMM1 tail tile (<= BN_OUT / 2 valid columns): N = BN_MMA / 2 reads the
+      // first BN_OUT / 2 rows of each CTA's B slice (W1 | W3), so h3 lands at
+      // accumulator column BN_OUT / 2 (tail_tile(), epilogue)
+      constexpr uint32_t idesc_tail = make_idesc_bf16(PBM, C::BN_MMA / 2);
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
       for (int t = cluster_id; t < p.total_tiles; t += n_clusters) {
@@ -450,6 +467,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * 256;
+        const uint32_t id = pair_tail_tile<MODE>(p, ti) ? idesc_tail : idesc;
         for (int kb = 0; kb < ti.nk; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -459,7 +477,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
           const uint64_t bdesc = make_sdesc_k128(sb);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc, (kb | k) != 0);
+            umma_bf16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, id, (kb | k) != 0);
           umma_commit_cg2(&empty[stage], 0x3);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -591,13 +609,15 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
                                                                       : (int64_t)(ti.a_row + row);
       bf16* orow = reinterpret_cast<bf16*>(bk.out) + orow_i * bk.out_ld + ti.n0;
       const int oflags = ti.bank ? p.bank[1].flags : p.bank[0].flags;
+      const bool tail = pair_tail_tile<MODE>(p, ti);
+      const uint32_t hoff = tail ? C::B_ROWS / 2 : C::B_ROWS;   // h3's first accumulator column
 #pragma unroll 1
-      for (int c = 0; c < C::BN_OUT / 16; ++c) {
+      for (int c = 0; c < (tail ? C::BN_OUT / 32 : C::BN_OUT / 16); ++c) {
         uint32_t a[16], g[16];
         tmem_ld16(tb + c * 16, a);
         float v[16];
         if (MODE == 0) {
-          tmem_ld16(tb + C::B_ROWS + c * 16, g);
+          tmem_ld16(tb + hoff + c * 16, g);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = silu_mul(__uint_as_float(a[j]), __uint_as_float(g[j]));

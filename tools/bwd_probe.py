@@ -1,12 +1,13 @@
-"""Build timing-probe variants of the backward kernels (NIMG_BWD_PROBE) next to the
-library; tools/gpu_bwd_probe.sh times each with bench.py (A/B only: probe results are wrong)."""
+"""Build A/B variants of the library (timing probes NIMG_BWD_PROBE, tile configurations) next
+to the default one; tools/gpu_bwd_probe.sh times each with bench.py (A/B only: probe results are wrong)."""
 import os
 import sys
 
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 from paper_2604_12163_b200 import _build  # noqa: E402
 
-VARIANTS = {"probe1": ("NIMG_BWD_PROBE=1",), "probe2": ("NIMG_BWD_PROBE=2",), "staged": ("NIMG_W_SECTOR=0",)}
+VARIANTS = {"probe1": ("NIMG_BWD_PROBE=1",), "probe2": ("NIMG_BWD_PROBE=2",), "staged": ("NIMG_W_SECTOR=0",),
+            "g1bn128": ("NIMG_G1_BN=128",)}
 for tag in (sys.argv[1:] or VARIANTS):
     defs = VARIANTS[tag]
     out = os.path.join(os.path.dirname(_build.LIB), f"libnimg_moe_{tag}.so")
