@@ -352,7 +352,7 @@ def run_single(args, c, peaks, peak_kind):
                          gemm1_traffic() if c == CFG2 else None),
                      "traffic_unit": "bytes (dram read+write per launch, ncu)",
                      "peak_source": f"{peak_kind} bf16_tflops (burst)",
-                     "kernel_impl": "grouped_gemm_sm100_pair<0>: tcgen05 cta_group::2, UMMA 256x224x16" + (
+                     "kernel_impl": "grouped_gemm_sm100_pair<0>: tcgen05 cta_group::2, UMMA 256x256x16 (last tile of a row block 256x128)" + (
                          "; the routed-row gather (537 MB of copies) runs inside it on background warps"
                          if os.environ.get("NIMG_BG_GATHER", "1") != "0" else ""),
                      "algorithmic": f"4*d*h*(R_rows+T) = {wc['flops_g1']:.4g} FLOP per launch"},

@@ -30,10 +30,12 @@ constexpr int kThreads = 192;
 constexpr int kATileBytes = BM * BK * 2;  // 16 KB
 
 template <int MODE> struct Cfg;
-// GEMM1 output columns per tile: 112 (h = 1344 = 12 x 112) or 128 (UMMA N =
-// 256; the last tile of a row block runs N = 128 in the pair kernel)
+// GEMM1 output columns per tile: 128 (UMMA N = 256; at h = 1344 = 10 x 128 +
+// 64 the last tile of a row block runs N = 128 in the pair kernel), or 112
+// (h = 12 x 112, N = 224). 128 measured ~1% faster at cfg2 (GEMM1 652 vs 659 us,
+// two runs each, profiles/r02_g1_variants.txt): 7% fewer operand bytes per MMA.
 #ifndef NIMG_G1_BN
-#define NIMG_G1_BN 112
+#define NIMG_G1_BN 128
 #endif
 template <> struct Cfg<0> {
   static constexpr int BN_OUT = NIMG_G1_BN;          // output columns per tile
