@@ -6,22 +6,24 @@
 // an 8-bit significand and an fp32 W_r a 24-bit one, so the x half is an exact
 // sum of integers once both sides are written in fixed point:
 //
-//   x[t, k] = X[t, k] * 2^(e_t - 134 - XW), |X| < 2^(XW+8)  (row scale;
-//             base-128 digits (LX = 4) X_i: X = sum_i X_i 128^(LX-1-i), the top digit
-//             signed, the others unsigned 7-bit)
-//   w[k, e] = W[k, e] * 2^(ew_e - 161),     |W| < 2^35       (column scale, 5
-//             sign-magnitude digits)
+//   x[t, k] = X[t, k] * 2^(e_t - 134 - XW), |X| < 2^(XW+8) = 2^31  (row scale)
+//   w[k, e] = W[k, e] * 2^(ew_e - WEXP),    |W| < 2^39                (column scale)
 //
-// and sum_k X W = sum_s G_s 128^(NG-1-s), G_s = sum_{i+j=s} sum_k X_i W_j,
+// Both are cut into base-256 digits, two's complement: X = sum_i X_i 256^(3-i)
+// and W = sum_j W_j 256^(4-j), the top digit signed and the others unsigned
+// bytes. Then sum_k X W = sum_s G_s 256^(7-s), G_s = sum_{i+j=s} sum_k X_i W_j,
 // where every G_s is an int8 x int8 GEMM with int32 accumulation: EXACT, in any
-// order (tcgen05.mma kind::i8: per K step, digit i x [W_0|W_1|W_2|W_3] (N = 256)
-// lands on TMEM groups i..i+3 and digit i x W_4 (N = 64) on group i+4).
+// order (tcgen05.mma kind::i8, whose A / B signedness is per instruction: per
+// K step, digit i x W_0 (N = 64, B signed) lands on TMEM group i and digit i x
+// [W_1|W_2|W_3|W_4] (N = 256, B unsigned) on groups i+1..i+4). (NIMG_I8_B256=0
+// builds the round-1/2 scheme: 7-bit balanced / sign-magnitude digits, 28-bit x
+// and 35-bit W windows.)
 // Elements outside the fixed-point windows are not lost: a W element below
-// 2^-11 of its column max becomes an exact f64 correction term (a per-expert
+// 2^-15 of its column max becomes an exact f64 correction term (a per-expert
 // list of up to CORR_MAX, ascending k), and an x element outside its row's XW-binade window (the
 // scale is guessed from the row's first 128 elements, XH binades of headroom)
 // becomes an exact f64 term in a per-row list; a row whose list overflows is
-// recomputed by the f64 fix-up kernel. The epilogue forms v = H 2^28 + L
+// recomputed by the f64 fix-up kernel. The epilogue forms v = H 2^32 + L
 // exactly in int64 halves, scales by a power of two, adds the corrections and
 // the f64 t-bias, rounds to fp32 and PROVES the rounding: if the f64 value is
 // not farther than its error bound from an fp32 rounding boundary, the token is
@@ -75,11 +77,27 @@ NIMG_DEV uint64_t sdesc_k(uint32_t addr) {
 #ifndef NIMG_I8_LX
 #define NIMG_I8_LX 4
 #endif
-constexpr int LX = NIMG_I8_LX, LW = 5, NG = LX + LW - 1;
-// binades of the x window: 12 or 19. |X| < 2^(7 LX - 1) keeps every balanced
-// digit of the fast path (below) within [-64, 64] and the top digit of the
-// slow path's two's-complement split within [-64, 63].
-constexpr int XW = 7 * LX - 9;
+// Digit base. 256 (default): x and W are two's-complement integers cut into
+// bytes -- the top byte signed, the others unsigned (tcgen05 kind::i8 takes the
+// signedness of A and B per instruction) -- with a 32-bit x window (24
+// binades) and a 40-bit W window. 128: balanced / sign-magnitude 7-bit digits,
+// 28-bit x window (19 binades), 35-bit W window (the round-1/2 scheme).
+#ifndef NIMG_I8_B256
+#define NIMG_I8_B256 1
+#endif
+constexpr bool B256 = NIMG_I8_B256;
+constexpr int LX = B256 ? 4 : NIMG_I8_LX, LW = 5, NG = LX + LW - 1;
+static_assert(!B256 || LX == 4, "base 256 uses 4 x digits");
+// binades of the x window: 12 or 19 (base 128; |X| < 2^(7 LX - 1) keeps every
+// balanced digit of the fast path within [-64, 64] and the top digit of the
+// slow path's two's-complement split within [-64, 63]), 23 (base 256: |X| <
+// 2^31, an int32)
+constexpr int XW = B256 ? 23 : 7 * LX - 9;
+constexpr int DB = B256 ? 8 : 7;             // bits per digit
+// W column window: the column max's 24-bit significand M lands as M << WSH
+// (base 256: |W| < 2^39, a signed 40-bit integer; base 128: 35-bit magnitude)
+constexpr int WSH = B256 ? LW * DB - 25 : LW * DB - 24;
+constexpr int WEXP = 150 + WSH;              // w = W * 2^(ew - WEXP)
 // Fast-path conversion on the FMA pipe (NIMG_I8_FCONV=0: the integer path)
 #ifndef NIMG_I8_FCONV
 #define NIMG_I8_FCONV 1
@@ -181,6 +199,9 @@ NIMG_DEV uint32_t spread_signed(uint32_t X) {
   if (LX == 4) X += X & ~0x7FFFFFu;
   return X;
 }
+// X (|X| < 2^(DB LX - 1), two's complement) -> its digits, byte i = digit i
+// from the bottom: base 256 is X itself
+NIMG_DEV uint32_t spread_digits(uint32_t X) { return B256 ? X : spread_signed(X); }
 // per-byte negation of digits in [0, 127]
 NIMG_DEV uint32_t neg_bytes(uint32_t Y) { return (0x80808080u - Y) ^ 0x80808080u; }
 NIMG_DEV void bar_conv() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
@@ -223,12 +244,27 @@ NIMG_DEV void digits_fma(float x, float scale, uint32_t (&t)[LXD]) {
   }
 }
 
+// Base-256 fast path. X = x * 2^(134 + XW - e_t) is an integer, |X| < 2^31:
+//   t = RD(X + 1.5*2^39)   (fma.rm) = 1.5*2^39 + q 2^16, q = floor(X / 2^16):
+//                          t's low 16 mantissa bits are q (two's complement),
+//                          the top digit (signed) and digit 2 (unsigned)
+//   r = X - q 2^16         exact, 0 <= r < 2^16
+//   u = r + 1.5*2^23       u's low 16 bits are r: digits 1 and 0 (unsigned)
+// so X = D3 2^24 + D2 2^16 + D1 2^8 + D0 exactly, in 4 FMA-pipe operations.
+NIMG_DEV void digits_b256(float x, float scale, uint32_t& hi, uint32_t& lo) {
+  constexpr float MH = 824633720832.0f, ML = 12582912.0f;   // 1.5 * 2^39, 1.5 * 2^23
+  const float t = __fmaf_rd(x, scale, MH);
+  const float r = fmaf(x, scale, -(t - MH));
+  hi = __float_as_uint(t);
+  lo = __float_as_uint(r + ML);
+}
+
 // ------------------------------------------------------------------ prep
 // blocks [0, B*KS): t-half partials (shared with the DMMA router).
 // blocks [B*KS, + 64): block e owns expert column e: the column's max exponent,
 // its five W digit planes written straight into the smem image the scores
 // kernel bulk-copies (K-major, 128-B swizzle), and the exact corrections of
-// the elements below the 35-bit column window, in ascending k.
+// the elements below the column window (WSH + 24 bits), in ascending k.
 __global__ void __launch_bounds__(256)
 router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
                       double* __restrict__ part, Ws ws, int B, int d) {
@@ -270,7 +306,7 @@ router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__
         const int e8 = (int)(mag >> 23);
         const uint32_t M = (mag & 0x7FFFFFu) | (e8 ? 0x800000u : 0u);
         const int ee = max(e8, 1);
-        const int sh = ee - ew + 11;
+        const int sh = ee - ew + WSH;
         uint64_t Wi;
         uint32_t res = 0;
         if (sh >= 0) {
@@ -283,11 +319,17 @@ router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__
         has[q] = res != 0u;
         // w - w~ = sign * res * 2^(ee - 150): exact in f64
         dw[q] = ((u >> 31) ? -1.0 : 1.0) * (double)res * pow2(ee - 150);
+        if (B256) {   // two's complement, byte j from the top (byte 0 signed)
+          const int64_t Ws = (u >> 31) ? -(int64_t)Wi : (int64_t)Wi;
 #pragma unroll
-        for (int j = 0; j < LW; ++j) {
-          uint32_t dj = (uint32_t)(Wi >> (7 * (LW - 1 - j))) & 0x7Fu;
-          if (u >> 31) dj = (0x80u - dj) ^ 0x80u;
-          dig[j] |= (dj & 0xFFu) << (8 * q);
+          for (int j = 0; j < LW; ++j) dig[j] |= ((uint32_t)(Ws >> (8 * (LW - 1 - j))) & 0xFFu) << (8 * q);
+        } else {      // sign-magnitude 7-bit digits
+#pragma unroll
+          for (int j = 0; j < LW; ++j) {
+            uint32_t dj = (uint32_t)(Wi >> (7 * (LW - 1 - j))) & 0x7Fu;
+            if (u >> 31) dj = (0x80u - dj) ^ 0x80u;
+            dig[j] |= (dj & 0xFFu) << (8 * q);
+          }
         }
       }
       const int kb = kq / KB, kin = kq % KB;
@@ -456,7 +498,25 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
         }
         const bool fast = min(mn & 0xFFFFu, mn >> 16) >= lo7[jj] && max(mxe & 0xFFFFu, mxe >> 16) <= hi7[jj];
         uint32_t out[LX][4];
-        if (fast && sok[jj]) {
+        if (B256 && fast && sok[jj]) {
+#pragma unroll
+          for (int g = 0; g < 4; ++g) {
+            uint32_t th[4], tl[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t w = wv[2 * g + (q >> 1)];
+              const float xv = __uint_as_float((q & 1) ? (w & 0xFFFF0000u) : (w << 16));
+              digits_b256(xv, xscale[jj], th[q], tl[q]);
+            }
+            // bytes 1 / 0 of th: digits 3 (top, signed) / 2; of tl: digits 1 / 0
+            const uint32_t h01 = __byte_perm(th[0], th[1], 0x5140), h23 = __byte_perm(th[2], th[3], 0x5140);
+            const uint32_t l01 = __byte_perm(tl[0], tl[1], 0x5140), l23 = __byte_perm(tl[2], tl[3], 0x5140);
+            out[0][g] = __byte_perm(h01, h23, 0x7632);
+            out[1][g] = __byte_perm(h01, h23, 0x5410);
+            out[2][g] = __byte_perm(l01, l23, 0x7632);
+            out[3][g] = __byte_perm(l01, l23, 0x5410);
+          }
+        } else if (!B256 && fast && sok[jj]) {
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
             uint32_t tb[4][LX];
@@ -480,8 +540,8 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
             const int ml = (int)(w << 16) >> 31, mh = (int)w >> 31;
             const uint32_t sl = ((((w & 0x7Fu) | 0x80u) ^ (uint32_t)ml) - (uint32_t)ml);
             const uint32_t shv = ((((w >> 16) & 0x7Fu) | 0x80u) ^ (uint32_t)mh) - (uint32_t)mh;
-            Y[2 * i] = spread_signed(sl << (((w >> 7) & 0xFFu) + base[jj]));
-            Y[2 * i + 1] = spread_signed(shv << (((w >> 23) & 0xFFu) + base[jj]));
+            Y[2 * i] = spread_digits(sl << (((w >> 7) & 0xFFu) + base[jj]));
+            Y[2 * i + 1] = spread_digits(shv << (((w >> 23) & 0xFFu) + base[jj]));
           }
         } else {
 #pragma unroll
@@ -500,7 +560,7 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
               }
             } else {
               const uint32_t m = (u & 0x8000u) ? 0xFFFFFFFFu : 0u;
-              Y[el] = spread_signed(((((u & 0x7Fu) | 0x80u) ^ m) - m) << sh);
+              Y[el] = spread_digits(((((u & 0x7Fu) | 0x80u) ^ m) - m) << sh);
             }
           }
         }
@@ -590,18 +650,25 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
       for (int s = 0; s < NG; ++s) tmem_ld4(tl + s * NE + e0, g[s]);
       tmem_ld_wait();
       // the four logits of this column quad side by side (independent chains)
-      double v4[4], cs4[4], ca4[4];
+      double v4[4], cs4[4], ca4[4], hl4[4];
       int ncs4[4], cmax = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int e = e0 + j;
-        // v = sum_s G_s 128^(NG-1-s) = H 2^28 + L, H and L exact in int64
-        int64_t H = 0;
+        // v = sum_s G_s base^(NG-1-s) = H 2^(4 DB) + L, H and L exact in int64
+        int64_t H = 0, L = 0;
 #pragma unroll
-        for (int s = 0; s < NG - 4; ++s) H = H * 128 + (int64_t)(int)g[s][j];
-        const int64_t L = (int64_t)(int)g[NG - 4][j] * 2097152 + (int64_t)(int)g[NG - 3][j] * 16384 +
-                          (int64_t)(int)g[NG - 2][j] * 128 + (int64_t)(int)g[NG - 1][j];
-        v4[j] = fma((double)H, 268435456.0, (double)L) * pow2(er + wew[e] - 295 - XW);
+        for (int s = 0; s < NG - 4; ++s) H = H * (1 << DB) + (int64_t)(int)g[s][j];
+#pragma unroll
+        for (int s = NG - 4; s < NG; ++s) L = L * (1 << DB) + (int64_t)(int)g[s][j];
+        // base 256: H and L may exceed 2^53 (d > 2048), so their conversions
+        // are inexact in general; hl4 bounds those roundings for the proof
+        const double Hd = (double)H, Ld = (double)L;
+        v4[j] = fma(Hd, B256 ? 4294967296.0 : 268435456.0, Ld);
+        hl4[j] = B256 ? fabs(Hd) * 4294967296.0 + fabs(Ld) : 0.0;
+        const double sc = pow2(er + wew[e] - 134 - WEXP - XW);
+        v4[j] *= sc;
+        hl4[j] *= sc;
         cs4[j] = 0.0;
         ca4[j] = 0.0;
         ncs4[j] = wcn[e];
@@ -648,8 +715,9 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
           ca += fabs(pr);
         }
         const double z = (v + cs) + tbr[e];
-        // rounding of v, of the correction sums and of the two adds
-        const double bound = (2.0 * fabs(v) + (ncw + nxu + 2) * ca + fabs(z)) * 0x1p-52;
+        // rounding of v (and of its halves' conversions), of the correction sums
+        // and of the two adds
+        const double bound = (2.0 * fabs(v) + hl4[j] + (ncw + nxu + 2) * ca + fabs(z)) * 0x1p-52;
         const float rf = __double2float_rn(z);
         // rf is the rounding of every value within `bound` of z iff that band
         // stays strictly inside rf's rounding interval [|rf| - hd, |rf| + hu]
@@ -704,6 +772,9 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
       // i..i+3; W_4 (N = 64) on group i+4.
       constexpr uint32_t idesc256 = make_idesc_s8(BM, 4 * NE);
       constexpr uint32_t idesc64 = make_idesc_s8(BM, NE);
+      // base 256: A is signed for the top x digit only, B for W_0 only; idesc
+      // bit 7 / 10 = A / B signed
+      constexpr uint32_t kASigned = 1u << 7, kBSigned = 1u << 10;
       int stage = 0;
       uint32_t phase = 0;
       for (int kb = 0; kb < nkb; ++kb) {
@@ -714,9 +785,28 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
         const uint32_t sw = sa + LX * A_SLICE;
         const uint64_t b03 = sdesc_k(sw);
         const uint64_t b4 = sdesc_k(sw + 4 * W_SLICE);
+        const uint64_t b0 = b03, b14 = sdesc_k(sw + W_SLICE);
 #pragma unroll
         for (int kk = 0; kk < KB / 32; ++kk) {
           const bool first = kb == 0 && kk == 0;
+          if constexpr (B256) {
+            // x digit i times W_0 (N = 64, signed B) lands on TMEM group i and
+            // times [W_1 | W_2 | W_3 | W_4] (N = 256, unsigned B) on groups
+            // i+1..i+4. Digits run top-down from i = 3 so that, in the first K
+            // step, every MMA either starts all its groups or accumulates onto
+            // groups already started.
+#pragma unroll
+            for (int i = LX - 1; i >= 0; --i) {
+              const uint64_t adesc = sdesc_k(sa + i * A_SLICE) + 2 * kk;
+              const uint32_t as = i == 0 ? kASigned : 0u;
+              if (NIMG_I8_PROBE != 2) {
+                umma_i8(tmem_base + i * NE, adesc, b0 + 2 * kk, (idesc64 & ~(kASigned | kBSigned)) | as | kBSigned,
+                        first ? 0u : 1u);
+                umma_i8(tmem_base + (i + 1) * NE, adesc, b14 + 2 * kk, (idesc256 & ~(kASigned | kBSigned)) | as,
+                        (first && i == LX - 1) ? 0u : 1u);
+              }
+            }
+          } else {
 #pragma unroll
           for (int i = 0; i < LX; ++i) {
             const uint64_t adesc = sdesc_k(sa + i * A_SLICE) + 2 * kk;
@@ -724,6 +814,7 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
               umma_i8(tmem_base + i * NE, adesc, b03 + 2 * kk, idesc256, (first && i == 0) ? 0u : 1u);
               umma_i8(tmem_base + (i + 4) * NE, adesc, b4 + 2 * kk, idesc64, first ? 0u : 1u);
             }
+          }
           }
         }
         umma_commit(&empty[stage]);
@@ -834,7 +925,8 @@ bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm) {
   // read per call (a getenv is ~100 ns) so tests can compare both routers in one process
   const char* v = getenv("NIMG_ROUTER");
   if (v && (!strcmp(v, "dmma") || !strcmp(v, "f64"))) return false;
-  return x_bf16 && E == ri8::NE && d % ri8::KB == 0 && d <= 32768 &&
+  // int32 group sums: <= 4 digit pairs x d x 255^2 < 2^31 for d <= 8192 (base 256)
+  return x_bf16 && E == ri8::NE && d % ri8::KB == 0 && d <= (ri8::B256 ? 8192 : 32768) &&
          (uintptr_t)x_norm % 16 == 0;
 }
 size_t router_i8_ws_bytes(int64_t T, int d) { return ri8::ws_bytes(T, d); }
