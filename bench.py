@@ -46,9 +46,9 @@ FP64_PEAK_TFLOPS = 37.0
 
 def router_uses_i8(c) -> bool:
     """Mirror of router_i8_eligible (csrc/router_i8.cu): bf16 x_norm, E = 64,
-    d % 128 == 0, unless NIMG_ROUTER=dmma."""
+    d % 64 == 0, d <= 8192, unless NIMG_ROUTER=dmma."""
     return (os.environ.get("NIMG_ROUTER") not in ("dmma", "f64") and c["E"] == 64
-            and c["d"] % 128 == 0)
+            and c["d"] % 64 == 0 and c["d"] <= 8192)
 
 
 def router_impl(c) -> str:

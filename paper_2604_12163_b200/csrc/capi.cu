@@ -612,7 +612,7 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const void* t_emb_v, 
   // caller-owned).
   if (!router_uses_dmma(E))
     CUDA_TRY(cudaMemsetAsync(w.counters, 0xFF, (size_t)B * 4, st));
-  if (router_i8_eligible(xn_bf16, dd, E, x_norm))
+  if (router_i8_eligible(xn_bf16, dd, E, x_norm, w_r))
     CUDA_TRY(launch_router_i8(x_norm, t_emb, w_r, w.part, w.i8, logits, scores_bes, B, S, dd, st));
   else
     CUDA_TRY(launch_router(xn_bf16, x_norm, t_emb, w_r, w.tb, w.part, w.counters, w.wd, logits,

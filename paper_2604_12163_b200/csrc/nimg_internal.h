@@ -214,7 +214,7 @@ cudaError_t launch_router(bool x_bf16, const void* x_norm, const float* t_emb, c
 size_t router_wd_bytes(int d, int E);
 // Exact INT8 tensor-core router (router_i8.cu): bf16 x_norm, E == 64, d % 128 == 0.
 // NIMG_ROUTER=dmma forces the FP64 router.
-bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm);
+bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm, const void* w_r);
 size_t router_i8_ws_bytes(int64_t T, int d);
 cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float* w_r, double* part,
                              void* i8ws, float* logits, float* scores_bes, int B, int S, int d,

@@ -86,13 +86,12 @@ NIMG_DEV uint64_t sdesc_k(uint32_t addr) {
 #define NIMG_I8_B256 1
 #endif
 constexpr bool B256 = NIMG_I8_B256;
-constexpr int LX = B256 ? 4 : NIMG_I8_LX, LW = 5, NG = LX + LW - 1;
-static_assert(!B256 || LX == 4, "base 256 uses 4 x digits");
+constexpr int LX = NIMG_I8_LX, LW = 5, NG = LX + LW - 1;
 // binades of the x window: 12 or 19 (base 128; |X| < 2^(7 LX - 1) keeps every
 // balanced digit of the fast path within [-64, 64] and the top digit of the
 // slow path's two's-complement split within [-64, 63]), 23 (base 256: |X| <
 // 2^31, an int32)
-constexpr int XW = B256 ? 23 : 7 * LX - 9;
+constexpr int XW = B256 ? 8 * LX - 9 : 7 * LX - 9;
 constexpr int DB = B256 ? 8 : 7;             // bits per digit
 // W column window: the column max's 24-bit significand M lands as M << WSH
 // (base 256: |W| < 2^39, a signed 40-bit integer; base 128: 35-bit magnitude)
@@ -116,7 +115,7 @@ NIMG_DEV uint64_t gtimer() {
 #ifndef NIMG_I8_PROBE
 #define NIMG_I8_PROBE 0
 #endif
-constexpr int XH = LX == 3 ? 1 : 2;          // headroom over the first-stage max
+constexpr int XH = LX == 3 ? 1 : 2;          // headroom over the first-stage max (binades)
 static_assert(LX == 3 || LX == 4, "x digit planes");
 constexpr int A_SLICE = BM * KB;             // 8 / 16 KB
 constexpr int W_SLICE = NE * KB;             // 4 / 8 KB
@@ -247,10 +246,12 @@ NIMG_DEV void digits_fma(float x, float scale, uint32_t (&t)[LXD]) {
 // Base-256 fast path. X = x * 2^(134 + XW - e_t) is an integer, |X| < 2^31:
 //   t = RD(X + 1.5*2^39)   (fma.rm) = 1.5*2^39 + q 2^16, q = floor(X / 2^16):
 //                          t's low 16 mantissa bits are q (two's complement),
-//                          the top digit (signed) and digit 2 (unsigned)
+//                          the top digit (signed) and digit 2 (unsigned); with
+//                          LX = 3 (|X| < 2^23) q is the top digit itself
 //   r = X - q 2^16         exact, 0 <= r < 2^16
 //   u = r + 1.5*2^23       u's low 16 bits are r: digits 1 and 0 (unsigned)
-// so X = D3 2^24 + D2 2^16 + D1 2^8 + D0 exactly, in 4 FMA-pipe operations.
+// so X = D3 2^24 + D2 2^16 + D1 2^8 + D0 exactly, in 4 FMA-pipe operations
+// (LX = 3: X = D2 2^16 + D1 2^8 + D0).
 NIMG_DEV void digits_b256(float x, float scale, uint32_t& hi, uint32_t& lo) {
   constexpr float MH = 824633720832.0f, ML = 12582912.0f;   // 1.5 * 2^39, 1.5 * 2^23
   const float t = __fmaf_rd(x, scale, MH);
@@ -508,13 +509,14 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
               const float xv = __uint_as_float((q & 1) ? (w & 0xFFFF0000u) : (w << 16));
               digits_b256(xv, xscale[jj], th[q], tl[q]);
             }
-            // bytes 1 / 0 of th: digits 3 (top, signed) / 2; of tl: digits 1 / 0
+            // LX = 4: bytes 1 / 0 of th are digits 3 (top, signed) / 2; LX = 3:
+            // byte 0 of th is digit 2 (top, signed). Bytes 1 / 0 of tl: digits 1 / 0.
             const uint32_t h01 = __byte_perm(th[0], th[1], 0x5140), h23 = __byte_perm(th[2], th[3], 0x5140);
             const uint32_t l01 = __byte_perm(tl[0], tl[1], 0x5140), l23 = __byte_perm(tl[2], tl[3], 0x5140);
-            out[0][g] = __byte_perm(h01, h23, 0x7632);
-            out[1][g] = __byte_perm(h01, h23, 0x5410);
-            out[2][g] = __byte_perm(l01, l23, 0x7632);
-            out[3][g] = __byte_perm(l01, l23, 0x5410);
+            if (LX == 4) out[0][g] = __byte_perm(h01, h23, 0x7632);
+            out[LX - 3][g] = __byte_perm(h01, h23, 0x5410);
+            out[LX - 2][g] = __byte_perm(l01, l23, 0x7632);
+            out[LX - 1][g] = __byte_perm(l01, l23, 0x5410);
           }
         } else if (!B256 && fast && sok[jj]) {
 #pragma unroll
@@ -703,17 +705,36 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
           }
         }
       }
+      // (x - x~) * w for the row's listed x elements: the four logits' W values
+      // are one 16-B load per element, all of them in flight at once
+      double xs4[4] = {0.0, 0.0, 0.0, 0.0}, xa4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (nxu > 0) {
+        float4 wl[XC_MAX];
+#pragma unroll
+        for (int c = 0; c < XC_MAX; ++c)
+          if (c < nxu) wl[c] = __ldg(reinterpret_cast<const float4*>(w_r + (int64_t)xck[r * XC_MAX + c] * NE + e0));
+#pragma unroll
+        for (int c = 0; c < XC_MAX; ++c) {
+          if (c < nxu) {
+            const double xv = (double)xcv[r * XC_MAX + c];
+            const double pr[4] = {xv * (double)wl[c].x, xv * (double)wl[c].y, xv * (double)wl[c].z,
+                                  xv * (double)wl[c].w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              xs4[j] += pr[j];
+              xa4[j] += fabs(pr[j]);
+            }
+          }
+        }
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int e = e0 + j;
         const double v = v4[j];
         double cs = cs4[j], ca = ca4[j];
         const int ncw = wcn[e];
-        for (int c = 0; c < nxu; ++c) {   // (x - x~) * w for the listed elements
-          const double pr = (double)xcv[r * XC_MAX + c] * (double)__ldg(w_r + (int64_t)xck[r * XC_MAX + c] * NE + e);
-          cs += pr;
-          ca += fabs(pr);
-        }
+        cs += xs4[j];   // (x - x~) * w for the listed elements (below)
+        ca += xa4[j];
         const double z = (v + cs) + tbr[e];
         // rounding of v (and of its halves' conversions), of the correction sums
         // and of the two adds
@@ -921,13 +942,13 @@ router_fix_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_r,
 
 }  // namespace ri8
 
-bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm) {
+bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm, const void* w_r) {
   // read per call (a getenv is ~100 ns) so tests can compare both routers in one process
   const char* v = getenv("NIMG_ROUTER");
   if (v && (!strcmp(v, "dmma") || !strcmp(v, "f64"))) return false;
   // int32 group sums: <= 4 digit pairs x d x 255^2 < 2^31 for d <= 8192 (base 256)
   return x_bf16 && E == ri8::NE && d % ri8::KB == 0 && d <= (ri8::B256 ? 8192 : 32768) &&
-         (uintptr_t)x_norm % 16 == 0;
+         (uintptr_t)x_norm % 16 == 0 && (uintptr_t)w_r % 16 == 0;
 }
 size_t router_i8_ws_bytes(int64_t T, int d) { return ri8::ws_bytes(T, d); }
 
