@@ -10,7 +10,9 @@ VARIANTS = {"probe1": ("NIMG_BWD_PROBE=1",), "probe2": ("NIMG_BWD_PROBE=2",), "s
             "g1bn112": ("NIMG_G1_BN=112",), "b128": ("NIMG_I8_B256=0",),
             "trace": ("NIMG_I8_TRACE=1",), "trace_nomma": ("NIMG_I8_TRACE=1", "NIMG_I8_PROBE=2"),
             "trace_noconv": ("NIMG_I8_TRACE=1", "NIMG_I8_PROBE=1"), "lx3": ("NIMG_I8_LX=3",),
-            "lx3_trace": ("NIMG_I8_LX=3", "NIMG_I8_TRACE=1")}
+            "lx3_trace": ("NIMG_I8_LX=3", "NIMG_I8_TRACE=1"),
+            "kb128": ("NIMG_I8_KB=128",), "intconv": ("NIMG_I8_FCONV=0",), "noconv": ("NIMG_I8_PROBE=1",),
+            "nomma": ("NIMG_I8_PROBE=2",), "noepi": ("NIMG_I8_PROBE=3",)}
 for tag in (sys.argv[1:] or VARIANTS):
     defs = VARIANTS[tag]
     out = os.path.join(os.path.dirname(_build.LIB), f"libnimg_moe_{tag}.so")

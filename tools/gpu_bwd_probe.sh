@@ -1,4 +1,4 @@
-# backward stage times of the default library and variant builds (tools/bwd_probe.py)
+# backward stage times of the default library and variant builds (tools/build_variants.py)
 # usage: bash tools/gpu_bwd_probe.sh [variant ...]   (default: probe1 probe2)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out

@@ -1,4 +1,4 @@
-# per-CTA %globaltimer traces of the INT8 router (tools/bwd_probe.py trace variants)
+# per-CTA %globaltimer traces of the INT8 router (tools/build_variants.py trace variants)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 TAG=${1:-trace}

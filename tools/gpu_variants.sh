@@ -1,4 +1,4 @@
-# A/B of library variants (tools/bwd_probe.py): parity + backward tests and a bench line each
+# A/B of library variants (tools/build_variants.py): parity + backward tests and a bench line each
 # usage: bash tools/gpu_variants.sh TAG variant ...
 cd $GRAFT_REPO_ROOT
 TAG=$1; shift
