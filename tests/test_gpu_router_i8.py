@@ -2,11 +2,13 @@
 and against the FP64 (DMMA) router: fp32 logits, affinities, the token
 permutation and the gates must be bit-identical (router.py:120-143).
 
-The int8 path takes bf16 x_norm with E == 64 and d % 128 == 0; these tests
-also drive its escape hatches: x elements below the 28-bit row window (row
-recomputed in f64), W_r elements below the 35-bit column window (exact
-correction terms), too many of those (every token recomputed), non-finite
-inputs, zero rows, subnormals and partial / sample-straddling tiles.
+The int8 path takes bf16 x_norm with E == 64, d % 64 == 0 and d <= 8192
+(base-256 digits: a 32-bit row window, a 40-bit column window); these tests
+also drive its escape hatches: x elements outside the row window (exact f64
+terms, or the row recomputed in f64), W_r elements below the column window
+(exact correction terms), too many of those (every token recomputed),
+non-finite inputs, zero rows, subnormals, partial / sample-straddling tiles,
+and K = 4096 / 8192 with digit sums near the int32 and 2^53 limits.
 """
 
 import os
@@ -79,8 +81,8 @@ def test_i8_router_full_width(B, S, seed):
 
 
 def test_i8_router_window_escapes():
-    """x elements below 2^-20 of their row max (the row is recomputed in f64),
-    W_r elements below 2^-11 of their column max (exact corrections), zero
+    """x elements far below their row max (exact f64 terms / the row
+    recomputed in f64), W_r elements below 2^-15 of their column max (exact corrections), zero
     rows, subnormal bf16 values, a row with a huge dynamic range."""
     rng = np.random.default_rng(11)
     inp = make_router_inputs(7, 2, 512, 1024, 64, mode="bf16")
@@ -138,3 +140,20 @@ def test_i8_router_repeatable():
     _, b = _gpu_route(inp, 2.0)
     np.testing.assert_array_equal(np_of(a["logits"]), np_of(b["logits"]))
     np.testing.assert_array_equal(a["token_flat"].cpu().numpy(), b["token_flat"].cpu().numpy())
+
+
+@pytest.mark.parametrize("d", [4096, 8192])
+def test_i8_router_wide_k(d):
+    """K = 4096 and 8192 (the int8 path's limit): random inputs, then
+    same-sign inputs at the top of both windows, where every int32 digit-group
+    sum is near its bound and the int64 halves exceed 2^53 (their conversions
+    round; the rounding proof accounts for it)."""
+    inp = make_router_inputs(13, 1, 256, d, 64, mode="bf16")
+    _check(inp, 4.0)
+    rng = np.random.default_rng(14)
+    x = np.full((1, 128, d), 1.9921875, np.float32)          # 0x3FFF: the largest bf16 significand
+    x[:, :, ::7] = -1.9921875
+    inp["x_norm"] = bf16_round(x * rng.uniform(0.5, 1.0, (1, 128, 1)).astype(np.float32))
+    w = np.float32(0.0059) * (1.0 + rng.uniform(0.0, 2.0 ** -20, (2 * d, 64))).astype(np.float32)
+    inp["w_r"] = w.astype(np.float32)
+    _check(inp, 8.0)
