@@ -268,6 +268,21 @@ NIMG_DEV void tmem_ld16x256(uint32_t taddr, uint32_t (&r)[16]) {
         "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
+// 32 contiguous bytes from one thread: one 256-bit store (STG.256, a whole L2
+// sector) when 32-B aligned, else two 16-B stores. NIMG_ST256=0: always two.
+#ifndef NIMG_ST256
+#define NIMG_ST256 1
+#endif
+NIMG_DEV void st_global_32(void* p, uint4 lo, uint4 hi) {
+  if (NIMG_ST256 && (reinterpret_cast<uintptr_t>(p) & 31u) == 0u) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(lo.x), "r"(lo.y),
+                 "r"(lo.z), "r"(lo.w), "r"(hi.x), "r"(hi.y), "r"(hi.z), "r"(hi.w)
+                 : "memory");
+  } else {
+    reinterpret_cast<uint4*>(p)[0] = lo;
+    reinterpret_cast<uint4*>(p)[1] = hi;
+  }
+}
 NIMG_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, K-major operand, 128B swizzle: 8-row atoms of

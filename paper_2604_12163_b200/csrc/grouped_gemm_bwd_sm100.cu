@@ -397,10 +397,8 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
               }
               uint4* d1 = reinterpret_cast<uint4*>(o + n);
               uint4* d3 = reinterpret_cast<uint4*>(o + h + n);
-              d1[0] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
-              d1[1] = make_uint4(p1[4], p1[5], p1[6], p1[7]);
-              d3[0] = make_uint4(p3[0], p3[1], p3[2], p3[3]);
-              d3[1] = make_uint4(p3[4], p3[5], p3[6], p3[7]);
+              st_global_32(d1, make_uint4(p1[0], p1[1], p1[2], p1[3]), make_uint4(p1[4], p1[5], p1[6], p1[7]));
+              st_global_32(d3, make_uint4(p3[0], p3[1], p3[2], p3[3]), make_uint4(p3[4], p3[5], p3[6], p3[7]));
             }
           }
           __syncwarp();
@@ -460,10 +458,8 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
             }
             uint4* d1 = reinterpret_cast<uint4*>(o + n);
             uint4* d3 = reinterpret_cast<uint4*>(o + h + n);
-            d1[0] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
-            d1[1] = make_uint4(p1[4], p1[5], p1[6], p1[7]);
-            d3[0] = make_uint4(p3[0], p3[1], p3[2], p3[3]);
-            d3[1] = make_uint4(p3[4], p3[5], p3[6], p3[7]);
+            st_global_32(d1, make_uint4(p1[0], p1[1], p1[2], p1[3]), make_uint4(p1[4], p1[5], p1[6], p1[7]));
+            st_global_32(d3, make_uint4(p3[0], p3[1], p3[2], p3[3]), make_uint4(p3[4], p3[5], p3[6], p3[7]));
           }
         }
       } else if constexpr (MODE == BWD_D1) {
@@ -479,8 +475,7 @@ grouped_gemm_bwd_sm100(const __grid_constant__ TmapSetBwd tm, const __grid_const
 #pragma unroll
           for (int j = 0; j < 8; ++j) pk[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
           uint4* dst = reinterpret_cast<uint4*>(orow + n);
-          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          st_global_32(dst, make_uint4(pk[0], pk[1], pk[2], pk[3]), make_uint4(pk[4], pk[5], pk[6], pk[7]));
         }
       } else if constexpr (NIMG_W_SECTOR) {
         // weight gradient stored from registers in whole 32-B sectors: the

@@ -97,10 +97,8 @@ NIMG_DEV void store_h1h3(void* h_out, int N, int64_t row, int n, const uint32_t 
   bf16* hb = reinterpret_cast<bf16*>(h_out);
   uint4* d1 = reinterpret_cast<uint4*>(hb + hblk_off(row, n >> 4, nch));
   uint4* d3 = reinterpret_cast<uint4*>(hb + hblk_off(row, nch + (n >> 4), nch));
-  d1[0] = make_uint4(p1[0], p1[1], p1[2], p1[3]);
-  d1[1] = make_uint4(p1[4], p1[5], p1[6], p1[7]);
-  d3[0] = make_uint4(p3[0], p3[1], p3[2], p3[3]);
-  d3[1] = make_uint4(p3[4], p3[5], p3[6], p3[7]);
+  st_global_32(d1, make_uint4(p1[0], p1[1], p1[2], p1[3]), make_uint4(p1[4], p1[5], p1[6], p1[7]));
+  st_global_32(d3, make_uint4(p3[0], p3[1], p3[2], p3[3]), make_uint4(p3[4], p3[5], p3[6], p3[7]));
 }
 
 template <int MODE>
@@ -238,8 +236,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
               pk[j] = pack_bf16x2(silu_mul(__uint_as_float(a[2 * j]), __uint_as_float(g[2 * j])),
                                   silu_mul(__uint_as_float(a[2 * j + 1]), __uint_as_float(g[2 * j + 1])));
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            st_global_32(dst, make_uint4(pk[0], pk[1], pk[2], pk[3]), make_uint4(pk[4], pk[5], pk[6], pk[7]));
             if (h_out != nullptr) store_h1h3(h_out, Nb, ti.a_row + r, ti.n0 + c * 16, a, g);
           }
         }
@@ -255,8 +252,7 @@ grouped_gemm_sm100(const __grid_constant__ TmapSet tm, const __grid_constant__ G
             for (int j = 0; j < 8; ++j)
               pk[j] = pack_bf16x2(__uint_as_float(a[2 * j]), __uint_as_float(a[2 * j + 1]));
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            st_global_32(dst, make_uint4(pk[0], pk[1], pk[2], pk[3]), make_uint4(pk[4], pk[5], pk[6], pk[7]));
           }
         }
       }
@@ -639,8 +635,7 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
             for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
-            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            st_global_32(dst, make_uint4(pk[0], pk[1], pk[2], pk[3]), make_uint4(pk[4], pk[5], pk[6], pk[7]));
             if (MODE == 0 && (oflags & kSplit3Out)) {   // fp32 mode: pre as [hi | hi | lo]
               uint32_t lo[8];
 #pragma unroll
@@ -650,10 +645,8 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
               }
               uint4* d2 = reinterpret_cast<uint4*>(orow + Nb + c * 16);
               uint4* d3 = reinterpret_cast<uint4*>(orow + 2 * Nb + c * 16);
-              d2[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-              d2[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-              d3[0] = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-              d3[1] = make_uint4(lo[4], lo[5], lo[6], lo[7]);
+              st_global_32(d2, make_uint4(pk[0], pk[1], pk[2], pk[3]), make_uint4(pk[4], pk[5], pk[6], pk[7]));
+              st_global_32(d3, make_uint4(lo[0], lo[1], lo[2], lo[3]), make_uint4(lo[4], lo[5], lo[6], lo[7]));
             }
             if (MODE == 0 && h_out != nullptr)   // training forward: keep h1 | h3
               store_h1h3(h_out, Nb, ti.a_row + row, ti.n0 + c * 16, a, g);
