@@ -632,7 +632,12 @@ grouped_gemm_sm100_pair(const __grid_constant__ TmapSet tm, const __grid_constan
             float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(bk.out) +
                                                     orow_i * bk.out_ld + ti.n0 + c * 16);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            for (int j = 0; j < 2; ++j)
+              st_global_32(dst + 2 * j,
+                           make_uint4(__float_as_uint(v[8 * j]), __float_as_uint(v[8 * j + 1]),
+                                      __float_as_uint(v[8 * j + 2]), __float_as_uint(v[8 * j + 3])),
+                           make_uint4(__float_as_uint(v[8 * j + 4]), __float_as_uint(v[8 * j + 5]),
+                                      __float_as_uint(v[8 * j + 6]), __float_as_uint(v[8 * j + 7])));
           } else {
             uint4* dst = reinterpret_cast<uint4*>(orow + c * 16);
             st_global_32(dst, make_uint4(pk[0], pk[1], pk[2], pk[3]), make_uint4(pk[4], pk[5], pk[6], pk[7]));

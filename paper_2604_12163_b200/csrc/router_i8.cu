@@ -776,11 +776,14 @@ router_scores_i8_kernel(const bf16* __restrict__ x, const float* __restrict__ w_
 #pragma unroll 4
       for (int e = p * 16; e < p * 16 + 16; ++e)
         scores_bes[((int64_t)b * NE + e) * S + srow] = (float)(exs[r * LGS + e] / sum);
-      float4* lo = reinterpret_cast<float4*>(logits + t * NE + p * 16);
+      const float* lr = lgs + r * LGS + p * 16;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        lo[i] = make_float4(lgs[r * LGS + p * 16 + 4 * i], lgs[r * LGS + p * 16 + 4 * i + 1],
-                            lgs[r * LGS + p * 16 + 4 * i + 2], lgs[r * LGS + p * 16 + 4 * i + 3]);
+      for (int i = 0; i < 2; ++i)   // 64 B of this row's logits: two whole sectors
+        st_global_32(logits + t * NE + p * 16 + 8 * i,
+                     make_uint4(__float_as_uint(lr[8 * i]), __float_as_uint(lr[8 * i + 1]),
+                                __float_as_uint(lr[8 * i + 2]), __float_as_uint(lr[8 * i + 3])),
+                     make_uint4(__float_as_uint(lr[8 * i + 4]), __float_as_uint(lr[8 * i + 5]),
+                                __float_as_uint(lr[8 * i + 6]), __float_as_uint(lr[8 * i + 7])));
       if (p == 0 && rflag_s[r]) ws.list[atomicAdd(ws.counter, 1u)] = (int)t;
     }
     if (trace && tid == 0) trs[44] = gtimer();
