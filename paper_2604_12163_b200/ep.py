@@ -64,6 +64,9 @@ _OWN_A = int(_os.environ.get("NIMG_EP_OWN_A", "-1"))
 # 2 warps per CTA, so the remote chunks -- and their dispatch copies -- finish
 # later than with the dedicated gather kernel.
 _BG_GATHER = _os.environ.get("NIMG_EP_BG_GATHER", "0") == "1"
+# NIMG_EP_OWN_BG=1: only the rank's own chunk is gathered on the first grouped
+# launch's background warps; the remote chunks by the gather kernel first
+_BG_OWN = _os.environ.get("NIMG_EP_OWN_BG", "0") == "1"
 _MAX_CHUNKS = 64
 
 
@@ -403,11 +406,21 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
         # persistent double buffer (read by the dispatch copy streams)
         xring = ctx.ring("xg", (E * B_l * cap, d), act, x_mod.device)
         xslot, xg = xring.next()
-        flags = (stages.bg_flags(r) if _BG_GATHER and ctx.world > 1 and ctx.world <= _MAX_CHUNKS
-                 and hasattr(stages, "bg_flags") else 0)
-        if flags:
+        flags = (stages.bg_flags(r) if (_BG_GATHER or _BG_OWN) and ctx.world > 1
+                 and ctx.world <= _MAX_CHUNKS and hasattr(stages, "bg_flags") else 0)
+        if flags and _BG_GATHER:
             # the first grouped launch gathers every chunk while it runs
             bg = {"src": xm, "idx": r["token_flat"], "dst": xg, "flags": flags}
+        elif flags:
+            # the remote chunks first (the dispatch copies wait for them), then
+            # the own chunk on the first grouped launch's background warps
+            n, me, tf = plan.chunk_rows, plan.rank, r["token_flat"]
+            if me > 0:
+                stages.gather(xm, tf[:me * n], out=xg[:me * n])
+            if me < ctx.world - 1:
+                stages.gather(xm, tf[(me + 1) * n:], out=xg[(me + 1) * n:])
+            bg = {"src": xm, "idx": tf[me * n:(me + 1) * n], "dst": xg[me * n:(me + 1) * n],
+                  "flags": flags, "own": True}
         else:
             stages.gather(xm, r["token_flat"], out=xg)
     else:
@@ -510,7 +523,10 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None,
     xbytes, ybytes = n * d * tp.act_es, n * d * tp.y_es
     coff, cex = plan.chunk_segments()
 
-    if bg is not None:
+    own_bg = bg is not None and bg.get("own", False)
+    if own_bg:   # the own chunk only: no dispatch copy waits on it
+        bg = {k: v for k, v in bg.items() if k != "own"}
+    elif bg is not None:
         # sub-blocks of 32 gathered rows overlapping each chunk: the running
         # totals the dispatch copies wait for
         bg = dict(bg, row_off=me * n, chunk_rows=n, chunk_done=tp.chunk_done.data_ptr())
@@ -555,7 +571,7 @@ def _ce_exchange(plan: EPPlan, ctx: EPContext, stages, xg, xm, w, timeline=None,
         if not serial or s == 1:
             st.wait_event(x_ready)
         sh = st.cuda_stream
-        if bg is not None:   # chunk q gathered by the first grouped launch
+        if bg is not None and not own_bg:   # chunk q gathered by the first grouped launch
             _lib.check(L.nimg_stream_wait_geq_u32(tp.chunk_done.data_ptr() + 4 * q,
                                                   tp.chunk_expect[q] & 0xFFFFFFFF, sh))
         if k > 1:   # q consumed my previous chunk
