@@ -77,6 +77,21 @@ def test_backward_full_width_bf16_vs_oracle():
         assert err <= TOL_BF16, (k, err)
 
 
+@pytest.mark.parametrize("h", [64, 192])
+def test_backward_tcgen05_tail_tile_widths(h):
+    """h % 128 == 64: GEMM1's last tile of every row block runs at half width
+    (N = 128, h3 at accumulator column 64), including h = 64 where that is the
+    only tile; the saved h1 | h3 feed the SwiGLU pullback."""
+    B, S, d, E, C = 2, 128, 256, 8, 2.0
+    inp = make_layer_inputs(48, B, S, d, E, h, mode="bf16")
+    g_out = bf16_round(np.random.default_rng(49).standard_normal((B, S, d)).astype(np.float32))
+    out, grads = _run(inp, dict(d=d, E=E, C=C), g_out, "bf16")
+    ref = O.moe_backward(*(inp[k] for k in GRADS), g_out, capacity_factor=C)
+    for k in GRADS:
+        err = rel_fro(np_of(grads[k]), ref[k])
+        assert err <= TOL_BF16, (k, err)
+
+
 def test_backward_cuda_core_path_bf16_ragged_width():
     """bf16 layer whose h is not a multiple of 64: the training path runs on
     CUDA cores (fp32 intermediates) -- same bar."""

@@ -436,11 +436,14 @@ def test_block_full_width_bf16():
     assert max(errs) <= TOL_BF16, f"block bf16 per-sample rel-err {errs}"
 
 
-@pytest.mark.parametrize("B,S,d,E,h,C", [(1, 40, 256, 8, 128, 1.0), (3, 56, 512, 8, 192, 2.0)])
+@pytest.mark.parametrize("B,S,d,E,h,C", [(1, 40, 256, 8, 128, 1.0), (3, 56, 512, 8, 192, 2.0),
+                                         (2, 72, 256, 8, 64, 2.0)])
 def test_ragged_routed_rows_tcgen05(B, S, d, E, h, C):
     """tcgen05 shapes whose routed row count is not a multiple of the 32-row
     background-gather sub-block or the 256-row pair tile (40 = 8 x 5 rows;
-    336 = 8 x 3 x 14): the gather inside GEMM1 and its flags at the edges."""
+    336 = 8 x 3 x 14; 288): the gather inside GEMM1 and its flags at the
+    edges; h = 192 and 64 also end every GEMM1 row block with a half-width
+    tile (h = 64: the only one)."""
     from paper_2604_12163_b200 import moe as M
     from paper_2604_12163_b200 import router as R
     inp = make_layer_inputs(61, B, S, d, E, h, mode="bf16")
