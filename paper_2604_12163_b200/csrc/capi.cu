@@ -205,6 +205,9 @@ struct RouteWs {
   int* row_map;
   float* gate_tok;
   int* cursor;
+  unsigned long long* tokmask;   // per-token selecting-expert masks (gates formed in the combine)
+  int32_t* tokrow;               // [T][E] routed row of each selecting (token, e)
+  float* tokraw;                 // [T][E] its raw score
 };
 // one flag per 32 routed rows, plus the sub-block claim counter (flags[nsub])
 int64_t bg_flag_count(const nimg_moe_desc* d) { return (d->E * d->B * d->cap + 31) / 32 + 1; }
@@ -215,7 +218,8 @@ size_t route_ws_bytes(const nimg_moe_desc* d) {
          align_up(router_wd_bytes((int)d->d, (int)d->E)) + align_up(slot_bytes(d)) +
          align_up((size_t)d->B * 4) + align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d)) +
          align_up((size_t)bg_flag_count(d) * 4) + align_up((size_t)d->B * d->S * 4) +
-         2 * align_up((size_t)d->E * d->B * d->cap * 4) + align_up((size_t)d->B * 4);
+         2 * align_up((size_t)d->E * d->B * d->cap * 4) + align_up((size_t)d->B * 4) +
+         align_up((size_t)d->B * d->S * 8) + 2 * align_up((size_t)d->B * d->S * d->E * 4);
 }
 RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
@@ -241,11 +245,25 @@ RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   r.gate_tok = reinterpret_cast<float*>(p);
   p += align_up((size_t)d->E * d->B * d->cap * 4);
   r.cursor = reinterpret_cast<int*>(p);
+  p += align_up((size_t)d->B * 4);
+  r.tokmask = reinterpret_cast<unsigned long long*>(p);
+  p += align_up((size_t)d->B * d->S * 8);
+  r.tokrow = reinterpret_cast<int32_t*>(p);
+  p += align_up((size_t)d->B * d->S * d->E * 4);
+  r.tokraw = reinterpret_cast<float*>(p);
   return r;
 }
 
 bool use_pair_kernels();
 bool use_tok_order();
+// NIMG_GATES_IN_COMBINE=0: the 1-GPU forward keeps the separate gate kernel
+static bool gates_in_combine() {
+  static const bool on = [] {
+    const char* e = getenv("NIMG_GATES_IN_COMBINE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 // fp32 mode on the bf16 tensor cores (split_kernels.cu, "bf16x3"): fp32
 // layers whose widths tile the tcgen05 pair kernels; NIMG_FP32_TC=0 keeps the
 // CUDA-core fp32 GEMMs
@@ -580,8 +598,12 @@ int expert_ffn_impl(const nimg_ffn_desc* f, const int64_t* off, const int32_t* e
   return NIMG_OK;
 }
 
+// fuse_gates: the layer forward's combine forms the gates itself (GateFuse):
+// select also writes the per-token expert masks, and the gate kernel is skipped
+// (comb_rows / comb_cnt are then not written; gates are, by the combine)
 int route_impl(const nimg_moe_desc* d, const void* x_norm, const void* t_emb_v, const void* w_r_v,
-               const nimg_route_out* o, void* ws, size_t ws_bytes, cudaStream_t st) {
+               const nimg_route_out* o, void* ws, size_t ws_bytes, cudaStream_t st,
+               bool fuse_gates = false) {
   NIMG_TRY(check_moe_desc(d));
   if (!o || !o->logits || !o->scores_bes || !o->token_flat || !o->gate_raw || !o->gates ||
       !o->comb_rows || !o->comb_cnt)
@@ -612,14 +634,25 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const void* t_emb_v, 
   // caller-owned).
   if (!router_uses_dmma(E))
     CUDA_TRY(cudaMemsetAsync(w.counters, 0xFF, (size_t)B * 4, st));
-  if (router_i8_eligible(xn_bf16, dd, E, x_norm, w_r))
-    CUDA_TRY(launch_router_i8(x_norm, t_emb, w_r, w.part, w.i8, logits, scores_bes, B, S, dd, st));
-  else
+  // fuse_gates: the token masks and what the gate kernel would have zeroed
+  // (GEMM1's gather flags) -- by the INT8 router's prep kernel, else memsets
+  const bool i8 = router_i8_eligible(xn_bf16, dd, E, x_norm, w_r);
+  if (fuse_gates && !i8) {
+    CUDA_TRY(cudaMemsetAsync(w.bg_flags, 0, (size_t)bg_flag_count(d) * 4, st));
+    CUDA_TRY(cudaMemsetAsync(w.tokmask, 0, (size_t)B * S * 8, st));
+  }
+  if (i8) {
+    ZeroSpans zs;
+    if (fuse_gates) zs = ZeroSpans{w.tokmask, (int64_t)B * S, w.bg_flags, bg_flag_count(d)};
+    CUDA_TRY(launch_router_i8(x_norm, t_emb, w_r, w.part, w.i8, logits, scores_bes, B, S, dd, st, zs));
+  } else
     CUDA_TRY(launch_router(xn_bf16, x_norm, t_emb, w_r, w.tb, w.part, w.counters, w.wd, logits,
                            scores_bes, B, S, dd, E, st));
   mark(6, st);   // router scores done (inside stage 0 -> 1)
   CUDA_TRY(launch_ec_select(scores_bes, o->token_flat, static_cast<float*>(o->gate_raw), w.slot_of, B,
-                            S, E, cap, st, w.cursor));
+                            S, E, cap, st, w.cursor, fuse_gates ? w.tokmask : nullptr,
+                            fuse_gates ? w.tokrow : nullptr, fuse_gates ? w.tokraw : nullptr));
+  if (fuse_gates) return NIMG_OK;
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
   CUDA_TRY(launch_gate_norm(scores_bes, w.slot_of, static_cast<float*>(o->gates), o->comb_rows, o->comb_cnt, B, S,
                             E, cap, d->gate_eps, d->gate_scale, st, w.bg_flags,
@@ -1024,8 +1057,14 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
   if (bg_gather)
     bg = BgGather{p->x_mod, p->route.token_flat, xg, carve_route(d, route_ws).bg_flags,
                   (int)f.n_rows, (int)(d->d * elt(d->act_dtype)), 0, 0, nullptr};
+  // inference on one GPU: the combine forms the gates (no gate kernel)
+  const bool tok_order_pre = !state && bf_tc && use_pair_kernels() && gate_tok_supported() &&
+                             use_tok_order() && f.n_rows > 0;
+  const bool fuse_gates = !state && d->act_dtype != NIMG_F64 && d->E <= 64 &&
+                          select_blk_path((int)d->S) && !tok_order_pre && gates_in_combine();
   mark(0, st);
-  NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st));
+  NIMG_TRY(route_impl(d, p->x_norm, p->t_emb, p->w_r, &p->route, route_ws, route_ws_bytes(d), st,
+                      fuse_gates));
   mark(1, st);
   if (!fused_gather && !bg_gather)
     CUDA_TRY(launch_gather_rows(p->x_mod, d->d * (int64_t)elt(d->act_dtype), p->route.token_flat,
@@ -1052,11 +1091,15 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
                                 static_cast<const double*>(p->route.gates), p->route.comb_rows,
                                 p->route.comb_cnt, static_cast<double*>(p->out), d->B * d->S,
                                 (int)d->d, (int)d->E, st));
-  else
+  else {
+    const GateFuse gf{rw.tokmask, rw.tokrow, rw.tokraw, static_cast<float*>(p->route.gates),
+                      d->gate_eps, d->gate_scale};
     CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys,
                             tok_order ? rw.gate_tok : static_cast<const float*>(p->route.gates),
                             p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,
-                            (int)d->E, st, resid_h, th_ff, (int)d->S, tok_order ? rw.tok_off : nullptr));
+                            (int)d->E, st, resid_h, th_ff, (int)d->S, tok_order ? rw.tok_off : nullptr,
+                            fuse_gates ? &gf : nullptr));
+  }
   mark(5, st);
   return NIMG_OK;
 }

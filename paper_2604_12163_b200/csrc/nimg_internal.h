@@ -216,13 +216,36 @@ size_t router_wd_bytes(int d, int E);
 // NIMG_ROUTER=dmma forces the FP64 router.
 bool router_i8_eligible(bool x_bf16, int d, int E, const void* x_norm, const void* w_r);
 size_t router_i8_ws_bytes(int64_t T, int d);
+// spans the INT8 router's prep kernel zeroes on the way (n = 0: none)
+struct ZeroSpans {
+  unsigned long long* p64 = nullptr;
+  int64_t n64 = 0;
+  int* p32 = nullptr;
+  int64_t n32 = 0;
+};
 cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float* w_r, double* part,
                              void* i8ws, float* logits, float* scores_bes, int B, int S, int d,
-                             cudaStream_t s);
+                             cudaStream_t s, ZeroSpans zs = ZeroSpans{});
 size_t router_part_bytes(int B, int d, int E);
+// tokmask (E <= 64, block select path): each selected (token, e) also sets bit
+// e of the token's mask and writes its routed row / raw score into the
+// token-major tokrow / tokraw (the combine then forms the gates itself, GateFuse)
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s,
-                             int* cursor = nullptr);
+                             int* cursor = nullptr, unsigned long long* tokmask = nullptr,
+                             int32_t* tokrow = nullptr, float* tokraw = nullptr);
+bool select_blk_path(int S);
+// Gates formed inside the combine (1-GPU inference): token t's selecting experts
+// are the set bits of tokmask[t] (ascending), their rows / raw scores come from
+// tokrow / tokraw, the gate chain is gate_tile_kernel's and every gate is also
+// written to gates_out (the routing output)
+struct GateFuse {
+  const unsigned long long* tokmask;
+  const int32_t* tokrow;   // [T][E]: routed row of (token, e), valid where the mask bit is set
+  const float* tokraw;     // [T][E]: its raw score
+  float* gates_out;
+  float eps32, alpha32;
+};
 // Token-ordered expert outputs for the 1-GPU combine (gate_tile_kernel):
 // null tok_off = off
 struct TokOrder {
@@ -247,7 +270,7 @@ cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, con
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
                            void* out, int64_t T, int d, int E, cudaStream_t s,
                            const void* hres = nullptr, const void* th_gate = nullptr, int S = 1,
-                           const int32_t* tok_off = nullptr);
+                           const int32_t* tok_off = nullptr, const GateFuse* gf = nullptr);
 // backbone MoE branch prologue (block_kernels.cu)
 cudaError_t launch_block_modvec(const float* sa_gate, const float* ff_scale, const float* ff_gate,
                                 double* th_sa, double* th_ff, float* onep, float* th_sa_f,

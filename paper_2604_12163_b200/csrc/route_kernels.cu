@@ -770,7 +770,9 @@ template <int KPL>
 __global__ void __launch_bounds__(SB_WARPS * 32)
 ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
                      float* __restrict__ gate_raw, int16_t* __restrict__ slot_of, int B, int S,
-                     int E, int cap, int P, int* __restrict__ cursor) {
+                     int E, int cap, int P, int* __restrict__ cursor,
+                     unsigned long long* __restrict__ tokmask, int32_t* __restrict__ tokrow,
+                     float* __restrict__ tokraw) {
   extern __shared__ __align__(16) uint64_t wsel[];   // [P] winners
   __shared__ int red[2][SB_WARPS][4];
   __shared__ int wcnt[SB_WARPS][2];
@@ -935,6 +937,12 @@ ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__
     token_flat[o] = (int32_t)((int64_t)b * S + idx);
     gate_raw[o] = c[idx];
     scol[idx] = (int16_t)j;
+    if (tokmask) {
+      const int64_t tt = (int64_t)b * S + idx;
+      tokrow[tt * E + e] = (int32_t)o;
+      tokraw[tt * E + e] = c[idx];
+      atomicOr(tokmask + tt, 1ull << e);
+    }
   }
 }
 
@@ -1163,7 +1171,7 @@ __global__ void __launch_bounds__(CB_WARPS * 32)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
                TO* __restrict__ out, int64_t T, int d, int E, const TO* __restrict__ hres,
-               const ACC* __restrict__ thg, int S, const int32_t* __restrict__ tok_off) {
+               const ACC* __restrict__ thg, int S, const int32_t* __restrict__ tok_off, GateFuse gf) {
   pdl_trigger();
   pdl_wait();
   extern __shared__ __align__(16) uint8_t sm[];
@@ -1172,26 +1180,69 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
   float* gl = reinterpret_cast<float*>(sm + (size_t)CB_WARPS * E * 4) + (size_t)warp * E;
   const int64_t t = (int64_t)blockIdx.x * CB_WARPS + warp;
   if (t >= T) return;
-  const int cnt = comb_cnt[t];
   const uint32_t row_bytes = (uint32_t)((int64_t)d * sizeof(TY));
+  int cnt;
 #ifndef NIMG_CB_NO_PREFETCH
   // whole-row L2 prefetches (one bulk instruction per row) as soon as the
   // row list is known: the column loop's loads then hit L2
   if (lane == 0 && row_bytes % 16 == 0) bulk_prefetch_l2(ys + t * d, row_bytes);
 #endif
-  // tok_off: the token's rows are consecutive in the token-ordered yr (and
-  // `gates` is indexed the same way); else the expert-major row list
-  const int32_t rbase = tok_off != nullptr ? tok_off[t] : 0;
-  for (int k = lane; k < cnt; k += 32) {
-    const int32_t r = tok_off != nullptr ? rbase + k : comb_rows[t * E + k];
-    rows[k] = r;
+  if (gf.tokmask != nullptr) {
+    // the gates of router.py:137-143 formed here (gate_tile_kernel's arithmetic):
+    // the token's selecting experts in ascending order are its mask's set bits
+    const unsigned long long m = gf.tokmask[t];
+    cnt = __popcll(m);
+    const uint32_t mlo = (uint32_t)m, mhi = (uint32_t)(m >> 32);
+    const int nlo = __popc(mlo);
+    for (int k = lane; k < cnt; k += 32) {
+      const int e = k < nlo ? (int)__fns(mlo, 0, k + 1) : 32 + (int)__fns(mhi, 0, k - nlo + 1);
+      const int32_t r = gf.tokrow[t * E + e];
+      rows[k] = r;
 #ifndef NIMG_CB_NO_PREFETCH
-    if (row_bytes % 16 == 0) bulk_prefetch_l2(yr + (int64_t)r * d, row_bytes);
+      if (row_bytes % 16 == 0) bulk_prefetch_l2(yr + (int64_t)r * d, row_bytes);
 #endif
-    gl[k] = gates != nullptr ? gates[r] : 1.0f;   // null: unit gates (gather pullback)
+      gl[k] = gf.tokraw[t * E + e];
+    }
+    // (the gate chain itself runs once the first row loads are in flight, below)
+  } else {
+    cnt = comb_cnt[t];
+    // tok_off: the token's rows are consecutive in the token-ordered yr (and
+    // `gates` is indexed the same way); else the expert-major row list
+    const int32_t rbase = tok_off != nullptr ? tok_off[t] : 0;
+    for (int k = lane; k < cnt; k += 32) {
+      const int32_t r = tok_off != nullptr ? rbase + k : comb_rows[t * E + k];
+      rows[k] = r;
+#ifndef NIMG_CB_NO_PREFETCH
+      if (row_bytes % 16 == 0) bulk_prefetch_l2(yr + (int64_t)r * d, row_bytes);
+#endif
+      gl[k] = gates != nullptr ? gates[r] : 1.0f;   // null: unit gates (gather pullback)
+    }
   }
   __syncwarp();
+  // GateFuse: gl[] holds raw scores until the first rows are in flight; then
+  // gl[k] = gate (router.py:137-143, gate_tile_kernel's arithmetic)
+  bool gates_ready = gf.tokmask == nullptr;
+  auto form_gates = [&]() {
+    float den = 0.f;
+    if (lane == 0) {   // fp32(sequential f64 sum in expert order): the np.add.at order
+      double tot = 0.0;
+      for (int k = 0; k < cnt; ++k) tot += (double)gl[k];
+      den = (float)((double)(float)tot + (double)gf.eps32);
+    }
+    den = __shfl_sync(0xffffffffu, den, 0);
+    for (int k = lane; k < cnt; k += 32) {
+      const float q = (float)((double)gl[k] / (double)den);
+      const float g = (float)((double)q * (double)gf.alpha32);
+      gl[k] = g;
+      gf.gates_out[rows[k]] = g;
+    }
+    __syncwarp();
+    gates_ready = true;
+  };
   constexpr int STEP = 32 * VEC;
+  // the in-loop call needs every lane to reach it: only when all lanes run the
+  // same number of column steps
+  if (!gates_ready && d % (STEP * UNR) != 0) form_gates();
   for (int c0 = lane * VEC; c0 < d; c0 += STEP * UNR) {
     VecIO<TY, VEC> sh[UNR];
     ACC acc[UNR][VEC];
@@ -1211,6 +1262,7 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
 #pragma unroll
           for (int u = 0; u < UNR; ++u) y[q][u].load(src + u * STEP);
         }
+      if (!gates_ready) form_gates();
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         if (kb + q < cnt) {
@@ -1359,10 +1411,14 @@ static bool select_warp_enabled() {
   return on;
 }
 
+bool select_blk_path(int S) { return select_warp_enabled() && S <= 4096; }
+
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s,
-                             int* cursor) {
-  if (select_warp_enabled() && S <= 4096) {
+                             int* cursor, unsigned long long* tokmask, int32_t* tokrow,
+                             float* tokraw) {
+  if (tokmask && (!select_blk_path(S) || E > 64)) return cudaErrorInvalidValue;
+  if (select_blk_path(S)) {
     const int P = next_pow2(cap);
     const size_t wsmem = (size_t)P * 8;
     const dim3 grid((unsigned)(B * E));
@@ -1371,7 +1427,8 @@ cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float
       cudaError_t e2 = set_max_dyn_smem(ec_select_blk_kernel<K>, (int)wsmem);                   \
       if (e2 != cudaSuccess) return e2;                                                         \
       return launch_pdl(ec_select_blk_kernel<K>, grid, dim3(SB_WARPS * 32), wsmem, s,           \
-                        scores_bes, token_flat, gate_raw, slot_of, B, S, E, cap, P, cursor);   \
+                        scores_bes, token_flat, gate_raw, slot_of, B, S, E, cap, P, cursor,    \
+                        tokmask, tokrow, tokraw);                                               \
     } while (0)
     if (S <= 256) NIMG_BSEL(2);
     if (S <= 512) NIMG_BSEL(4);
@@ -1445,14 +1502,14 @@ template <typename TY, typename TO, bool RESID>
 static cudaError_t combine_dispatch(const void* yr, const void* ys, const float* gates,
                              const int32_t* rows, const int32_t* cnt, void* out, int64_t T, int d,
                              int E, const void* hres, const void* thg, int S, cudaStream_t s,
-                             const int32_t* tok_off) {
+                             const int32_t* tok_off, const GateFuse& gf) {
   const unsigned grid = (unsigned)((T + CB_WARPS - 1) / CB_WARPS);
   const size_t smem = (size_t)CB_WARPS * E * 8;
   using ACC = typename std::conditional<sizeof(TO) == 2, float, double>::type;
 #define NIMG_COMBINE(V, U)                                                                      \
   launch_pdl(combine_kernel<TY, TO, V, ACC, U, RESID>, dim3(grid), dim3(CB_WARPS * 32), smem, s, \
              (const TY*)yr, (const TY*)ys, gates, rows, cnt, (TO*)out, T, d, E, (const TO*)hres, \
-             (const ACC*)thg, S, tok_off)
+             (const ACC*)thg, S, tok_off, gf)
   if (d % 512 == 0) return NIMG_COMBINE(8, 2);
   if (d % 8 == 0) return NIMG_COMBINE(8, 1);
   return NIMG_COMBINE(1, 1);
@@ -1462,14 +1519,16 @@ static cudaError_t combine_dispatch(const void* yr, const void* ys, const float*
 cudaError_t launch_combine(bool y_bf16, bool out_bf16, const void* y_routed, const void* y_shared,
                            const float* gates, const int32_t* comb_rows, const int32_t* comb_cnt,
                            void* out, int64_t T, int d, int E, cudaStream_t s, const void* hres,
-                           const void* th_gate, int S, const int32_t* tok_off) {
+                           const void* th_gate, int S, const int32_t* tok_off, const GateFuse* gfp) {
   if (T <= 0) return cudaSuccess;
   const bool r = hres != nullptr;
+  GateFuse gf{};
+  if (gfp) gf = *gfp;
 #define NIMG_CD(TY, TO)                                                                              \
   (r ? combine_dispatch<TY, TO, true>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, \
-                                      hres, th_gate, S, s, tok_off)                                 \
+                                      hres, th_gate, S, s, tok_off, gf)                             \
      : combine_dispatch<TY, TO, false>(y_routed, y_shared, gates, comb_rows, comb_cnt, out, T, d, E, \
-                                       hres, th_gate, S, s, tok_off))
+                                       hres, th_gate, S, s, tok_off, gf))
   cudaError_t err;
   if (y_bf16 && out_bf16) err = NIMG_CD(bf16, bf16);
   else if (y_bf16) err = NIMG_CD(bf16, float);

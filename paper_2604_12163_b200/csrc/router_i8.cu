@@ -268,8 +268,17 @@ NIMG_DEV void digits_b256(float x, float scale, uint32_t& hi, uint32_t& lo) {
 // the elements below the column window (WSH + 24 bits), in ascending k.
 __global__ void __launch_bounds__(256)
 router_prep_i8_kernel(const float* __restrict__ t_emb, const float* __restrict__ w_r,
-                      double* __restrict__ part, Ws ws, int B, int d) {
+                      double* __restrict__ part, Ws ws, int B, int d, ZeroSpans zs) {
   pdl_trigger();
+  // buffers later kernels of the step accumulate into (the layer forward's
+  // token masks and GEMM1's gather flags); every earlier use is complete, as
+  // this is an ordinary launch
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zs.n64;
+       i += (int64_t)gridDim.x * blockDim.x)
+    zs.p64[i] = 0ull;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < zs.n32;
+       i += (int64_t)gridDim.x * blockDim.x)
+    zs.p32[i] = 0;
   const int KS = router_tpart_ks(d);
   if ((int)blockIdx.x < B * KS) {
     if (blockIdx.x == 0 && threadIdx.x == 0) *ws.counter = 0u;
@@ -957,7 +966,7 @@ size_t router_i8_ws_bytes(int64_t T, int d) { return ri8::ws_bytes(T, d); }
 
 cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float* w_r, double* part,
                              void* i8ws, float* logits, float* scores_bes, int B, int S, int d,
-                             cudaStream_t s) {
+                             cudaStream_t s, ZeroSpans zs) {
   const int64_t T = (int64_t)B * S;
   ri8::Ws ws = ri8::carve(i8ws, T, d);
   // the first kernel of the chain: an ORDINARY launch (full stream order). The
@@ -965,7 +974,7 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
   // everything that wrote x_norm (e.g. the block prologue) must have completed
   // before this kernel starts and triggers its dependents. (A PDL launch here
   // would let the scores kernel start while the prologue still writes x_norm.)
-  ri8::router_prep_i8_kernel<<<B * router_tpart_ks(d) + ri8::NE, 256, 0, s>>>(t_emb, w_r, part, ws, B, d);
+  ri8::router_prep_i8_kernel<<<B * router_tpart_ks(d) + ri8::NE, 256, 0, s>>>(t_emb, w_r, part, ws, B, d, zs);
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   err = set_max_dyn_smem(ri8::router_scores_i8_kernel, (int)ri8::SMEM);

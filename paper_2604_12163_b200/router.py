@@ -131,6 +131,8 @@ def build_routing(r: dict, B: int, S: int, E: int, cap: int, with_decisions: boo
         "capacity": cap,
         "shape": (B, S, E),
         # device-side extras used by the MoE layer / expert parallel path
+        # (comb_rows / comb_cnt are filled by route() and the training forward;
+        # the 1-GPU inference forward forms the gates in its combine instead)
         "gate_raw": r["gate_raw"],
         "scores_bes": r["scores_bes"],
         "comb_rows": r["comb_rows"],
