@@ -51,6 +51,13 @@ def router_uses_i8(c) -> bool:
             and c["d"] % 64 == 0 and c["d"] <= 8192)
 
 
+def gates_in_combine(c) -> bool:
+    """Mirror of capi.cu's fuse_gates for the 1-GPU forward: E <= 64, the block
+    select path (S <= 4096), no token-ordered outputs, not switched off."""
+    return (c["E"] <= 64 and c["S"] <= 4096 and os.environ.get("NIMG_GATES_IN_COMBINE") != "0"
+            and os.environ.get("NIMG_SELECT") != "cta" and os.environ.get("NIMG_TOK_ORDER") != "1")
+
+
 def router_impl(c) -> str:
     return ("exact INT8 tensor-core digit GEMM (tcgen05 kind::i8) + f64 fix-up" if router_uses_i8(c)
             else "FP64 tensor pipe (DMMA m8n8k4)")
@@ -362,8 +369,9 @@ def run_single(args, c, peaks, peak_kind):
         "fp32_mode": fp32,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        # router (prep + scores [+ INT8 fix-up]) + select + gates [+ gather] + GEMM1 + GEMM2 + combine
-        "gpu_launches": ((3 if router_uses_i8(c) else 2) + 2
+        # router (prep + scores [+ INT8 fix-up]) + select [+ gates] [+ gather] + GEMM1 + GEMM2
+        # + combine; the 1-GPU forward forms the gates in the combine (capi.cu fuse_gates)
+        "gpu_launches": ((3 if router_uses_i8(c) else 2) + 1 + (0 if gates_in_combine(c) else 1)
                          + (0 if os.environ.get("NIMG_BG_GATHER", "1") != "0" else 1) + 3) * args.steps,
         "clocks": clocks,
     }
