@@ -206,8 +206,7 @@ struct RouteWs {
   float* gate_tok;
   int* cursor;
   unsigned long long* tokmask;   // per-token selecting-expert masks (gates formed in the combine)
-  int32_t* tokrow;               // [T][E] routed row of each selecting (token, e)
-  float* tokraw;                 // [T][E] its raw score
+  int2* tokent;                  // [T][E] (routed row, raw score) of each selecting (token, e)
 };
 // one flag per 32 routed rows, plus the sub-block claim counter (flags[nsub])
 int64_t bg_flag_count(const nimg_moe_desc* d) { return (d->E * d->B * d->cap + 31) / 32 + 1; }
@@ -219,7 +218,7 @@ size_t route_ws_bytes(const nimg_moe_desc* d) {
          align_up((size_t)d->B * 4) + align_up(router_i8_ws_bytes(d->B * d->S, (int)d->d)) +
          align_up((size_t)bg_flag_count(d) * 4) + align_up((size_t)d->B * d->S * 4) +
          2 * align_up((size_t)d->E * d->B * d->cap * 4) + align_up((size_t)d->B * 4) +
-         align_up((size_t)d->B * d->S * 8) + 2 * align_up((size_t)d->B * d->S * d->E * 4);
+         align_up((size_t)d->B * d->S * 8) + align_up((size_t)d->B * d->S * d->E * 8);
 }
 RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   uint8_t* p = static_cast<uint8_t*>(ws);
@@ -248,9 +247,7 @@ RouteWs carve_route(const nimg_moe_desc* d, void* ws) {
   p += align_up((size_t)d->B * 4);
   r.tokmask = reinterpret_cast<unsigned long long*>(p);
   p += align_up((size_t)d->B * d->S * 8);
-  r.tokrow = reinterpret_cast<int32_t*>(p);
-  p += align_up((size_t)d->B * d->S * d->E * 4);
-  r.tokraw = reinterpret_cast<float*>(p);
+  r.tokent = reinterpret_cast<int2*>(p);
   return r;
 }
 
@@ -651,7 +648,7 @@ int route_impl(const nimg_moe_desc* d, const void* x_norm, const void* t_emb_v, 
   mark(6, st);   // router scores done (inside stage 0 -> 1)
   CUDA_TRY(launch_ec_select(scores_bes, o->token_flat, static_cast<float*>(o->gate_raw), w.slot_of, B,
                             S, E, cap, st, w.cursor, fuse_gates ? w.tokmask : nullptr,
-                            fuse_gates ? w.tokrow : nullptr, fuse_gates ? w.tokraw : nullptr));
+                            fuse_gates ? w.tokent : nullptr));
   if (fuse_gates) return NIMG_OK;
   // fp32(eps) / fp32(alpha): as_tensor(scalar, like=fp32 tensor) (tensor.py:183-187)
   CUDA_TRY(launch_gate_norm(scores_bes, w.slot_of, static_cast<float*>(o->gates), o->comb_rows, o->comb_cnt, B, S,
@@ -1092,8 +1089,8 @@ static int moe_forward_impl(const nimg_moe_desc* d, const nimg_moe_ptrs* p, void
                                 p->route.comb_cnt, static_cast<double*>(p->out), d->B * d->S,
                                 (int)d->d, (int)d->E, st));
   else {
-    const GateFuse gf{rw.tokmask, rw.tokrow, rw.tokraw, static_cast<float*>(p->route.gates),
-                      d->gate_eps, d->gate_scale};
+    const GateFuse gf{rw.tokmask, rw.tokent, static_cast<float*>(p->route.gates), d->gate_eps,
+                      d->gate_scale};
     CUDA_TRY(launch_combine(ydt == NIMG_BF16, d->act_dtype == NIMG_BF16, yr, ys,
                             tok_order ? rw.gate_tok : static_cast<const float*>(p->route.gates),
                             p->route.comb_rows, p->route.comb_cnt, p->out, d->B * d->S, (int)d->d,

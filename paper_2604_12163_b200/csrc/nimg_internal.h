@@ -228,21 +228,20 @@ cudaError_t launch_router_i8(const void* x_norm, const float* t_emb, const float
                              cudaStream_t s, ZeroSpans zs = ZeroSpans{});
 size_t router_part_bytes(int B, int d, int E);
 // tokmask (E <= 64, block select path): each selected (token, e) also sets bit
-// e of the token's mask and writes its routed row / raw score into the
-// token-major tokrow / tokraw (the combine then forms the gates itself, GateFuse)
+// e of the token's mask and writes its (routed row, raw score) into the
+// token-major tokent (the combine then forms the gates itself, GateFuse)
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s,
                              int* cursor = nullptr, unsigned long long* tokmask = nullptr,
-                             int32_t* tokrow = nullptr, float* tokraw = nullptr);
+                             int2* tokent = nullptr);
 bool select_blk_path(int S);
 // Gates formed inside the combine (1-GPU inference): token t's selecting experts
 // are the set bits of tokmask[t] (ascending), their rows / raw scores come from
-// tokrow / tokraw, the gate chain is gate_tile_kernel's and every gate is also
+// tokent, the gate chain is gate_tile_kernel's and every gate is also
 // written to gates_out (the routing output)
 struct GateFuse {
   const unsigned long long* tokmask;
-  const int32_t* tokrow;   // [T][E]: routed row of (token, e), valid where the mask bit is set
-  const float* tokraw;     // [T][E]: its raw score
+  const int2* tokent;      // [T][E]: (routed row, raw score bits) of (token, e), valid where the mask bit is set
   float* gates_out;
   float eps32, alpha32;
 };

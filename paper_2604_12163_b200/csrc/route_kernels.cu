@@ -771,8 +771,7 @@ __global__ void __launch_bounds__(SB_WARPS * 32)
 ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__ token_flat,
                      float* __restrict__ gate_raw, int16_t* __restrict__ slot_of, int B, int S,
                      int E, int cap, int P, int* __restrict__ cursor,
-                     unsigned long long* __restrict__ tokmask, int32_t* __restrict__ tokrow,
-                     float* __restrict__ tokraw) {
+                     unsigned long long* __restrict__ tokmask, int2* __restrict__ tokent) {
   extern __shared__ __align__(16) uint64_t wsel[];   // [P] winners
   __shared__ int red[2][SB_WARPS][4];
   __shared__ int wcnt[SB_WARPS][2];
@@ -939,8 +938,7 @@ ec_select_blk_kernel(const float* __restrict__ scores_bes, int32_t* __restrict__
     scol[idx] = (int16_t)j;
     if (tokmask) {
       const int64_t tt = (int64_t)b * S + idx;
-      tokrow[tt * E + e] = (int32_t)o;
-      tokraw[tt * E + e] = c[idx];
+      tokent[tt * E + e] = make_int2((int32_t)o, __float_as_int(c[idx]));
       atomicOr(tokmask + tt, 1ull << e);
     }
   }
@@ -1196,12 +1194,12 @@ combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float
     const int nlo = __popc(mlo);
     for (int k = lane; k < cnt; k += 32) {
       const int e = k < nlo ? (int)__fns(mlo, 0, k + 1) : 32 + (int)__fns(mhi, 0, k - nlo + 1);
-      const int32_t r = gf.tokrow[t * E + e];
-      rows[k] = r;
+      const int2 te = gf.tokent[t * E + e];
+      rows[k] = te.x;
 #ifndef NIMG_CB_NO_PREFETCH
-      if (row_bytes % 16 == 0) bulk_prefetch_l2(yr + (int64_t)r * d, row_bytes);
+      if (row_bytes % 16 == 0) bulk_prefetch_l2(yr + (int64_t)te.x * d, row_bytes);
 #endif
-      gl[k] = gf.tokraw[t * E + e];
+      gl[k] = __int_as_float(te.y);
     }
     // (the gate chain itself runs once the first row loads are in flight, below)
   } else {
@@ -1415,8 +1413,7 @@ bool select_blk_path(int S) { return select_warp_enabled() && S <= 4096; }
 
 cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float* gate_raw,
                              int16_t* slot_of, int B, int S, int E, int cap, cudaStream_t s,
-                             int* cursor, unsigned long long* tokmask, int32_t* tokrow,
-                             float* tokraw) {
+                             int* cursor, unsigned long long* tokmask, int2* tokent) {
   if (tokmask && (!select_blk_path(S) || E > 64)) return cudaErrorInvalidValue;
   if (select_blk_path(S)) {
     const int P = next_pow2(cap);
@@ -1428,7 +1425,7 @@ cudaError_t launch_ec_select(const float* scores_bes, int32_t* token_flat, float
       if (e2 != cudaSuccess) return e2;                                                         \
       return launch_pdl(ec_select_blk_kernel<K>, grid, dim3(SB_WARPS * 32), wsmem, s,           \
                         scores_bes, token_flat, gate_raw, slot_of, B, S, E, cap, P, cursor,    \
-                        tokmask, tokrow, tokraw);                                               \
+                        tokmask, tokent);                                                       \
     } while (0)
     if (S <= 256) NIMG_BSEL(2);
     if (S <= 512) NIMG_BSEL(4);
