@@ -1164,8 +1164,15 @@ template <typename T, int VEC> struct VecIO {
 
 // RESID (the backbone's MoE branch, backbone.py:606): instead of the layer
 // output, write h + tanh(ff_gate) * round(layer output) (f64, rounded).
+// Resident blocks per SM the register allocation must allow. The bf16 combine at
+// 3 (80 registers instead of 92: 24 warps per SM instead of 16) measured 90 vs
+// 97-101 us in the cfg2 step; 4 spills (profiles/r02_combine_occupancy_ab.txt).
+// The variants with fp32 rows or output keep 1 (they would spill).
+#ifndef NIMG_CB_MINB
+#define NIMG_CB_MINB 3
+#endif
 template <typename TY, typename TO, int VEC, typename ACC, int UNR, bool RESID>
-__global__ void __launch_bounds__(CB_WARPS * 32)
+__global__ void __launch_bounds__(CB_WARPS * 32, (sizeof(TY) == 2 && sizeof(TO) == 2) ? NIMG_CB_MINB : 1)
 combine_kernel(const TY* __restrict__ yr, const TY* __restrict__ ys, const float* __restrict__ gates,
                const int32_t* __restrict__ comb_rows, const int32_t* __restrict__ comb_cnt,
                TO* __restrict__ out, int64_t T, int d, int E, const TO* __restrict__ hres,
