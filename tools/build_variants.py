@@ -6,7 +6,7 @@ import sys
 sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 from paper_2604_12163_b200 import _build  # noqa: E402
 
-VARIANTS = {"probe1": ("NIMG_BWD_PROBE=1",), "probe2": ("NIMG_BWD_PROBE=2",), "staged": ("NIMG_W_SECTOR=0",), "st128": ("NIMG_ST256=0",), "cbminb1": ("NIMG_CB_MINB=1",), "cbb4m4": ("NIMG_CB_BATCH=4", "NIMG_CB_MINB=4"),
+VARIANTS = {"probe1": ("NIMG_BWD_PROBE=1",), "probe2": ("NIMG_BWD_PROBE=2",), "staged": ("NIMG_W_SECTOR=0",), "st128": ("NIMG_ST256=0",), "cbminb1": ("NIMG_CB_MINB=1",), "d2nostage": ("NIMG_D2_HSTAGE=0",), "cbb4m4": ("NIMG_CB_BATCH=4", "NIMG_CB_MINB=4"),
             "g1bn112": ("NIMG_G1_BN=112",), "b128": ("NIMG_I8_B256=0",),
             "trace": ("NIMG_I8_TRACE=1",), "trace_nomma": ("NIMG_I8_TRACE=1", "NIMG_I8_PROBE=2"),
             "trace_noconv": ("NIMG_I8_TRACE=1", "NIMG_I8_PROBE=1"), "lx3": ("NIMG_I8_LX=3",),
