@@ -190,6 +190,23 @@ int nimg_route(const nimg_moe_desc* desc, const void* x_norm, const void* t_emb,
                const void* w_r, const nimg_route_out* out, void* ws, size_t ws_bytes,
                void* stream);
 
+/* nimg_route for a routing that nimg_combine_routed consumes: router.py:137-143
+ * (the gates) is left to the combine, so no gate kernel runs and gates /
+ * comb_rows / comb_cnt are not written here; per-token expert masks and
+ * (row, raw score) entries stay in ws, which must live until the combine.
+ * Applies when nimg_route_fusable() returns 1 (E <= 64, S <= 4096, fp32 / bf16). */
+int nimg_route_fusable(const nimg_moe_desc* desc);
+int nimg_route_for_combine(const nimg_moe_desc* desc, const void* x_norm, const void* t_emb,
+                           const void* w_r, const nimg_route_out* out, void* ws, size_t ws_bytes,
+                           void* stream);
+/* nimg_combine (hres == NULL) or nimg_combine_residual for a routing made by
+ * nimg_route_for_combine with route_ws: the combine forms every gate
+ * (router.py:137-143, the same bits as nimg_route) and also writes it to gates
+ * (E*B*cap, the routing output). T = B*S of desc. */
+int nimg_combine_routed(const nimg_moe_desc* desc, const void* route_ws, int32_t y_dtype,
+                        int32_t out_dtype, const void* y_routed, const void* y_shared, void* gates,
+                        const void* hres, const void* th_ff, void* out, void* stream);
+
 /* tensor.py:348-363  gather_rows: dst[i,:] = src[idx[i],:] (row_bytes each) */
 int nimg_gather_rows(const void* src, int64_t n_src_rows, int64_t row_bytes, const int32_t* idx,
                      int64_t n_idx, void* dst, void* stream);

@@ -32,6 +32,7 @@ EXPORTS = (
     "nimg_moe_block_prologue_workspace_bytes", "nimg_moe_block_prologue", "nimg_combine_residual",
     "nimg_moe_train_state_bytes", "nimg_moe_forward_train", "nimg_moe_backward_workspace_bytes",
     "nimg_moe_backward", "nimg_route_bg_flags", "nimg_expert_ffn_gather",
+    "nimg_route_fusable", "nimg_route_for_combine", "nimg_combine_routed",
 )
 
 
@@ -136,6 +137,10 @@ def _load():
         "nimg_route_bg_flags": ([C.POINTER(MoeDesc), P, C.POINTER(C.c_void_p)], C.c_int),
         "nimg_expert_ffn_gather": ([C.POINTER(FfnDesc), P, P, P, P, P, P, P, P, P, P, P, P, P, SZ,
                                     C.POINTER(BgGatherDesc), P], C.c_int),
+        "nimg_route_fusable": ([C.POINTER(MoeDesc)], C.c_int),
+        "nimg_route_for_combine": ([C.POINTER(MoeDesc), P, P, P, C.POINTER(RouteOut), P, SZ, P],
+                                   C.c_int),
+        "nimg_combine_routed": ([C.POINTER(MoeDesc), P, I32, I32, P, P, P, P, P, P, P], C.c_int),
     }
     for name in EXPORTS:
         fn = getattr(lib, name)

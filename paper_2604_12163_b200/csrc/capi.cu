@@ -858,6 +858,40 @@ int nimg_route(const nimg_moe_desc* d, const void* x_norm, const void* t_emb, co
   return route_impl(d, x_norm, t_emb, w_r, out, ws, ws_bytes, (cudaStream_t)stream);
 }
 
+// The fused routing form (gates formed in the combine): E <= 64, the block
+// select path, fp32 / bf16 values.
+static bool route_fusable(const nimg_moe_desc* d) {
+  return d && d->act_dtype != NIMG_F64 && d->E <= 64 && select_blk_path((int)d->S);
+}
+int nimg_route_fusable(const nimg_moe_desc* d) {
+  NIMG_TRY(check_moe_desc(d));
+  return route_fusable(d) ? 1 : 0;
+}
+int nimg_route_for_combine(const nimg_moe_desc* d, const void* x_norm, const void* t_emb,
+                           const void* w_r, const nimg_route_out* out, void* ws, size_t ws_bytes,
+                           void* stream) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!route_fusable(d)) return fail(NIMG_ERR_CONFIG, "routing not fusable with the combine (E %lld, S %lld)",
+                                     (long long)d->E, (long long)d->S);
+  return route_impl(d, x_norm, t_emb, w_r, out, ws, ws_bytes, (cudaStream_t)stream, true);
+}
+int nimg_combine_routed(const nimg_moe_desc* d, const void* route_ws, int32_t y_dtype,
+                        int32_t out_dtype, const void* y_routed, const void* y_shared, void* gates,
+                        const void* hres, const void* th_ff, void* out, void* stream) {
+  NIMG_TRY(check_moe_desc(d));
+  if (!route_fusable(d)) return fail(NIMG_ERR_CONFIG, "routing not fusable with the combine");
+  if (!route_ws || !y_shared || !out || !gates || (d->cap > 0 && !y_routed))
+    return fail(NIMG_ERR_SHAPE, "null pointer");
+  if (y_dtype == NIMG_F64 || out_dtype == NIMG_F64) return fail(NIMG_ERR_CONFIG, "f64 combine is not fused");
+  const RouteWs rw = carve_route(d, const_cast<void*>(route_ws));
+  const GateFuse gf{rw.tokmask, rw.tokent, static_cast<float*>(gates), d->gate_eps, d->gate_scale};
+  const int64_t T = d->B * d->S;
+  CUDA_TRY(launch_combine(y_dtype == NIMG_BF16, out_dtype == NIMG_BF16, y_routed, y_shared, nullptr,
+                          nullptr, nullptr, out, T, (int)d->d, (int)d->E, (cudaStream_t)stream, hres,
+                          th_ff, (int)d->S, nullptr, &gf));
+  return NIMG_OK;
+}
+
 int nimg_gather_rows(const void* src, int64_t n_src_rows, int64_t row_bytes, const int32_t* idx,
                      int64_t n_idx, void* dst, void* stream) {
   if (n_idx < 0 || row_bytes < 0 || n_src_rows < 0) return fail(NIMG_ERR_SHAPE, "negative size");

@@ -67,6 +67,9 @@ _BG_GATHER = _os.environ.get("NIMG_EP_BG_GATHER", "0") == "1"
 # NIMG_EP_OWN_BG=1: only the rank's own chunk is gathered on the first grouped
 # launch's background warps; the remote chunks by the gather kernel first
 _BG_OWN = _os.environ.get("NIMG_EP_OWN_BG", "0") == "1"
+# the rank-local combine forms the gates (no gate kernel; nimg_route_for_combine
+# / nimg_combine_routed); NIMG_EP_FUSE_GATES=0 keeps the gate kernel
+_FUSE_GATES = _os.environ.get("NIMG_EP_FUSE_GATES", "1") != "0"
 _MAX_CHUNKS = 64
 
 
@@ -398,7 +401,7 @@ def ep_moe_forward(x_norm, x_mod, t_emb, cfg: RouterConfig, bank_local: ExpertBa
     w = bank_local
 
     _mark(timeline, "start")
-    r = stages.route(x_norm, t_emb, w_r, cfg, cap)
+    r = stages.route(x_norm, t_emb, w_r, cfg, cap, for_combine=_FUSE_GATES)
     _mark(timeline, "routed")
     xring = None
     bg = None

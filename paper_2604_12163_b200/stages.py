@@ -24,8 +24,12 @@ class CudaStages:
     name = "cuda"
 
     def route(self, x_norm: torch.Tensor, t_emb: torch.Tensor, w_r: torch.Tensor,
-              cfg: RouterConfig, cap: int) -> dict:
-        """router.py:104-162 on (B,S,d) x_norm; returns the device routing dict."""
+              cfg: RouterConfig, cap: int, for_combine: bool = False) -> dict:
+        """router.py:104-162 on (B,S,d) x_norm; returns the device routing dict.
+        for_combine: when the shape allows it (nimg_route_fusable), the gates
+        are left to combine() (nimg_route_for_combine / nimg_combine_routed):
+        no gate kernel, and gates / comb_rows / comb_cnt are valid only after
+        combine() ran."""
         B, S, d = x_norm.shape
         desc = make_desc(B, S, d, cfg.n_experts, cap, 1, 1, cfg, x_norm.dtype)
         nbytes = C.c_size_t()
@@ -33,9 +37,12 @@ class CudaStages:
         ws = workspace(nbytes.value)
         r = alloc_route_out(B, S, cfg.n_experts, cap, x_norm.device)
         ro = route_struct(r)
-        _lib.check(_lib.lib.nimg_route(C.byref(desc), ptr(x_norm), ptr(t_emb), ptr(w_r),
-                                       C.byref(ro), ptr(ws), ws.numel(), stream_handle()))
+        fused = for_combine and _lib.lib.nimg_route_fusable(C.byref(desc)) == 1
+        fn = _lib.lib.nimg_route_for_combine if fused else _lib.lib.nimg_route
+        _lib.check(fn(C.byref(desc), ptr(x_norm), ptr(t_emb), ptr(w_r), C.byref(ro), ptr(ws),
+                      ws.numel(), stream_handle()))
         r["_route_ws"], r["_route_desc"] = ws, desc   # bg_flags() points into ws
+        r["_fused"] = fused
         return r
 
     def bg_flags(self, r: dict) -> int:
@@ -122,6 +129,14 @@ class CudaStages:
         T, d = y_shared.shape
         E = r["comb_rows"].shape[1]
         out = torch.empty((T, d), dtype=out_dtype, device=y_shared.device)
+        if r.get("_fused"):   # the gates are formed here (nimg_route_for_combine routing)
+            h, th = residual if residual is not None else (None, None)
+            _lib.check(_lib.lib.nimg_combine_routed(
+                C.byref(r["_route_desc"]), ptr(r["_route_ws"]), nimg_dtype(y_shared.dtype),
+                nimg_dtype(out_dtype), ptr(y_routed) if y_routed is not None else None,
+                ptr(y_shared), ptr(r["gates"]), ptr(h) if h is not None else None,
+                ptr(th) if th is not None else None, ptr(out), stream_handle()))
+            return out
         if residual is None:
             _lib.check(_lib.lib.nimg_combine(T, d, E, nimg_dtype(y_shared.dtype),
                                              nimg_dtype(out_dtype), ptr(y_routed), ptr(y_shared),

@@ -14,7 +14,7 @@ from oracle import nimg_oracle as O
 class OracleStages:
     name = "oracle-cpu"
 
-    def route(self, x_norm, t_emb, w_r, cfg, cap):
+    def route(self, x_norm, t_emb, w_r, cfg, cap, for_combine=False):
         r = O.route_full(x_norm.numpy(), t_emb.numpy(), w_r.numpy(), n_experts=cfg.n_experts,
                          capacity_factor=cfg.capacity_factor, gate_scale=cfg.gate_scale,
                          gate_eps=cfg.gate_eps)
